@@ -1,0 +1,259 @@
+"""Workload records for BASELINE.json configs 0-4 and their reduced test variants.
+
+Everything here is a *parameter* of a run (geometry, material, drive, seeds), as
+listed in BASELINE.json ``configs`` and fixed where the configs are silent by the
+readings in DESIGN.md section "Readings" (R-numbers).  Units are SI throughout.
+
+Record layout (plain dicts / numpy arrays, no method arithmetic):
+
+``boxes``      list of {origin[3], extent[3], nel[3], degree, c, rho, bc[6]}
+               bc order: -x, +x, -y, +y, -z, +z  (BC_RIGID / BC_ABSORBING / BC_INTERFACE)
+``interface``  None or {fine_box, coarse_box, alpha}
+``pmut``       None or {box, face, centers[n,2], side, mode_mn[M,2], freq_hz[n,M],
+               modal_mass[M], damping[M], eta[M], rx, t_switch, capacitance,
+               amp_v, f0_hz, n_cycles, delay_s[n]}
+``plane_wave`` None or {box, face, amp_pa, f0_hz, sigma_s, t0_s, direction[3]}
+``dt``, ``n_steps``, ``coupling`` ('predicted' | 'literal'), ``seed``
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+BC_RIGID, BC_ABSORBING, BC_INTERFACE = 0, 1, 2
+FACE_NAMES = ("-x", "+x", "-y", "+y", "-z", "+z")
+
+UM = 1e-6
+C_WATER, RHO_WATER = 1500.0, 1000.0
+
+# BASELINE.json config 0: PMUT element parameters shared by all configs.
+MEMBRANE_SIDE = 100 * UM
+PITCH = 150 * UM
+MODES_3 = ((1, 1), (1, 3), (3, 1))
+FREQS_3 = (3.0e6, 15.0e6, 15.0e6)
+# config 3: six modes.  Shapes for modes 5-6 are reading R15.
+MODES_6 = ((1, 1), (1, 3), (3, 1), (3, 3), (1, 5), (5, 1))
+FREQS_6 = (3.0e6, 15.0e6, 15.0e6, 27.0e6, 33.0e6, 33.0e6)
+MODAL_MASS = 1e-10      # kg
+DAMPING = 0.01
+ETA = 1e-6              # N/V (= C/m)
+DRIVE_V, DRIVE_F0, DRIVE_CYCLES = 5.0, 3.0e6, 3
+CFL = 0.3
+STEER_DEG = 20.0        # reading R11 (linear steering angle, configs 1-2)
+RX_CAPACITANCE = 1e-10  # reading R14
+PENALTY_ALPHA = 10.0    # config 2: "penalty coefficient 10*N^2/h"
+
+
+def _box(origin, extent, nel, degree, bc, c=C_WATER, rho=RHO_WATER):
+    return {"origin": tuple(float(v) for v in origin), "extent": tuple(float(v) for v in extent),
+            "nel": tuple(int(v) for v in nel), "degree": int(degree), "c": float(c),
+            "rho": float(rho), "bc": list(bc)}
+
+
+def cfl_dt(boxes, cfl=CFL):
+    """Reading R8: dt = cfl * min_box h_min / (c N^2)."""
+    best = math.inf
+    for b in boxes:
+        h = min(e / n for e, n in zip(b["extent"], b["nel"]))
+        best = min(best, h / (b["c"] * b["degree"] ** 2))
+    return cfl * best
+
+
+def _scatter(n_pmut, seed, rel=0.01):
+    """Reading R16: one N(0,1) draw per PMUT (row-major, x fastest), applied to all its modes."""
+    return 1.0 + rel * np.random.default_rng(seed).standard_normal(n_pmut)
+
+
+def _grid_centers(n_side, pitch, offset):
+    c = offset + pitch * np.arange(n_side)
+    xx, yy = np.meshgrid(c, c, indexing="xy")       # x fastest in the flattened order
+    return np.stack([xx.ravel(), yy.ravel()], axis=1)
+
+
+def _pmut(centers, modes, freqs, scatter, delay, *, rx=False, amp=DRIVE_V, box=0, face=4):
+    n = len(centers)
+    m = len(modes)
+    f = np.asarray(freqs, float)[None, :] * (np.ones(n) if scatter is None else scatter)[:, None]
+    return {"box": box, "face": face, "centers": np.asarray(centers, float).reshape(n, 2),
+            "side": MEMBRANE_SIDE, "mode_mn": np.asarray(modes, np.int32).reshape(m, 2),
+            "freq_hz": f, "modal_mass": np.full(m, MODAL_MASS), "damping": np.full(m, DAMPING),
+            "eta": np.full(m, ETA), "rx": bool(rx), "t_switch": 0.0 if rx else math.inf,
+            "capacitance": RX_CAPACITANCE, "amp_v": 0.0 if rx else amp, "f0_hz": DRIVE_F0,
+            "n_cycles": DRIVE_CYCLES, "delay_s": np.asarray(delay, float).reshape(n)}
+
+
+def _steer_delay(centers, c=C_WATER, deg=STEER_DEG):
+    """Reading R11: tau_k = (x_k - min x) sin(theta) / c."""
+    x = centers[:, 0]
+    return (x - x.min()) * math.sin(math.radians(deg)) / c
+
+
+def _focus_delay(centers, focus, c=C_WATER):
+    """Reading R12: tau_k = (max_j |x_j - F| - |x_k - F|) / c (farthest element fires first)."""
+    pts = np.concatenate([centers, np.zeros((len(centers), 1))], axis=1)
+    d = np.linalg.norm(pts - np.asarray(focus)[None, :], axis=1)
+    return (d.max() - d) / c
+
+
+def _two_box(n_side, fine_nz, coarse_nz, *, nf=5, nc=3, hf=25 * UM):
+    """Configs 2-4 layout (reading R17/R18): fine N=5 primary z in [0, fine_nz*hf],
+    coarse N=3 secondary above it, lateral size n_side * pitch, 2:1 in h."""
+    L = n_side * PITCH
+    nfx = int(round(L / hf))
+    hc = 2 * hf
+    fine = _box((0, 0, 0), (L, L, fine_nz * hf), (nfx, nfx, fine_nz), nf,
+                [BC_RIGID] * 4 + [BC_RIGID, BC_INTERFACE])
+    coarse = _box((0, 0, fine_nz * hf), (L, L, coarse_nz * hc), (nfx // 2, nfx // 2, coarse_nz), nc,
+                  [BC_RIGID] * 4 + [BC_INTERFACE, BC_ABSORBING])
+    return [fine, coarse]
+
+
+def _finish(rec):
+    rec.setdefault("interface", None)
+    rec.setdefault("pmut", None)
+    rec.setdefault("plane_wave", None)
+    rec.setdefault("coupling", "predicted")
+    rec["dt"] = cfl_dt(rec["boxes"]) if rec.get("dt") is None else float(rec["dt"])
+    return rec
+
+
+def _plane_wave(box, *, amp=1e3, f0=3.0e6, deg=20.0):
+    """Reading R13: Gaussian-modulated sine s(tau)=exp(-(tau-t0)^2/(2 sigma^2)) sin(2 pi f0 (tau-t0)),
+    sigma = 1/(2 f0), t0 = 4 sigma, direction (sin th, 0, -cos th), entering through +z of ``box``."""
+    sigma = 1.0 / (2.0 * f0)
+    th = math.radians(deg)
+    return {"box": box, "face": 5, "amp_pa": amp, "f0_hz": f0, "sigma_s": sigma, "t0_s": 4 * sigma,
+            "direction": (math.sin(th), 0.0, -math.cos(th))}
+
+
+def config(i: int, **over):
+    """BASELINE.json configs[i] as a workload record."""
+    if i == 0:
+        boxes = [_box((0, 0, 0), (600 * UM,) * 3, (4, 4, 4), 4, [BC_RIGID] * 5 + [BC_ABSORBING])]
+        pm = _pmut([[300 * UM, 300 * UM]], MODES_3, FREQS_3, None, [0.0])
+        rec = {"name": "cfg0", "boxes": boxes, "pmut": pm, "n_steps": 400, "seed": 0}
+    elif i == 1:
+        boxes = [_box((0, 0, 0), (900 * UM, 900 * UM, 1200 * UM), (24, 24, 32), 4,
+                      [BC_RIGID] * 5 + [BC_ABSORBING])]
+        cen = _grid_centers(4, PITCH, 225 * UM)
+        pm = _pmut(cen, MODES_3, FREQS_3, _scatter(16, 0), _steer_delay(cen))
+        rec = {"name": "cfg1", "boxes": boxes, "pmut": pm, "n_steps": 2000, "seed": 0}
+    elif i == 2:
+        boxes = _two_box(16, 24, 80)
+        cen = _grid_centers(16, PITCH, 75 * UM)
+        pm = _pmut(cen, MODES_3, FREQS_3, _scatter(256, 0), _steer_delay(cen))
+        rec = {"name": "cfg2", "boxes": boxes, "pmut": pm, "n_steps": 3000, "seed": 0,
+               "interface": {"fine_box": 0, "coarse_box": 1, "alpha": PENALTY_ALPHA}}
+    elif i == 3:
+        boxes = _two_box(64, 24, 80)
+        cen = _grid_centers(64, PITCH, 75 * UM)
+        focus = (4.8e-3, 4.8e-3, 4.0e-3)
+        pm = _pmut(cen, MODES_6, FREQS_6, _scatter(4096, 0), _focus_delay(cen, focus))
+        rec = {"name": "cfg3", "boxes": boxes, "pmut": pm, "n_steps": 2000, "seed": 0,
+               "interface": {"fine_box": 0, "coarse_box": 1, "alpha": PENALTY_ALPHA}}
+    elif i == 4:
+        boxes = _two_box(32, 24, 80)
+        cen = _grid_centers(32, PITCH, 75 * UM)
+        pm = _pmut(cen, MODES_3, FREQS_3, _scatter(1024, 4), np.zeros(1024), rx=True)
+        rec = {"name": "cfg4", "boxes": boxes, "pmut": pm, "n_steps": 4000, "seed": 4,
+               "interface": {"fine_box": 0, "coarse_box": 1, "alpha": PENALTY_ALPHA},
+               "plane_wave": _plane_wave(1)}
+    else:
+        raise ValueError(f"no config {i}")
+    rec.update(over)
+    return _finish(rec)
+
+
+def config_names():
+    return [f"cfg{i}" for i in range(5)]
+
+
+def small_config(name: str, **over):
+    """Reduced variants with the structure of configs 1-4 (same N, h, interface, PMUT physics)
+    at sizes the oracle finishes in seconds.  Used by parity tests only."""
+    if name == "cfg1s":   # config 1 physics, 2x2 array, N=4, h=37.5um, unaligned membranes
+        boxes = [_box((0, 0, 0), (450 * UM, 450 * UM, 300 * UM), (12, 12, 8), 4,
+                      [BC_RIGID] * 5 + [BC_ABSORBING])]
+        cen = _grid_centers(2, PITCH, 150 * UM)
+        pm = _pmut(cen, MODES_3, FREQS_3, _scatter(4, 0), _steer_delay(cen))
+        rec = {"name": name, "boxes": boxes, "pmut": pm, "n_steps": 300, "seed": 0}
+    elif name == "cfg2s":  # config 2 layout, 2x2 array, N5/N3 2:1 interface
+        boxes = _two_box(2, 4, 4)
+        cen = _grid_centers(2, PITCH, 75 * UM)
+        pm = _pmut(cen, MODES_3, FREQS_3, _scatter(4, 0), _steer_delay(cen))
+        rec = {"name": name, "boxes": boxes, "pmut": pm, "n_steps": 300, "seed": 0,
+               "interface": {"fine_box": 0, "coarse_box": 1, "alpha": PENALTY_ALPHA}}
+    elif name == "cfg3s":  # config 3 physics: 6 modes, focus law
+        boxes = _two_box(2, 4, 4)
+        cen = _grid_centers(2, PITCH, 75 * UM)
+        focus = (150 * UM, 150 * UM, 4.0e-3)
+        pm = _pmut(cen, MODES_6, FREQS_6, _scatter(4, 0), _focus_delay(cen, focus))
+        rec = {"name": name, "boxes": boxes, "pmut": pm, "n_steps": 300, "seed": 0,
+               "interface": {"fine_box": 0, "coarse_box": 1, "alpha": PENALTY_ALPHA}}
+    elif name == "cfg4s":  # config 4 physics: RX feedback + plane-wave boundary source
+        boxes = _two_box(2, 4, 3)
+        cen = _grid_centers(2, PITCH, 75 * UM)
+        pm = _pmut(cen, MODES_3, FREQS_3, _scatter(4, 4), np.zeros(4), rx=True)
+        pw = _plane_wave(1)
+        pw["t0_s"] = 0.0  # pulse centred at t=0 so the short run sees the full waveform's rise
+        rec = {"name": name, "boxes": boxes, "pmut": pm, "n_steps": 400, "seed": 4,
+               "interface": {"fine_box": 0, "coarse_box": 1, "alpha": PENALTY_ALPHA},
+               "plane_wave": pw}
+    else:
+        raise ValueError(f"no small config {name}")
+    rec.update(over)
+    return _finish(rec)
+
+
+def small_config_names():
+    return ["cfg1s", "cfg2s", "cfg3s", "cfg4s"]
+
+
+def cavity_config(nel=(3, 3, 3), degree=4, extent=(1e-3, 1e-3, 1e-3), c=C_WATER, n_steps=100, cfl=0.3):
+    """Closed rigid box, no PMUT, no ABC: for cavity eigenmode and energy pins."""
+    boxes = [_box((0, 0, 0), extent, nel, degree, [BC_RIGID] * 6, c=c)]
+    rec = {"name": "cavity", "boxes": boxes, "n_steps": n_steps, "seed": 0}
+    rec["dt"] = cfl_dt(boxes, cfl)
+    return _finish(rec)
+
+
+def conforming_cut_config(nel_xy=3, nz_lo=2, nz_hi=2, degree=4, h=1e-4 / 3, alpha=PENALTY_ALPHA,
+                          n_steps=100, cfl=0.3, ratio=1, degree_hi=None, bc_top=BC_RIGID):
+    """Two boxes stacked in z with a DG interface between them.  ratio=1 and degree_hi=None gives
+    a conforming mesh cut by the interface (pin: equals the single CG box up to discretisation)."""
+    dh = degree if degree_hi is None else degree_hi
+    lo = _box((0, 0, 0), (nel_xy * h, nel_xy * h, nz_lo * h), (nel_xy, nel_xy, nz_lo), degree,
+              [BC_RIGID] * 5 + [BC_INTERFACE])
+    hh = ratio * h
+    hi = _box((0, 0, nz_lo * h), (nel_xy * h, nel_xy * h, nz_hi * hh),
+              (nel_xy // ratio, nel_xy // ratio, nz_hi), dh, [BC_RIGID] * 4 + [BC_INTERFACE, bc_top])
+    rec = {"name": "cut", "boxes": [lo, hi], "n_steps": n_steps, "seed": 0,
+           "interface": {"fine_box": 0, "coarse_box": 1, "alpha": alpha}}
+    rec["dt"] = cfl_dt(rec["boxes"], cfl)
+    return _finish(rec)
+
+
+def n_nodes(box):
+    return tuple(box["degree"] * n + 1 for n in box["nel"])
+
+
+def box_dof(box):
+    nx, ny, nz = n_nodes(box)
+    return nx * ny * nz
+
+
+def total_dof(rec):
+    return sum(box_dof(b) for b in rec["boxes"])
+
+
+def random_state(rec, seed=1234, scale_v=None):
+    """Seeded random (p, pdot) per box for operator-level tests (lexicographic x-fastest)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for b in rec["boxes"]:
+        n = box_dof(b)
+        p = rng.standard_normal(n)
+        v = rng.standard_normal(n) * (1.0 / rec["dt"] * 1e-3 if scale_v is None else scale_v)
+        out.append((p, v))
+    return out
