@@ -1,0 +1,180 @@
+/*
+ * sem.h -- C ABI of libsem: one explicit leapfrog time step of the coupled PMUT-array /
+ * DG-SEM acoustic model of arxiv 2603.06267, in FP64 on NVIDIA B200 (sm_100a).
+ *
+ * Citations are PAPER.md lines (P:L<n>), equations in the paper's LaTeX order, and the
+ * readings R<n> listed in DESIGN.md.  All quantities are SI.
+ *
+ * Problem (Eqs. 9-12):   M p'' + K p + C p' = f(q'')      (acoustic, DG-SEM)
+ *                                     q'' + W q = g(p, phi)            (PMUT modal ROM)
+ * advanced by Algorithm 1 (Newmark gamma = 1/2, beta = 0 == leapfrog) with the
+ * coupling time level of reading R2 (default: the PMUT solve consumes the acoustic predictor).
+ *
+ * Conventions (all entry points):
+ *  - Host arrays passed in are owned by the caller and copied before the call returns.
+ *  - The context owns every device allocation it makes (cudaMalloc on ctx->device).
+ *  - Every call returns a sem_status; no C++ exception crosses the ABI.  On error the
+ *    context's message is available from sem_last_error(ctx) (NULL-safe).
+ *  - sem_step only enqueues work on the context stream; asynchronous CUDA errors surface at
+ *    the next synchronising call (sem_read_*, sem_sync, sem_query).
+ *  - One context per rank / device; a context is not thread-safe.
+ *  - Node layout of every acoustic field (input and output): per box, lexicographic over the
+ *    GLL lattice, x fastest:  id = gx + NX (gy + NY gz),  NX = N nel_x + 1 (P:L413-420,
+ *    continuous inside a box, discontinuous across the DG interface).
+ */
+#ifndef SEM_H
+#define SEM_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sem_ctx sem_ctx;   /* opaque: device state of one rank */
+
+typedef enum {
+    SEM_OK = 0,
+    SEM_E_ARG = -1,        /* invalid argument (degree outside 1..8, overlapping membranes, C <= 0, ...) */
+    SEM_E_CUDA = -2,       /* CUDA runtime error (message holds cudaGetErrorString) */
+    SEM_E_NCCL = -3,       /* NCCL error in the slab halo exchange */
+    SEM_E_STATE = -4,      /* call out of order (e.g. interface built twice, step before setup) */
+    SEM_E_NONFINITE = -5,  /* NaN/Inf detected (SEM_F_NAN_CHECK); message names the step */
+    SEM_E_PARTITION = -6,  /* slab cut not element- / 2:1- / membrane-aligned */
+    SEM_E_UNMATCHED = -7,  /* interface quadrature point without a coarse owner */
+    SEM_E_OOM = -8         /* device allocation failed */
+} sem_status;
+
+/* Boundary condition of each box face, order -x, +x, -y, +y, -z, +z. */
+typedef enum {
+    SEM_BC_RIGID = 0,      /* hard wall, homogeneous Neumann (natural; no work)               */
+    SEM_BC_ABSORBING = 1,  /* first-order ABC, d(w, v) = int_F c w v (Eq. 8)      */
+    SEM_BC_INTERFACE = 2   /* DG interface Gamma_I, set up by sem_dg_interface_build (Eq. 7)  */
+} sem_bc;
+
+/* Coupling time level of the PMUT solve (reading R2). */
+enum {
+    SEM_F_COUPLING_LITERAL = 1 << 0, /* g(p^n, phi^n) exactly as printed (unstable at cfg masses)  */
+    SEM_F_NAN_CHECK = 1 << 1,        /* check p for NaN/Inf after every sem_step call              */
+    SEM_F_NO_GRAPH = 1 << 2          /* launch kernels directly instead of a captured CUDA graph   */
+};
+
+/* One axis-aligned box of hexahedral GLL elements of degree `degree` (1..8). */
+typedef struct {
+    double origin[3];      /* lower corner [m]                                      */
+    double extent[3];      /* edge lengths [m]                                      */
+    int nel[3];            /* elements per axis (>= 1)                              */
+    int degree;            /* GLL degree N (1..8); (N+1)^3 nodes per element        */
+    double c;              /* sound speed [m/s] (> 0)                               */
+    double rho;            /* density [kg/m^3] (>= 0); kappa = rho c^2     */
+    int bc[6];             /* sem_bc per face                                       */
+} sem_box_desc;
+
+typedef struct {
+    int n_boxes;                 /* 1 or 2                                               */
+    const sem_box_desc* boxes;   /* [n_boxes]                                            */
+    double dt;                   /* time step [s], caller-computed (reading R8)          */
+    int device;                  /* CUDA device ordinal                                  */
+    void* stream;                /* cudaStream_t to enqueue on; NULL -> library stream   */
+    int rank, world;             /* slab decomposition along x; world == 1 -> no NCCL    */
+    const void* nccl_unique_id;  /* ncclUniqueId (128 bytes) when world > 1, else NULL  */
+    int flags;                   /* SEM_F_*                                              */
+} sem_mesh_desc;
+
+/* Create the context: validates boxes, builds the 1D GLL tables and allocates p (two time
+ * levels), w = p' + dt/2 p'' (one level) per box, zero-initialised.
+ * Errors: SEM_E_ARG (bad descriptor), SEM_E_PARTITION (world > 1 and nel_x not divisible),
+ * SEM_E_CUDA / SEM_E_OOM.  *out is NULL on error. */
+sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out);
+
+/* PMUT array on face `face` (only 4 = -z) of box `box` (Eqs. 2-3, 5, 11-12).
+ * Mode shapes S_{k,m}(x,y) = sin(m pi x'/a) sin(n pi y'/a) on the square membrane of side a
+ * centred at center[k] (reading R19); U.n = -S (reading R4).  Modal ODE (reading R3):
+ *   q'' = -w^2 q - 2 zeta w q'* + (int_gamma_k p U.n + eta phi) / M_m,   w = 2 pi freq_hz.
+ * phi_k = TX Hann burst amp_v sin(2 pi f0 t')(1 - cos(2 pi f0 t'/n_cycles))/2, t' = t - delay_s[k]
+ * in [0, n_cycles/f0] (reading R10) for t <= t_switch; (1/C) sum_m eta_m q_m after (Eq. 3).
+ * Arrays: center [n_pmut*2] (x, y), mode_mn [n_modes*2], freq_hz [n_pmut*n_modes] (k-major),
+ * modal_mass / damping_ratio / eta [n_modes], delay_s [n_pmut].  n_modes <= 8.
+ * Errors: SEM_E_ARG (membranes overlapping or off the face, zero-node membrane, rx with C <= 0),
+ * SEM_E_STATE (already attached). */
+typedef struct {
+    int box, face;
+    int n_pmut, n_modes;
+    const double* center;
+    double side;
+    const int* mode_mn;
+    const double* freq_hz;
+    const double* modal_mass;
+    const double* damping_ratio;
+    const double* eta;
+    int rx;                       /* 1: open-circuit RX feedback for t > t_switch        */
+    double t_switch;              /* t_bar [s]; +inf for pure TX                */
+    double capacitance;           /* C [F]                                               */
+    double amp_v, f0_hz;          /* TX burst amplitude [V] and carrier [Hz]             */
+    int n_cycles;
+    const double* delay_s;
+} sem_pmut_desc;
+sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pm);
+
+/* Non-conforming SIPG interface between the +z face of `fine_box` and the -z face of
+ * `coarse_box` (Eq. 7's three Gamma_I sums), gamma_F = penalty_alpha cbar^2
+ * max(N+, N-)^2 / min(h+, h-) with cbar the harmonic mean of c (reading R7).
+ * quad_rule 0 = fine-face GLL nodes (reading R9; the only rule implemented).
+ * Requires matching lateral extents and h_coarse = R h_fine for an integer R >= 1.
+ * Errors: SEM_E_ARG (geometry), SEM_E_UNMATCHED (lattices do not nest), SEM_E_STATE. */
+sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, double penalty_alpha,
+                                  int quad_rule);
+
+/* Incident plane wave entering through absorbing face `face` (only 5 = +z) of `box`
+ * (reading R13): p_inc = amp s(t - k.(x - x_ref)/c), s(u) = exp(-(u-t0)^2/(2 sigma^2))
+ * sin(2 pi f0 (u-t0)), imposed as total-field first-order ABC data
+ * b_j = int c amp s'(tau) (1 - n.k) psi_j.  dir is the unit propagation direction k. */
+sem_status sem_plane_wave_source(sem_ctx* ctx, int box, int face, double amp_pa, double f0_hz,
+                                 double sigma_s, double t0_s, const double dir[3]);
+
+/* Advance n_steps iterations of Algorithm 1 (async on the context stream). */
+sem_status sem_step(sem_ctx* ctx, int n_steps);
+
+/* Block until all enqueued work finished; reports asynchronous errors. */
+sem_status sem_sync(sem_ctx* ctx);
+
+/* p^S of box `box` after S steps into host[n] (n must equal the box's node count).
+ * Synchronising.  Shared DG interface nodes are reported once per side. */
+sem_status sem_read_pressure(sem_ctx* ctx, int box, double* host, size_t n);
+
+/* p^S at n sampled node ids (layout above) of `box` into out[n] (host).  Synchronising. */
+sem_status sem_read_pressure_at(sem_ctx* ctx, int box, const long long* ids, size_t n, double* out);
+
+/* q^S, q'^S [n_pmut*n_modes] and phi_k(t^S) [n_pmut] (received voltage for RX, drive for TX).
+ * n must equal n_pmut*n_modes.  Any pointer may be NULL.  Synchronising. */
+sem_status sem_read_modal(sem_ctx* ctx, double* q, double* qdot, double* v_rx, size_t n);
+
+/* Test hook: set p^0, p'^0 of `box` from host arrays [n] (p''^0 = 0; reading R20),
+ * modal state and step counter reset to zero for every box's first call. */
+sem_status sem_write_state(sem_ctx* ctx, int box, const double* p, const double* pdot, size_t n);
+
+/* Test hook: fill p^0 = p_scale u(seed, box, 0, id), p'^0 = v_scale u(seed, box, 1, id) on the
+ * device with the counter-based generator u in [-1, 1) documented in DESIGN.md (splitmix64);
+ * p''^0 = 0, modal state and step counter reset. */
+sem_status sem_fill_random_state(sem_ctx* ctx, int box, unsigned long long seed, double p_scale,
+                                 double v_scale);
+
+/* Total acoustic node count over all boxes of this rank, steps taken, and t = steps * dt. */
+sem_status sem_query(sem_ctx* ctx, long long* n_dof, long long* step, double* t);
+
+/* Per-kernel device time [ms] accumulated since the last reset while SEM_F_NO_GRAPH profiling
+ * is enabled (sem_set_profiling).  which: 0 = volume (all boxes), 1 = interface, 2 = modal.
+ * n_launches receives the number of launches timed. */
+sem_status sem_set_profiling(sem_ctx* ctx, int on);
+sem_status sem_kernel_time(sem_ctx* ctx, int which, double* ms, long long* n_launches);
+
+/* Number of kernel launches issued by the last sem_step call (graph nodes counted). */
+sem_status sem_last_launch_count(sem_ctx* ctx, long long* n);
+
+const char* sem_last_error(const sem_ctx* ctx);
+void sem_destroy(sem_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEM_H */

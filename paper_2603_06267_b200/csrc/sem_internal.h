@@ -1,0 +1,200 @@
+// Internal declarations of libsem (host setup <-> kernels).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sem.h"
+
+namespace sem {
+
+constexpr int kMaxN = 8;          // supported GLL degrees 1..8
+constexpr int kRows = kMaxN + 3;  // row classes per direction: R[0..N-1], L, B0, BN
+constexpr int kMaxModes = 8;
+constexpr int kTX = 32;           // volume kernel tile width in x (one warp)
+
+// Row-class indices inside a direction table.
+//   R[a]  interior node with local index a (a = 0: shared, right element), base = i - a
+//   L     interior shared node (a = 0), left element, base = i - N
+//   B0    box lower boundary node (i = 0), right element only
+//   BN    box upper boundary node (i = N nel), left element only
+__host__ __device__ inline int row_L(int N) { return N; }
+__host__ __device__ inline int row_B0(int N) { return N + 1; }
+__host__ __device__ inline int row_BN(int N) { return N + 2; }
+
+// Per-box coefficient tables, passed by value inside VolParams (kernel parameter constant bank,
+// per launch: contexts never share them).
+struct BoxTables {
+    // G[d][row][b] = c^2 (2/h_d)^2 A_hat[a][b] / w_asm(a)   (M^-1 K restricted to direction d)
+    double G[3][kRows][kMaxN + 1];
+    // interface layer coefficients: a -= tau * ktau[c] + sigma * ksig[c] on the element layer
+    // adjacent to the interface (c = local index across that layer, 0..N)
+    double ksig[kMaxN + 1];
+    double ktau[kMaxN + 1];
+};
+
+struct VolParams {
+    BoxTables tab;
+    const double* __restrict__ P;   // p^{n+1}
+    double* __restrict__ Pn;        // p^{n+2} (output)
+    double* __restrict__ W;         // w^n in, w^{n+1} out (in place)
+    long long NX, NY, NZ;           // node counts of the (local) box
+    int nelz;
+    double dt;
+    // lumped ABC: C_ii / M_ii at boundary nodes of absorbing faces (0 if rigid)
+    double damp[6];
+    // PMUT forcing plane on z = 0 (F = kappa sum_m qdd S), scaled by kF = 1 / m_z(0)
+    const double* __restrict__ F;
+    double kF;
+    // DG interface layer: side = +1 (this box's +z face is Gamma_I, fine side),
+    // -1 (its -z face, coarse side), 0 none; tau / sigma on the face lattice [NX*NY]
+    int iface_side;
+    const double* __restrict__ tau;
+    const double* __restrict__ sig;
+    // plane-wave boundary source on the +z face (reading R13)
+    int pw_on;
+    double pw_fac;                  // c A (1 - n.k) / m_z(top)
+    double pw_k[3], pw_xref[3], pw_c, pw_t0, pw_sigma, pw_om, pw_ztop;
+    const double* __restrict__ xc; // node x coordinates [NX]
+    const double* __restrict__ yc; // node y coordinates [NY]
+    // step bookkeeping (device): t^{n+1} = (step + 1) dt; last block increments step
+    long long* step;
+    unsigned int* done;
+    unsigned int total_blocks;
+    int bump_step;                  // 1 for the last volume launch of a step
+};
+
+struct ModalParams {
+    int n_pmut, n_modes, lmax;      // lmax = stride of the per-pmut 1D tables
+    int literal;
+    double dt;
+    const double* __restrict__ P;   // plane z = 0 of the PMUT box (p^{n+1} or p^n if literal)
+    long long NX;
+    const int* __restrict__ rect;   // [k][4] = i0, j0, ni, nj
+    const double* __restrict__ sx;  // [k][m][lmax] S factors along x (unweighted)
+    const double* __restrict__ sy;
+    const double* __restrict__ wx;  // [k][lmax] face mass factors m_x(i)
+    const double* __restrict__ wy;
+    const double* __restrict__ omega2;   // [k][m]
+    const double* __restrict__ twozw;    // [k][m]  2 zeta omega
+    const double* __restrict__ invmass;  // [m]
+    const double* __restrict__ eta;      // [m]
+    const double* __restrict__ delay;    // [k]
+    double amp, om0, ncyc, t_end, t_switch, invC;
+    int rx;
+    double kappa;
+    double* __restrict__ q;
+    double* __restrict__ qd;
+    double* __restrict__ qdd;
+    double* __restrict__ phi;       // phi_k(t^{n+1}, q^{n+1}) for readout
+    double* __restrict__ F;         // force plane [NX*NY]
+    const long long* step;
+};
+
+struct IfaceParams {
+    const double* __restrict__ Pf;  // fine box p^{n+1}
+    const double* __restrict__ Pc;  // coarse box p^{n+1}
+    long long NXf, NYf, NZf, NXc, NYc;
+    int Nf, Nc, R, nelcx, nelcy;
+    double gamma, cf2, cc2;
+    double dfT[kMaxN + 1];          // (2/h_f) D_f[N_f][c]: d/dz at the fine top face
+    double dcB[kMaxN + 1];          // (2/h_c) D_c[0][c]: d/dz at the coarse bottom face
+    const double* __restrict__ I;   // [(Nf R + 1)][(Nc + 1)] coarse basis at fine lattice points
+    const double* __restrict__ mxf; // [NXf] fine face mass factors
+    const double* __restrict__ myf;
+    const double* __restrict__ mxc; // [NXc]
+    const double* __restrict__ myc;
+    double* trc; double* drc;       // coarse trace / normal derivative [NXc*NYc]
+    double* tauf; double* sigf;     // fine outputs [NXf*NYf]
+    double* g1; double* g2;         // fine weighted terms for the coarse gather
+    double* h1; double* h2;         // [NYc][NXf] after the y gather
+    double* tauc; double* sigc;     // coarse outputs [NXc*NYc]
+};
+
+struct Box {
+    sem_box_desc d{};
+    int N = 0;
+    long long NX = 0, NY = 0, NZ = 0;
+    double h[3] = {0, 0, 0};
+    double* P[2] = {nullptr, nullptr};
+    double* W = nullptr;
+    double* xc = nullptr;
+    double* yc = nullptr;
+    double* mx = nullptr;  // face mass factors along x [NX] = (h_x/2) w_asm
+    double* my = nullptr;
+    BoxTables tab{};
+    std::vector<double> xh, yh, mxh, myh, mzh;  // host copies
+    int iface_side = 0;
+    double* tau = nullptr;  // interface outputs on this box's face lattice
+    double* sig = nullptr;
+    long long ndof() const { return NX * NY * NZ; }
+};
+
+struct Pmut {
+    bool on = false;
+    int box = 0, n_pmut = 0, n_modes = 0, lmax = 0;
+    int* rect = nullptr;
+    double *sx = nullptr, *sy = nullptr, *wx = nullptr, *wy = nullptr;
+    double *omega2 = nullptr, *twozw = nullptr, *invmass = nullptr, *eta = nullptr, *delay = nullptr;
+    double *q = nullptr, *qd = nullptr, *qdd = nullptr, *phi = nullptr, *F = nullptr;
+    double amp = 0, om0 = 0, ncyc = 1, t_end = 0, t_switch = 0, invC = 0, kappa = 0;
+    int rx = 0;
+};
+
+struct Iface {
+    bool on = false;
+    int fine = 0, coarse = 1;
+    IfaceParams prm{};
+    std::vector<void*> allocs;
+};
+
+struct PlaneWave {
+    bool on = false;
+    int box = 0;
+    double amp = 0, f0 = 0, sigma = 0, t0 = 0, k[3] = {0, 0, 0}, xref[3] = {0, 0, 0};
+};
+
+}  // namespace sem
+
+struct sem_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int flags = 0;
+    int rank = 0, world = 1;
+    double dt = 0;
+    std::vector<sem::Box> boxes;
+    sem::Pmut pm;
+    sem::Iface itf;
+    sem::PlaneWave pw;
+    int cur = 0;                 // P[cur] = p^{step+1}, P[1-cur] = p^{step}
+    long long step = 0;          // host mirror of the device counter
+    long long* d_step = nullptr;
+    unsigned int* d_done = nullptr;
+    double* d_scratch = nullptr; // readback / reductions
+    unsigned long long* d_flag = nullptr;
+    cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [parity][1 or 2 steps]
+    long long graph_launches[2][2] = {{0, 0}, {0, 0}};
+    long long last_launches = 0;
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
+    double kt_ms[3] = {0, 0, 0};
+    long long kt_n[3] = {0, 0, 0};
+    std::string err;
+    std::vector<void*> allocs;
+};
+
+namespace sem {
+// kernels.cu
+void launch_volume(const VolParams& p, int N, cudaStream_t s);
+void launch_modal(const ModalParams& p, cudaStream_t s);
+void launch_iface(const IfaceParams& p, cudaStream_t s);
+void launch_fill_random(double* p, double* w, double* pn, long long n, unsigned long long seed, int box,
+                        double ps, double vs, double dt, cudaStream_t s);
+void launch_set_state(double* pprev, double* pcur, double* w, const double* p0, const double* v0,
+                      long long n, double dt, cudaStream_t s);
+void launch_gather(const double* src, const long long* ids, long long n, double* out, cudaStream_t s);
+void launch_nonfinite(const double* p, long long n, unsigned long long* flag, cudaStream_t s);
+}  // namespace sem

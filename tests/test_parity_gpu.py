@@ -1,0 +1,124 @@
+"""GPU parity: libsem (CUDA, sm_100a) vs the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): relative L2 <= 1e-11 on every box's pressure field and on the modal
+amplitudes after the configured number of steps (reading R21 floor for near-zero modal amplitudes).
+"""
+import numpy as np
+import pytest
+
+from sem_inputs import cavity_config, config, conforming_cut_config, random_state, small_config
+
+from parity import TOL, compare, gpu_run, oracle_run, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def test_cfg0_full():
+    rec = config(0)
+    nm = oracle_run(rec, rec["n_steps"])
+    sim = gpu_run(rec, rec["n_steps"])
+    r = compare(sim, nm)
+    assert np.abs(nm.p).max() > 1.0 and np.abs(nm.q).max() > 1e-12     # non-trivial run
+    for k, v in r.items():
+        assert v < TOL, (k, v, r)
+
+
+@pytest.mark.parametrize("name", ["cfg1s", "cfg2s", "cfg3s", "cfg4s"])
+def test_small_configs_full_run(name):
+    rec = small_config(name)
+    nm = oracle_run(rec, rec["n_steps"])
+    sim = gpu_run(rec, rec["n_steps"])
+    r = compare(sim, nm)
+    for k, v in r.items():
+        assert v < TOL, (k, v, r)
+
+
+@pytest.mark.parametrize("name", ["cfg0", "cfg1s", "cfg2s", "cfg4s"])
+def test_random_state_operator_parity(name):
+    """Seeded random p^0, p'^0 (rough fields exercise every stencil entry and the penalty)."""
+    rec = config(0) if name == "cfg0" else small_config(name)
+    st = random_state(rec, seed=7)
+    for n in (1, 2, 5):
+        nm = oracle_run(rec, n, state=st)
+        sim = gpu_run(rec, n, state=st)
+        r = compare(sim, nm)
+        # the increment p^n - p^0 isolates the operator from the (exactly copied) initial field
+        for b in range(len(sim.ndof)):
+            d_gpu = sim.pressure(b) - st[b][0]
+            d_orc = nm.sys.split(nm.p)[b] - st[b][0]
+            assert rel_l2(d_gpu, d_orc) < 1e-12 * 100, (name, n, b)
+        for k, v in r.items():
+            assert v < TOL, (name, n, k, v)
+        sim.close()
+
+
+def test_literal_coupling_flag():
+    rec = config(0, coupling="literal")
+    nm = oracle_run(rec, 300)
+    sim = gpu_run(rec, 300)
+    for k, v in compare(sim, nm).items():
+        assert v < TOL, (k, v)
+
+
+@pytest.mark.parametrize("N,nel", [(1, (3, 5, 2)), (2, (2, 3, 4)), (3, (11, 3, 2)), (6, (2, 1, 3)),
+                                   (7, (1, 2, 1)), (8, (2, 2, 1))])
+def test_degrees_and_ragged_tiles(N, nel):
+    """Every compiled degree; NX not a multiple of 32, NY not of 8, single-element directions."""
+    rec = cavity_config(nel=nel, degree=N, extent=(1.1e-4 * nel[0], 0.9e-4 * nel[1], 1.3e-4 * nel[2]))
+    rec["boxes"][0]["bc"] = [1, 0, 0, 1, 0, 1]           # mixed absorbing / rigid faces
+    st = random_state(rec, seed=N)
+    nm = oracle_run(rec, 40, state=st)
+    sim = gpu_run(rec, 40, state=st)
+    for k, v in compare(sim, nm).items():
+        assert v < TOL, (k, v)
+
+
+@pytest.mark.parametrize("ratio,nh", [(1, 5), (2, 3), (3, 2)])
+def test_interface_ratios(ratio, nh):
+    rec = conforming_cut_config(nel_xy=6, nz_lo=2, nz_hi=3, degree=5, degree_hi=nh, ratio=ratio, h=25e-6,
+                                bc_top=1)
+    st = random_state(rec, seed=11)
+    nm = oracle_run(rec, 30, state=st)
+    sim = gpu_run(rec, 30, state=st)
+    for k, v in compare(sim, nm).items():
+        assert v < TOL, (k, v)
+
+
+def test_graph_and_direct_launch_bitwise_equal():
+    from paper_2603_06267_b200 import SEM_F_NO_GRAPH
+    rec = small_config("cfg2s")
+    a = gpu_run(rec, 37, chunks=[1, 2, 5, 29])
+    b = gpu_run(rec, 37, flags=SEM_F_NO_GRAPH)
+    c = gpu_run(rec, 37)
+    for box in range(2):
+        assert np.array_equal(a.pressure(box), b.pressure(box))
+        assert np.array_equal(a.pressure(box), c.pressure(box))
+    assert np.array_equal(a.modal()[0], b.modal()[0])
+
+
+def test_error_paths():
+    from paper_2603_06267_b200 import SemError, Simulation
+    rec = config(0)
+    bad = config(0)
+    bad["boxes"][0]["degree"] = 9
+    with pytest.raises(SemError):
+        Simulation(bad)
+    ov = config(1)
+    ov["pmut"]["centers"][1] = ov["pmut"]["centers"][0] + np.array([50e-6, 0.0])
+    with pytest.raises(SemError, match="overlap"):
+        Simulation(ov)
+    it = small_config("cfg2s")
+    ex = it["boxes"][1]["extent"]
+    it["boxes"][1]["extent"] = (ex[0] * 2 / 3, ex[1], ex[2])   # interface faces do not coincide
+    with pytest.raises(SemError, match="UNMATCHED"):
+        Simulation(it)
+    sim = Simulation(rec)
+    with pytest.raises(SemError):
+        sim.write_state(0, np.zeros(5), np.zeros(5))
