@@ -1,0 +1,272 @@
+"""Benchmark of the B200 DG-SEM / PMUT leapfrog step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path (Algorithm 1): modal ROM update, SIPG
+interface flux, fused volume stiffness + ABC + PMUT forcing + kick-drift on every acoustic node of
+both boxes.  Workload: BASELINE.json configs[3] (64x64 PMUT array, 526,755,050 FP64 DOF; the
+largest config and the one the north-star's roofline / scaling targets name), synthetic inputs
+(sem_inputs), state resident in HBM (12.6 GB > L2, so no flush is needed between steps).
+
+Prints ONE JSON line on rank 0.  For N > 1 (torchrun), ranks run the slab decomposition.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "acoustic GDOF-updates/s per leapfrog step (FP64)"
+UNIT = "GDOF/s"
+BYTES_PER_DOF = 32.0          # algorithmic: read p, w; write p, w (FP64) -- DESIGN.md "Byte budget"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def cpu_baseline(steps, warmup=1, patch=4):
+    """The oracle as it stands (numpy, FP64) on a bounded sample of the config-3 workload: a
+    patch x patch PMUT lateral crop with the full config-3 depth, N, h, interface and modes."""
+    import numpy as np  # noqa: F401
+    from oracle.newmark import Newmark
+    from oracle.operators import System
+    from sem_inputs.workloads import crop_config
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([t.get("num_threads", 1) for t in threadpool_info()] or [1])
+    except Exception:
+        cores = os.cpu_count()
+    rec = crop_config(3, patch)
+    sys_ = System(rec)
+    nm = Newmark(sys_)
+    nm.run(warmup)
+    t0 = time.perf_counter()
+    nm.run(steps)
+    dt = time.perf_counter() - t0
+    val = sys_.ndof * steps / dt / 1e9
+    return {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"config-3 crop: {patch}x{patch} PMUTs ({rec['boxes'][0]['nel']} fine + "
+                      f"{rec['boxes'][1]['nel']} coarse elements, {sys_.ndof} DOF), {steps} timed steps "
+                      f"after {warmup} warm-up, {dt:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cb = cpu_baseline(args.steps, args.warmup, patch=args.ref_patch)
+    out = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+           "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"cfg{args.config} (bounded crop, oracle on host cores)"},
+           "cpu_baseline": cb,
+           "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=20)
+    ap.add_argument("--ref-patch", type=int, default=4)
+    args = ap.parse_args()
+    assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_SHORT"), "timing rules: warmup >= 3"
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2603_06267_b200.sem import (Simulation, sem_kernel_time, sem_last_launch_count, sem_read_modal,
+                                           sem_read_pressure_ptr, sem_set_profiling, sem_write_state_ptr)
+    from sem_inputs import config
+
+    rec = config(args.config)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    nccl_id = None
+    if world > 1:
+        raise SystemExit("slab decomposition not built into libsem yet")
+    sim = Simulation(rec, device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_unique_id=nccl_id)
+    ndof_total = sum(sim.ndof)
+
+    # ---- device-resident timed region ----------------------------------------------------------
+    sim.step(args.warmup)
+    sim.sync()
+    sem_set_profiling(sim.ctx, 1)            # CUDA events around each kernel group on this stream
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    e0.record(stream)
+    sim.step(args.steps)
+    launches += sem_last_launch_count(sim.ctx)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    vol_ms, vol_n = sem_kernel_time(sim.ctx, 0)
+    ifc_ms, ifc_n = sem_kernel_time(sim.ctx, 1)
+    mod_ms, mod_n = sem_kernel_time(sim.ctx, 2)
+    sem_set_profiling(sim.ctx, 0)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = ndof_total * world * args.steps / (ms / 1e3) / 1e9
+
+    peak, peak_kind = _peaks()
+    vol_step_ms = vol_ms / max(vol_n, 1)
+    achieved = BYTES_PER_DOF * ndof_total / (vol_step_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_step")
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the C ABI with host buffers ------------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        hp = [torch.zeros(n, dtype=torch.float64).pin_memory() for n in sim.ndof]
+        hv = [torch.zeros(n, dtype=torch.float64).pin_memory() for n in sim.ndof]
+        ho = [torch.empty(n, dtype=torch.float64).pin_memory() for n in sim.ndof]
+        nm = sim.n_pmut_modes
+        qh = np.empty(nm)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for b in range(len(sim.ndof)):
+            sem_write_state_ptr(sim.ctx, b, hp[b].data_ptr(), hv[b].data_ptr(), sim.ndof[b])
+        sim.step(args.steps)
+        launches_e2e = sem_last_launch_count(sim.ctx)
+        for b in range(len(sim.ndof)):
+            sem_read_pressure_ptr(sim.ctx, b, ho[b].data_ptr(), sim.ndof[b])
+        if nm:
+            sem_read_modal(sim.ctx, nm)
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        h2d = 16.0 * ndof_total
+        d2h = 8.0 * ndof_total + 16.0 * nm
+        e2e = {"value": ndof_total * args.steps / t_e2e / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+               "note": "write_state (pinned H2D p0, p'0) + sem_step(K) + read_pressure/read_modal (D2H), "
+                       "host wall clock", "gpu_launches": launches_e2e}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg{args.config}", "dof": ndof_total,
+                   "boxes": [f"{b['nel'][0]}x{b['nel'][1]}x{b['nel'][2]} N={b['degree']}" for b in rec["boxes"]],
+                   "n_pmut": len(rec["pmut"]["centers"]) if rec.get("pmut") else 0,
+                   "n_modes": len(rec["pmut"]["mode_mn"]) if rec.get("pmut") else 0,
+                   "dt": rec["dt"], "l2": "state 24 B/DOF resident = %.1f GB > 126 MB L2; no flush needed"
+                   % (24 * ndof_total / 1e9), "parallelism": f"x-slabs x{world}"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "vol_kernel (both boxes, per step)",
+                     "bytes_per_step_algorithmic": BYTES_PER_DOF * ndof_total,
+                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                     "share_of_step": vol_ms / ms if ms > 0 else None,
+                     "interface_ms_per_step": ifc_ms / max(ifc_n, 1), "modal_ms_per_step": mod_ms / max(mod_n, 1)},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.cpu_steps)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    sim.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

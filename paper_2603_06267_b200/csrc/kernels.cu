@@ -1,14 +1,18 @@
 // sm_100a FP64 kernels of one leapfrog step (Algorithm 1) of the DG-SEM / PMUT model.
 //
 //  vol_kernel     volume stiffness (Eq. 7 first sum) in 1D-stiffness sum-factorised form on affine
-//                 GLL elements, CG assembly in registers/shared memory (owner computes), fused with
-//                 ABC (Eq. 8), PMUT forcing (Eq. 11), the SIPG layer terms and the kick-drift update.
-//                 One CTA = 32 x TY node columns marching over z: the z-stencil lives in a register
-//                 window, the x/y stencils read one shared-memory plane (with an N-node halo).
-//  modal_kernel   one warp per PMUT: pressure projection (Eq. 12), modal predictor/solve/corrector
+//                 GLL elements, CG assembly in registers / shared memory (owner computes), fused with
+//                 the ABC (Eq. 8), the PMUT forcing (Eq. 11), the SIPG layer terms (Eq. 7) and the
+//                 kick-drift update.  One CTA owns a (TXE x TY) column of nodes and marches over z:
+//                 TMA streams each z-plane of p (with an N-node halo, zero-filled outside the box) and
+//                 of w into a D-deep shared-memory ring guarded by mbarriers; the z-stencil lives in a
+//                 register window, the x / y stencils read the shared plane.
+//  modal_kernel   one warp per PMUT: pressure projection (Eq. 12), modal predictor / solve / corrector
 //                 (Eq. 10), force plane f = kappa B^T qdd (Eq. 11).
-//  iface_*        SIPG flux of Eq. 7 on the 2:1 non-conforming face on the fine-face GLL lattice.
-// See DESIGN.md for the derivation of every coefficient and the byte budget of each kernel.
+//  iface_*        SIPG flux of Eq. 7 on the 2:1 non-conforming face, quadrature at the fine-face GLL
+//                 lattice (reading R9).
+// DESIGN.md derives every coefficient and gives the byte budget of each kernel.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -17,216 +21,323 @@
 namespace sem {
 
 // ------------------------------------------------------------------------------------------------
+// mbarrier / TMA helpers (inline PTX)
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
+        : "memory");
+}
+
+// ------------------------------------------------------------------------------------------------
 // Volume + update kernel
 // ------------------------------------------------------------------------------------------------
 template <int N, int TY>
-__global__ void __launch_bounds__(kTX* TY) vol_kernel(const __grid_constant__ VolParams p) {
-    constexpr int SW = kTX + 2 * N;         // shared plane pitch (doubles)
-    constexpr int SH = TY + 2 * N;
-    constexpr int NT = kTX * TY;
-    constexpr int HX = 2 * N * TY;          // x-halo cells per plane
-    constexpr int H = HX + 2 * N * kTX;     // + y-halo cells
-    constexpr int HPT = (H + NT - 1) / NT;  // halo cells per thread
-    __shared__ double sbuf[2][SH * SW];
+struct VolGeo {
+    static constexpr int TXE = vol_txe(N);
+    static constexpr int NH = vol_nh(N);         // x halo width in the shared plane (even)
+    static constexpr int SW = vol_pbox_w(N);     // shared P plane pitch (doubles)
+    static constexpr int WW = vol_wbox_w(N);     // shared W plane pitch
+    static constexpr int SH = TY + 2 * N;
+    static constexpr int D = vol_depth(N);
+    static constexpr int SLOT = vol_slot_bytes(N, TY);
+    static constexpr int PBYTES = SW * SH * 8;
+    static constexpr int POFF = vol_pbytes_aligned(N, TY);   // W tile offset inside a slot
+    static constexpr int WBYTES = WW * TY * 8;
+};
 
+template <int N, int TY>
+__device__ __forceinline__ void vol_issue(const VolParams& p, unsigned char* ring, uint32_t bars, int slot, int z,
+                                          int tx0, int ty0) {
+    using G = VolGeo<N, TY>;
+    unsigned char* s = ring + slot * G::SLOT;
+    const uint32_t bar = bars + 8u * slot;
+    mbar_expect_tx(bar, G::PBYTES + G::WBYTES);
+    tma_load_3d(smem_u32(s), &p.tmP, tx0 - G::NH, ty0 - N, z, bar);
+    tma_load_3d(smem_u32(s + G::POFF), &p.tmW, tx0, ty0, z, bar);
+}
+
+// Per-thread state of the volume kernel.
+template <int N>
+struct VolThread {
+    double cR[N + 1];     // x row of this lane's node (right element, or B0); zeros if none
+    double cyR[N + 1];    // y row (right element or B0)
+    double fL;            // factor on the left-element x row received from lane-1 (0, 1, or 2 at BN)
+    double dxy;           // lateral ABC C_ii / M_ii
+    double fv, tauv, sigv, pwx, pwy;
+    int xb;               // smem column of the right element's first node (lane 31: left element of lane 0)
+    int own;              // smem offset of the own node in the P plane
+    int wown;             // smem offset in the W plane
+    int yb;               // smem offset of the right element's first row (x col of the own node)
+    int yl;               // smem offset of the left element's first row
+    int yLf;              // left-element y row factor (0, 1, 2), warp-uniform
+    bool valid;
+};
+
+// One plane: a = -(M^-1 K p)_i - C_ii/M_ii w_i + extras;  w <- w + dt a;  p <- p + dt w.
+template <int N, int TY, int C, bool EDGE>
+__device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>& t, const double* __restrict__ sP,
+                                          const double* __restrict__ sW, const double (&zw)[2 * N + 1], long long iz,
+                                          int ez, double t1, double* __restrict__ outP, double* __restrict__ outW) {
+    using G = VolGeo<N, TY>;
     const BoxTables& T = p.tab;
-    const int lx = threadIdx.x, ly = threadIdx.y, tid = ly * kTX + lx;
-    const long long NX = p.NX, NY = p.NY, NZ = p.NZ;
-    const long long tx0 = (long long)blockIdx.x * kTX, ty0 = (long long)blockIdx.y * TY;
-    const long long ix = tx0 + lx, iy = ty0 + ly;
-    const bool valid = ix < NX && iy < NY;
-    const long long S = NX * NY;
-    const long long col = valid ? iy * NX + ix : 0;
-
-    // ---- 1D row coefficients of this thread's x / y position (see sem_internal.h) ----
-    int ax = 0, ay = 0;
-    bool hxR = false, hxL = false, hyR = false, hyL = false;
-    int rxR = 0, ryR = 0;
-    if (valid) {
-        if (ix == 0) { rxR = row_B0(N); hxR = true; }
-        else if (ix == NX - 1) { hxL = true; }
-        else { ax = (int)(ix % N); rxR = ax; hxR = true; hxL = (ax == 0); }
-        if (iy == 0) { ryR = row_B0(N); hyR = true; }
-        else if (iy == NY - 1) { hyL = true; }
-        else { ay = (int)(iy % N); ryR = ay; hyR = true; hyL = (ay == 0); }
-    }
-    const int rxL = (ix == NX - 1) ? row_BN(N) : row_L(N);
-    const int ryL = (iy == NY - 1) ? row_BN(N) : row_L(N);
-    double cxR[N + 1], cxL[N + 1], cyR[N + 1], cyL[N + 1];
+    // ---- x: right-element row with per-lane coefficients, left-element row (uniform) by lane-1
+    double v[N + 1];
+#pragma unroll
+    for (int b = 0; b <= N; ++b) v[b] = sP[t.xb + b];
+    double xr = 0.0, xl = 0.0;
 #pragma unroll
     for (int b = 0; b <= N; ++b) {
-        cxR[b] = hxR ? T.G[0][rxR][b] : 0.0;
-        cxL[b] = hxL ? T.G[0][rxL][b] : 0.0;
-        cyR[b] = hyR ? T.G[1][ryR][b] : 0.0;
-        cyL[b] = hyL ? T.G[1][ryL][b] : 0.0;
+        xr = fma(t.cR[b], v[b], xr);
+        xl = fma(T.G[0][row_L(N)][b], v[b], xl);
     }
-    const int own = (ly + N) * SW + lx + N;
-    const int bRx = own - ax, bLx = (ly + N) * SW + lx;
-    const int bRy = (ly + N - ay) * SW + lx + N, bLy = ly * SW + lx + N;
-
-    double dxy = 0.0;
-    if (valid) {
-        if (ix == 0) dxy += p.damp[0];
-        if (ix == NX - 1) dxy += p.damp[1];
-        if (iy == 0) dxy += p.damp[2];
-        if (iy == NY - 1) dxy += p.damp[3];
-    }
-
-    // ---- halo slots ----
-    int hs[HPT];
-    long long hg[HPT];
+    const unsigned FULL = 0xffffffffu;
+    const double xlr = __shfl_sync(FULL, xl, (threadIdx.x + 31) & 31);
+    double acc = fma(t.fL, xlr, xr);
+    // ---- y: warp-uniform row class
+    double yr = 0.0;
 #pragma unroll
-    for (int k = 0; k < HPT; ++k) {
-        const int h = tid + k * NT;
-        hs[k] = -1;
-        hg[k] = -1;
-        if (h < H) {
-            long long gx, gy;
-            int sx, sy;
-            if (h < HX) {
-                const int side = h / (N * TY), rem = h % (N * TY), r = rem / N, c = rem % N;
-                sy = r + N;
-                sx = side ? kTX + N + c : c;
-                gx = side ? tx0 + kTX + c : tx0 - N + c;
-                gy = ty0 + r;
-            } else {
-                const int hh = h - HX, side = hh / (N * kTX), rem = hh % (N * kTX), r = rem / kTX,
-                          c = rem % kTX;
-                sy = side ? TY + N + r : r;
-                sx = c + N;
-                gx = tx0 + c;
-                gy = side ? ty0 + TY + r : ty0 - N + r;
+    for (int b = 0; b <= N; ++b) yr = fma(t.cyR[b], sP[t.yb + b * G::SW], yr);
+    if (t.yLf) {
+        double yl = 0.0;
+#pragma unroll
+        for (int b = 0; b <= N; ++b) yl = fma(T.G[1][row_L(N)][b], sP[t.yl + b * G::SW], yl);
+        acc = fma((double)t.yLf, yl, acc);
+    }
+    acc += yr;
+    // ---- z: register window zw[k] = p(z0 - N + k), compile-time rows
+    double zp = 0.0;
+    if (C == N) {   // top boundary plane: left element only, BN = 2 L
+#pragma unroll
+        for (int b = 0; b <= N; ++b) zp = fma(T.G[2][row_L(N)][b], zw[N + b], zp);
+        zp *= 2.0;
+    } else if (C == 0) {
+        if (EDGE && ez == 0) {
+#pragma unroll
+            for (int b = 0; b <= N; ++b) zp = fma(T.G[2][row_B0(N)][b], zw[N + b], zp);
+        } else {
+#pragma unroll
+            for (int b = 0; b <= N; ++b) zp = fma(T.G[2][0][b], zw[N + b], zp);
+            double zl = 0.0;
+#pragma unroll
+            for (int b = 0; b <= N; ++b) zl = fma(T.G[2][row_L(N)][b], zw[b], zl);
+            zp += zl;
+        }
+    } else {
+#pragma unroll
+        for (int b = 0; b <= N; ++b) zp = fma(T.G[2][C][b], zw[N + b], zp);
+    }
+    double a = -(acc + zp);
+    const double wv = sW[t.wown];
+    const double pv = zw[N + C];
+    double damp = t.dxy;
+    if (EDGE) {
+        if (iz == 0) {
+            damp += p.damp[4];
+            a = fma(p.kF, t.fv, a);
+        }
+        if (iz == p.NZ - 1) damp += p.damp[5];
+        if (p.iface_side > 0 && iz >= p.NZ - 1 - N) {
+            const int cc = (int)(iz - (p.NZ - 1 - N));
+            a -= t.tauv * T.ktau[cc] + t.sigv * T.ksig[cc];
+        } else if (p.iface_side < 0 && iz <= N) {
+            const int cc = (int)iz;
+            a -= t.tauv * T.ktau[cc] + t.sigv * T.ksig[cc];
+        }
+        if (p.pw_on && iz == p.NZ - 1) {
+            const double tau = t1 - (p.pw_k[0] * (t.pwx - p.pw_xref[0]) + p.pw_k[1] * (t.pwy - p.pw_xref[1]) +
+                                     p.pw_k[2] * (p.pw_ztop - p.pw_xref[2])) / p.pw_c;
+            const double u = tau - p.pw_t0;
+            const double is2 = 1.0 / (p.pw_sigma * p.pw_sigma);
+            double sn, cs;
+            sincos(p.pw_om * u, &sn, &cs);
+            a += p.pw_fac * (exp(-0.5 * u * u * is2) * (-u * is2 * sn + p.pw_om * cs));
+        }
+    } else if (C == 0 && p.iface_side < 0 && iz == N) {
+        a -= t.sigv * T.ksig[N];   // coarse-side layer term on the shared plane z = N
+    }
+    a = fma(-damp, wv, a);
+    const double wn = fma(p.dt, a, wv);
+    const double pn = fma(p.dt, wn, pv);
+    if (t.valid) {
+        __stcs(outW, wn);
+        __stcs(outP, pn);
+    }
+}
+
+// One element layer: planes z0 .. z0+N-1 (plus the top plane N nel_z on the last layer), unrolled by
+// compile-time recursion over the local plane index C so that every z row and window index is a
+// constant.
+template <int N, int TY, bool EDGE, int C>
+__device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
+                                               uint32_t bars, int ez, bool last, int tx0, int ty0, double t1,
+                                               const double (&zw)[2 * N + 1], double (&nxt)[N], double*& outP,
+                                               double*& outW) {
+    if constexpr (C <= N) {
+        using G = VolGeo<N, TY>;
+        if (C == N && !last) return;
+        const int NZ = (int)p.NZ;
+        const int z0 = N * ez;
+        const int iz = z0 + C;
+        if constexpr (C < N) {   // the next layer's plane z0 + N + 1 + C into the window queue
+            const int zn = z0 + N + 1 + C;
+            nxt[C] = 0.0;
+            if (zn < NZ) {
+                const int sn = zn % G::D;
+                mbar_wait(bars + 8u * sn, (uint32_t)((zn / G::D) & 1));
+                nxt[C] = reinterpret_cast<const double*>(ring + sn * G::SLOT)[t.own];
             }
-            hs[k] = sy * SW + sx;
-            if (gx >= 0 && gx < NX && gy >= 0 && gy < NY) hg[k] = gy * NX + gx;
+        }
+        const int sl = iz % G::D;
+        const double* sP = reinterpret_cast<const double*>(ring + sl * G::SLOT);
+        const double* sW = reinterpret_cast<const double*>(ring + sl * G::SLOT + G::POFF);
+        vol_plane<N, TY, C, EDGE>(p, t, sP, sW, zw, iz, ez, t1, outP, outW);
+        const long long PS = p.PX * p.NY;
+        outP += PS;
+        outW += PS;
+        __syncthreads();   // every warp is done with slot sl: refill it with plane iz + D
+        if (threadIdx.x == 0 && threadIdx.y == 0 && iz + G::D < NZ)
+            vol_issue<N, TY>(p, ring, bars, sl, iz + G::D, tx0, ty0);
+        vol_layer_step<N, TY, EDGE, C + 1>(p, t, ring, bars, ez, last, tx0, ty0, t1, zw, nxt, outP, outW);
+    }
+}
+
+template <int N, int TY, bool EDGE>
+__device__ __forceinline__ void vol_layer(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
+                                          uint32_t bars, int ez, int tx0, int ty0, double t1, double (&zw)[2 * N + 1],
+                                          double*& outP, double*& outW) {
+    double nxt[N];
+    const bool last = (ez == p.nelz - 1);
+    vol_layer_step<N, TY, EDGE, 0>(p, t, ring, bars, ez, last, tx0, ty0, t1, zw, nxt, outP, outW);
+#pragma unroll
+    for (int k = 0; k <= N; ++k) zw[k] = zw[k + N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) zw[N + 1 + j] = nxt[j];
+}
+
+template <int N, int TY>
+__global__ void __launch_bounds__(32 * TY) vol_kernel(const __grid_constant__ VolParams p) {
+    using G = VolGeo<N, TY>;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    const uint32_t bars = smem_u32(ring + G::D * G::SLOT);
+    const int lane = threadIdx.x, ly = threadIdx.y;
+    const int tx0 = blockIdx.x * G::TXE, ty0 = blockIdx.y * TY;
+    const long long NX = p.NX, NY = p.NY;
+    const int NZ = (int)p.NZ;
+
+    if (lane == 0 && ly == 0) {
+        for (int s = 0; s < G::D; ++s) mbar_init(bars + 8u * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (lane == 0 && ly == 0)
+        for (int s = 0; s < G::D && s < NZ; ++s) vol_issue<N, TY>(p, ring, bars, s, s, tx0, ty0);
+
+    // ---- thread setup (overlaps the first TMA loads)
+    const BoxTables& T = p.tab;
+    VolThread<N> t;
+    const long long ix = tx0 + lane, iy = ty0 + ly;
+    const bool node_lane = lane < G::TXE;
+    t.valid = node_lane && ix < NX && iy < NY;
+    const int a = lane % N;
+    int rxR = -1;
+    t.fL = 0.0;
+    if (t.valid) {
+        if (ix == 0) rxR = row_B0(N);
+        else if (ix < NX - 1) rxR = a;
+        if (a == 0 && ix > 0) t.fL = (ix == NX - 1) ? 2.0 : 1.0;
+    }
+    t.xb = (ly + N) * G::SW + (node_lane ? lane - a + G::NH : G::NH - N);
+    const int ay = (int)(iy % N);
+    int ryR = -1;
+    t.yLf = 0;
+    if (iy < NY) {
+        if (iy == 0) ryR = row_B0(N);
+        else if (iy < NY - 1) ryR = ay;
+        if (ay == 0 && iy > 0) t.yLf = (iy == NY - 1) ? 2 : 1;
+    }
+#pragma unroll
+    for (int b = 0; b <= N; ++b) {
+        t.cR[b] = rxR >= 0 ? T.G[0][rxR][b] : 0.0;
+        t.cyR[b] = ryR >= 0 ? T.G[1][ryR][b] : 0.0;
+    }
+    const int col = node_lane ? lane + G::NH : 0;
+    t.own = (ly + N) * G::SW + col;
+    t.wown = ly * G::WW + (node_lane ? lane : 0);
+    t.yb = (ly + N - ay) * G::SW + col;
+    t.yl = ly * G::SW + col;
+    t.dxy = 0.0;
+    t.fv = t.tauv = t.sigv = t.pwx = t.pwy = 0.0;
+    if (t.valid) {
+        if (ix == 0) t.dxy += p.damp[0];
+        if (ix == NX - 1) t.dxy += p.damp[1];
+        if (iy == 0) t.dxy += p.damp[2];
+        if (iy == NY - 1) t.dxy += p.damp[3];
+        const long long fc = iy * NX + ix;
+        if (p.F) t.fv = p.F[fc];
+        if (p.iface_side != 0) {
+            t.tauv = p.tau[fc];
+            t.sigv = p.sig[fc];
+        }
+        if (p.pw_on) {
+            t.pwx = p.xc[ix];
+            t.pwy = p.yc[iy];
         }
     }
-
-    // ---- per-column extras ----
     const long long n = __ldcg(p.step);
     const double t1 = (double)(n + 1) * p.dt;
-    const double fv = (p.F != nullptr && valid) ? p.F[col] : 0.0;
-    double tauv = 0.0, sigv = 0.0;
-    if (p.iface_side != 0 && valid) { tauv = p.tau[col]; sigv = p.sig[col]; }
-    double pw_x = 0.0, pw_y = 0.0;
-    if (p.pw_on && valid) { pw_x = p.xc[ix]; pw_y = p.yc[iy]; }
+    const long long off = t.valid ? iy * p.PX + ix : 0;
+    double* outP = p.Pn + off;
+    double* outW = p.W + off;
 
-    const double* __restrict__ P = p.P;
+    // ---- register window zw[k] = p(-N + k), k = 0..2N: planes 0..N from the ring
     double zw[2 * N + 1];
 #pragma unroll
-    for (int k = 0; k <= 2 * N; ++k) {
-        const long long pl = k - N;
-        zw[k] = (valid && pl >= 0 && pl < NZ) ? __ldg(P + col + pl * S) : 0.0;
-    }
-    double hv[HPT];
+    for (int k = 0; k < N; ++k) zw[k] = 0.0;
 #pragma unroll
-    for (int k = 0; k < HPT; ++k) hv[k] = (hg[k] >= 0) ? __ldg(P + hg[k]) : 0.0;
-    double wpre = valid ? __ldcs(p.W + col) : 0.0;
+    for (int k = 0; k <= N; ++k) {
+        zw[N + k] = 0.0;
+        if (k < NZ) {
+            mbar_wait(bars + 8u * (k % G::D), (uint32_t)((k / G::D) & 1));
+            zw[N + k] = reinterpret_cast<const double*>(ring + (k % G::D) * G::SLOT)[t.own];
+        }
+    }
 
     const int nelz = p.nelz;
     for (int ez = 0; ez < nelz; ++ez) {
-        const long long z0 = (long long)N * ez;
-        const bool last = (ez == nelz - 1);
-        double nxt[N];
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-            const long long pl = z0 + N + 1 + j;
-            nxt[j] = (valid && pl < NZ) ? __ldg(P + col + pl * S) : 0.0;
-        }
-#pragma unroll
-        for (int c = 0; c <= N; ++c) {
-            if (c == N && !last) break;
-            const long long iz = z0 + c;
-            double* sb = sbuf[iz & 1];
-            const double v = zw[N + c];
-            sb[own] = v;
-#pragma unroll
-            for (int k = 0; k < HPT; ++k)
-                if (hs[k] >= 0) sb[hs[k]] = hv[k];
-            const double wv = wpre;
-            if (iz + 1 < NZ) {
-#pragma unroll
-                for (int k = 0; k < HPT; ++k) hv[k] = (hg[k] >= 0) ? __ldg(P + hg[k] + (iz + 1) * S) : 0.0;
-                wpre = valid ? __ldcs(p.W + col + (iz + 1) * S) : 0.0;
-            }
-            __syncthreads();
-
-            // z: register window (compile-time rows)
-            double zp = 0.0;
-            if (c == N) {
-#pragma unroll
-                for (int b = 0; b <= N; ++b) zp = fma(T.G[2][row_BN(N)][b], zw[N + b], zp);
-            } else if (c == 0) {
-                if (ez == 0) {
-#pragma unroll
-                    for (int b = 0; b <= N; ++b) zp = fma(T.G[2][row_B0(N)][b], zw[N + b], zp);
-                } else {
-#pragma unroll
-                    for (int b = 0; b <= N; ++b) zp = fma(T.G[2][0][b], zw[N + b], zp);
-#pragma unroll
-                    for (int b = 0; b <= N; ++b) zp = fma(T.G[2][row_L(N)][b], zw[b], zp);
-                }
-            } else {
-#pragma unroll
-                for (int b = 0; b <= N; ++b) zp = fma(T.G[2][c][b], zw[N + b], zp);
-            }
-            // x, y: shared plane
-            double xp = 0.0, yp = 0.0;
-            if (hxR) {
-#pragma unroll
-                for (int b = 0; b <= N; ++b) xp = fma(cxR[b], sb[bRx + b], xp);
-            }
-            if (hxL) {
-#pragma unroll
-                for (int b = 0; b <= N; ++b) xp = fma(cxL[b], sb[bLx + b], xp);
-            }
-            if (hyR) {
-#pragma unroll
-                for (int b = 0; b <= N; ++b) yp = fma(cyR[b], sb[bRy + b * SW], yp);
-            }
-            if (hyL) {
-#pragma unroll
-                for (int b = 0; b <= N; ++b) yp = fma(cyL[b], sb[bLy + b * SW], yp);
-            }
-            double a = -(xp + yp + zp);
-            double damp = dxy;
-            if (iz == 0) damp += p.damp[4];
-            if (iz == NZ - 1) damp += p.damp[5];
-            a -= damp * wv;
-            if (iz == 0) a += p.kF * fv;
-            if (p.iface_side > 0 && iz >= NZ - 1 - N) {
-                const int cc = (int)(iz - (NZ - 1 - N));
-                a -= tauv * T.ktau[cc] + sigv * T.ksig[cc];
-            } else if (p.iface_side < 0 && iz <= N) {
-                const int cc = (int)iz;
-                a -= tauv * T.ktau[cc] + sigv * T.ksig[cc];
-            }
-            if (p.pw_on && iz == NZ - 1) {
-                const double tau = t1 - (p.pw_k[0] * (pw_x - p.pw_xref[0]) + p.pw_k[1] * (pw_y - p.pw_xref[1]) +
-                                         p.pw_k[2] * (p.pw_ztop - p.pw_xref[2])) / p.pw_c;
-                const double u = tau - p.pw_t0;
-                const double is2 = 1.0 / (p.pw_sigma * p.pw_sigma);
-                double sn, cs;
-                sincos(p.pw_om * u, &sn, &cs);
-                const double ds = exp(-0.5 * u * u * is2) * (-u * is2 * sn + p.pw_om * cs);
-                a += p.pw_fac * ds;
-            }
-            const double wn = fma(p.dt, a, wv);
-            const double pn = fma(p.dt, wn, v);
-            if (valid) {
-                __stcs(p.W + col + iz * S, wn);
-                __stcs(p.Pn + col + iz * S, pn);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k <= N; ++k) zw[k] = zw[k + N];
-#pragma unroll
-        for (int j = 0; j < N; ++j) zw[N + 1 + j] = nxt[j];
+        if (ez == 0 || ez == nelz - 1)
+            vol_layer<N, TY, true>(p, t, ring, bars, ez, tx0, ty0, t1, zw, outP, outW);
+        else
+            vol_layer<N, TY, false>(p, t, ring, bars, ez, tx0, ty0, t1, zw, outP, outW);
     }
 
     if (p.bump_step) {
-        __syncthreads();
-        if (tid == 0) {
+        if (lane == 0 && ly == 0) {
             __threadfence();
             const unsigned prev = atomicAdd(p.done, 1u);
             if (prev == p.total_blocks - 1) {
@@ -238,12 +349,34 @@ __global__ void __launch_bounds__(kTX* TY) vol_kernel(const __grid_constant__ Vo
     }
 }
 
+constexpr int kTY = 16;
+
+template <int N>
+static void prepare_vol_N() {
+    cudaFuncSetAttribute(vol_kernel<N, kTY>, cudaFuncAttributeMaxDynamicSharedMemorySize, vol_smem_bytes(N, kTY));
+}
+
+void volume_prepare(int N) {
+    switch (N) {
+        case 1: prepare_vol_N<1>(); break;
+        case 2: prepare_vol_N<2>(); break;
+        case 3: prepare_vol_N<3>(); break;
+        case 4: prepare_vol_N<4>(); break;
+        case 5: prepare_vol_N<5>(); break;
+        case 6: prepare_vol_N<6>(); break;
+        case 7: prepare_vol_N<7>(); break;
+        case 8: prepare_vol_N<8>(); break;
+        default: break;
+    }
+}
+
 template <int N>
 static void launch_vol_N(const VolParams& p, cudaStream_t s) {
-    constexpr int TY = 8;
-    dim3 blk(kTX, TY);
-    dim3 grd((unsigned)((p.NX + kTX - 1) / kTX), (unsigned)((p.NY + TY - 1) / TY));
-    vol_kernel<N, TY><<<grd, blk, 0, s>>>(p);
+    using G = VolGeo<N, kTY>;
+    const int smem = vol_smem_bytes(N, kTY);
+    dim3 blk(32, kTY);
+    dim3 grd((unsigned)((p.NX + G::TXE - 1) / G::TXE), (unsigned)((p.NY + kTY - 1) / kTY));
+    vol_kernel<N, kTY><<<grd, blk, smem, s>>>(p);
 }
 
 void launch_volume(const VolParams& p, int N, cudaStream_t s) {
@@ -260,8 +393,12 @@ void launch_volume(const VolParams& p, int N, cudaStream_t s) {
     }
 }
 
-unsigned volume_blocks(long long NX, long long NY) {
-    return (unsigned)(((NX + kTX - 1) / kTX) * ((NY + 8 - 1) / 8));
+int volume_smem_bytes(int N) { return vol_smem_bytes(N, kTY); }
+int volume_tile_y() { return kTY; }
+
+unsigned volume_blocks(int N, long long NX, long long NY) {
+    const int txe = vol_txe(N);
+    return (unsigned)(((NX + txe - 1) / txe) * ((NY + kTY - 1) / kTY));
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -272,7 +409,7 @@ __device__ __forceinline__ double drive_tx(const ModalParams& p, double tp) {
     return p.amp * sin(p.om0 * tp) * 0.5 * (1.0 - cos(p.om0 * tp / p.ncyc));
 }
 
-__global__ void __launch_bounds__(128) modal_kernel(const ModalParams p) {
+__global__ void __launch_bounds__(128) modal_kernel(const __grid_constant__ ModalParams p) {
     const int lane = threadIdx.x & 31;
     const int k = blockIdx.x * 4 + (threadIdx.x >> 5);
     if (k >= p.n_pmut) return;
@@ -299,7 +436,7 @@ __global__ void __launch_bounds__(128) modal_kernel(const ModalParams p) {
 #pragma unroll
         for (int m = 0; m < kMaxModes; ++m) bx[m] = (on && m < M) ? wxk[i] * sxk[m * L + i] : 0.0;
         for (int j = 0; j < nj; ++j) {
-            const double val = on ? p.P[(long long)(j0 + j) * p.NX + i0 + i] : 0.0;
+            const double val = on ? p.P[(long long)(j0 + j) * p.PX + i0 + i] : 0.0;
             const double wj = wyk[j];
 #pragma unroll
             for (int m = 0; m < kMaxModes; ++m)
@@ -369,14 +506,15 @@ void launch_modal(const ModalParams& p, cudaStream_t s) {
 // ------------------------------------------------------------------------------------------------
 // Interface (SIPG, Eq. 7) on the 2:1 face, fine-face GLL lattice as quadrature (reading R9)
 // ------------------------------------------------------------------------------------------------
-__global__ void iface_coarse_trace(const IfaceParams p) {
+__global__ void iface_coarse_trace(const __grid_constant__ IfaceParams p) {
     const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long n = p.NXc * p.NYc;
-    if (id >= n) return;
-    const long long S = n;
+    if (id >= p.NXc * p.NYc) return;
+    const long long jx = id % p.NXc, jy = id / p.NXc;
+    const long long S = p.PXc * p.NYc;
+    const double* col = p.Pc + jy * p.PXc + jx;
     double d = 0.0;
-    for (int c = 0; c <= p.Nc; ++c) d = fma(p.dcB[c], p.Pc[id + c * S], d);
-    p.trc[id] = p.Pc[id];
+    for (int c = 0; c <= p.Nc; ++c) d = fma(p.dcB[c], col[c * S], d);
+    p.trc[id] = col[0];
     p.drc[id] = d;
 }
 
@@ -387,18 +525,17 @@ __device__ __forceinline__ void coarse_locate(long long i, int NfR, int nelc, in
     base = e * Nc;
 }
 
-__global__ void iface_fine(const IfaceParams p) {
+__global__ void iface_fine(const __grid_constant__ IfaceParams p) {
     const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long n = p.NXf * p.NYf;
-    if (id >= n) return;
+    if (id >= p.NXf * p.NYf) return;
     const long long ix = id % p.NXf, iy = id / p.NXf;
-    const long long S = n;
-    const long long top = (p.NZf - 1) * S;
+    const long long S = p.PXf * p.NYf;
+    const double* top = p.Pf + (p.NZf - 1) * S + iy * p.PXf + ix;
     const int Nf = p.Nf, Nc = p.Nc, NfR = p.Nf * p.R, Nc1 = Nc + 1;
     // fine trace and normal derivative (n+ = +e_z)
-    const double pp = p.Pf[top + id];
+    const double pp = top[0];
     double dpp = 0.0;
-    for (int c = 0; c <= Nf; ++c) dpp = fma(p.dfT[c], p.Pf[top - (Nf - c) * S + id], dpp);
+    for (int c = 0; c <= Nf; ++c) dpp = fma(p.dfT[c], top[-(long long)(Nf - c) * S], dpp);
     // coarse trace / derivative interpolated to x_q
     long long bx, by;
     int qx, qy;
@@ -427,8 +564,7 @@ __global__ void iface_fine(const IfaceParams p) {
 }
 
 // transposed interpolation along one lattice direction: out(j) = sum_i psi_j(x_i) in(i)
-__device__ __forceinline__ void gather_range(long long j, int Nc, int NfR, int nelc, long long nf, long long& lo,
-                                             long long& hi) {
+__device__ __forceinline__ void gather_range(long long j, int Nc, int NfR, long long nf, long long& lo, long long& hi) {
     const long long e = j / Nc;
     const int b = (int)(j - e * Nc);
     lo = (b == 0 && e > 0) ? (e - 1) * NfR : e * NfR;
@@ -446,14 +582,13 @@ __device__ __forceinline__ double gather_weight(const IfaceParams& p, long long 
     return p.I[q * (p.Nc + 1) + b];
 }
 
-__global__ void iface_gather_y(const IfaceParams p) {
+__global__ void iface_gather_y(const __grid_constant__ IfaceParams p) {
     const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long n = p.NXf * p.NYc;
-    if (id >= n) return;
+    if (id >= p.NXf * p.NYc) return;
     const long long ix = id % p.NXf, jy = id / p.NXf;
     const int NfR = p.Nf * p.R;
     long long lo, hi;
-    gather_range(jy, p.Nc, NfR, p.nelcy, p.NYf, lo, hi);
+    gather_range(jy, p.Nc, NfR, p.NYf, lo, hi);
     double s1 = 0.0, s2 = 0.0;
     for (long long iy = lo; iy <= hi; ++iy) {
         const double w = gather_weight(p, iy, jy, NfR, p.nelcy);
@@ -464,14 +599,13 @@ __global__ void iface_gather_y(const IfaceParams p) {
     p.h2[id] = s2;
 }
 
-__global__ void iface_gather_x(const IfaceParams p) {
+__global__ void iface_gather_x(const __grid_constant__ IfaceParams p) {
     const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long n = p.NXc * p.NYc;
-    if (id >= n) return;
+    if (id >= p.NXc * p.NYc) return;
     const long long jx = id % p.NXc, jy = id / p.NXc;
     const int NfR = p.Nf * p.R;
     long long lo, hi;
-    gather_range(jx, p.Nc, NfR, p.nelcx, p.NXf, lo, hi);
+    gather_range(jx, p.Nc, NfR, p.NXf, lo, hi);
     double s1 = 0.0, s2 = 0.0;
     for (long long ix = lo; ix <= hi; ++ix) {
         const double w = gather_weight(p, ix, jx, NfR, p.nelcx);
@@ -493,11 +627,12 @@ void launch_iface(const IfaceParams& p, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------------------------
-// State / test-hook kernels
+// State / test-hook kernels (pitched device layout: element (ix, r) at r * PX + ix, r = iy + NY iz)
 // ------------------------------------------------------------------------------------------------
 // Counter-based generator: splitmix64 finaliser of
 // key = seed * 0xD1B54A32D192ED03 + box * 0x8CB92BA72F3D8DD7 + field * 0x9E3779B97F4A7C15
-// advanced by (id + 1) * 0x9E3779B97F4A7C15; u = 2 (z >> 11) 2^-53 - 1 in [-1, 1).
+// advanced by (id + 1) * 0x9E3779B97F4A7C15; u = 2 (z >> 11) 2^-53 - 1 in [-1, 1); id is the
+// lexicographic node id of the ABI layout.
 __device__ __forceinline__ double cb_uniform(unsigned long long seed, int box, int field, long long id) {
     unsigned long long z = seed * 0xD1B54A32D192ED03ull + (unsigned long long)box * 0x8CB92BA72F3D8DD7ull +
                            (unsigned long long)field * 0x9E3779B97F4A7C15ull;
@@ -508,52 +643,64 @@ __device__ __forceinline__ double cb_uniform(unsigned long long seed, int box, i
     return 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
 }
 
-__global__ void fill_random_kernel(double* pprev, double* w, double* pcur, long long n, unsigned long long seed,
-                                   int box, double ps, double vs, double dt) {
+__global__ void fill_random_kernel(double* pprev, double* w, double* pcur, long long NX, long long PX, long long rows,
+                                   unsigned long long seed, int box, double ps, double vs, double dt) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= NX * rows) return;
+    const long long ix = i % NX, r = i / NX, d = r * PX + ix;
     const double p0 = ps * cb_uniform(seed, box, 0, i);
     const double v0 = vs * cb_uniform(seed, box, 1, i);
-    pprev[i] = p0;
-    w[i] = v0;
-    pcur[i] = p0 + dt * v0;     // p^1 = p^0 + dt p'^0 (+ dt^2/2 p''^0 = 0)
+    pprev[d] = p0;
+    w[d] = v0;
+    pcur[d] = p0 + dt * v0;     // p^1 = p^0 + dt p'^0 (+ dt^2/2 p''^0 = 0)
 }
 
-void launch_fill_random(double* pprev, double* w, double* pcur, long long n, unsigned long long seed, int box,
-                        double ps, double vs, double dt, cudaStream_t s) {
-    fill_random_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pprev, w, pcur, n, seed, box, ps, vs, dt);
+void launch_fill_random(double* pprev, double* w, double* pcur, long long NX, long long PX, long long rows,
+                        unsigned long long seed, int box, double ps, double vs, double dt, cudaStream_t s) {
+    const long long n = NX * rows;
+    fill_random_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pprev, w, pcur, NX, PX, rows, seed, box, ps, vs,
+                                                                   dt);
 }
 
-__global__ void set_state_kernel(const double* pprev, double* pcur, const double* w, long long n, double dt) {
+__global__ void set_state_kernel(const double* pprev, double* pcur, const double* w, long long NX, long long PX,
+                                 long long rows, double dt) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    pcur[i] = pprev[i] + dt * w[i];
+    if (i >= NX * rows) return;
+    const long long d = (i / NX) * PX + i % NX;
+    pcur[d] = pprev[d] + dt * w[d];
 }
 
-void launch_set_state(double* pprev, double* pcur, double* w, const double*, const double*, long long n, double dt,
-                      cudaStream_t s) {
-    set_state_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pprev, pcur, w, n, dt);
+void launch_set_state(const double* pprev, double* pcur, const double* w, long long NX, long long PX, long long rows,
+                      double dt, cudaStream_t s) {
+    const long long n = NX * rows;
+    set_state_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pprev, pcur, w, NX, PX, rows, dt);
 }
 
-__global__ void gather_kernel(const double* src, const long long* ids, long long n, double* out) {
+__global__ void gather_kernel(const double* src, const long long* ids, long long n, long long NX, long long PX,
+                              double* out) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = src[ids[i]];
+    if (i < n) {
+        const long long id = ids[i];
+        out[i] = src[(id / NX) * PX + id % NX];
+    }
 }
 
-void launch_gather(const double* src, const long long* ids, long long n, double* out, cudaStream_t s) {
-    gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, ids, n, out);
+void launch_gather(const double* src, const long long* ids, long long n, long long NX, long long PX, double* out,
+                   cudaStream_t s) {
+    gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, ids, n, NX, PX, out);
 }
 
-__global__ void nonfinite_kernel(const double* p, long long n, unsigned long long* flag) {
+__global__ void nonfinite_kernel(const double* p, long long NX, long long PX, long long rows, unsigned long long* flag) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long stride = (long long)gridDim.x * blockDim.x;
     bool bad = false;
-    for (; i < n; i += stride) bad |= !isfinite(p[i]);
+    for (; i < NX * rows; i += stride) bad |= !isfinite(p[(i / NX) * PX + i % NX]);
     if (bad) atomicOr(flag, 1ull);
 }
 
-void launch_nonfinite(const double* p, long long n, unsigned long long* flag, cudaStream_t s) {
-    nonfinite_kernel<<<148 * 8, 256, 0, s>>>(p, n, flag);
+void launch_nonfinite(const double* p, long long NX, long long PX, long long rows, unsigned long long* flag,
+                      cudaStream_t s) {
+    nonfinite_kernel<<<148 * 8, 256, 0, s>>>(p, NX, PX, rows, flag);
 }
 
 }  // namespace sem

@@ -1,6 +1,8 @@
 // libsem host side: C ABI entry points (include/sem.h), validation, 1D GLL tables, PMUT and
 // interface tables, device allocation, CUDA-graph step capture.  No compute runs on the host:
 // every step of the method executes in kernels.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -15,12 +17,40 @@
 #include "sem_internal.h"
 
 namespace sem {
-unsigned volume_blocks(long long NX, long long NY);
+int volume_tile_y();
 }
 
 using sem::Box;
 
 namespace {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link needed).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3D FP64 map of a pitched box field: dims (NX, NY, NZ), row pitch PX doubles, box (bw, bh, 1),
+// out-of-bounds elements zero-filled (the halo outside the box reads as p = 0 with zero weight).
+bool make_map(CUtensorMap* m, double* base, const Box& b, int bw, int bh) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)b.NX, (cuuint64_t)b.NY, (cuuint64_t)b.NZ};
+    cuuint64_t strides[2] = {(cuuint64_t)b.PX * 8, (cuuint64_t)b.PX * b.NY * 8};
+    cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
 
 // ---------------------------------------------------------------- GLL (host, setup only)
 // Nodes: Newton iteration on (1 - x^2) P_N'(x) through x P_N - P_{N-1} (Chebyshev-Gauss-Lobatto
@@ -211,13 +241,15 @@ sem_status check_box(sem_ctx* ctx, const sem_box_desc& d) {
 sem::VolParams vol_params(sem_ctx* ctx, int bi, int cur) {
     Box& b = ctx->boxes[bi];
     sem::VolParams p{};
+    p.tmP = b.tmP[cur];
+    p.tmW = b.tmW;
     p.tab = b.tab;
-    p.P = b.P[cur];
     p.Pn = b.P[1 - cur];
     p.W = b.W;
     p.NX = b.NX;
     p.NY = b.NY;
     p.NZ = b.NZ;
+    p.PX = b.PX;
     p.nelz = b.d.nel[2];
     p.dt = ctx->dt;
     std::vector<double> x, w;
@@ -252,7 +284,7 @@ sem::VolParams vol_params(sem_ctx* ctx, int bi, int cur) {
     p.step = ctx->d_step;
     p.done = ctx->d_done;
     unsigned tot = 0;
-    for (auto& bb : ctx->boxes) tot += sem::volume_blocks(bb.NX, bb.NY);
+    for (auto& bb : ctx->boxes) tot += sem::volume_blocks(bb.N, bb.NX, bb.NY);
     p.total_blocks = tot;
     p.bump_step = 1;
     return p;
@@ -269,6 +301,7 @@ sem::ModalParams modal_params(sem_ctx* ctx, int cur) {
     p.dt = ctx->dt;
     p.P = p.literal ? b.P[1 - cur] : b.P[cur];
     p.NX = b.NX;
+    p.PX = b.PX;
     p.rect = pm.rect;
     p.sx = pm.sx;
     p.sy = pm.sy;
@@ -408,16 +441,25 @@ sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
         b.NX = (long long)b.N * b.d.nel[0] + 1;
         b.NY = (long long)b.N * b.d.nel[1] + 1;
         b.NZ = (long long)b.N * b.d.nel[2] + 1;
+        b.PX = (b.NX + 7) / 8 * 8;
         for (int k = 0; k < 3; ++k) b.h[k] = b.d.extent[k] / b.d.nel[k];
         build_tables(b);
         ctx->boxes.push_back(b);
     }
     for (size_t i = 0; i < ctx->boxes.size(); ++i) {
         Box& b = ctx->boxes[i];
-        const size_t n = (size_t)b.ndof();
+        const size_t n = (size_t)b.nalloc();
         if (dalloc(ctx, &b.P[0], n) || dalloc(ctx, &b.P[1], n) || dalloc(ctx, &b.W, n)) return bail(SEM_E_OOM);
         if (cudaMemset(b.P[0], 0, n * 8) || cudaMemset(b.P[1], 0, n * 8) || cudaMemset(b.W, 0, n * 8))
             return bail(SEM_E_CUDA);
+        const int TY = sem::volume_tile_y();
+        sem::volume_prepare(b.N);
+        if (!make_map(&b.tmP[0], b.P[0], b, sem::vol_pbox_w(b.N), TY + 2 * b.N) ||
+            !make_map(&b.tmP[1], b.P[1], b, sem::vol_pbox_w(b.N), TY + 2 * b.N) ||
+            !make_map(&b.tmW, b.W, b, sem::vol_wbox_w(b.N), TY)) {
+            fprintf(stderr, "libsem: cuTensorMapEncodeTiled failed\n");
+            return bail(SEM_E_CUDA);
+        }
         if (upload(ctx, &b.xc, b.xh) || upload(ctx, &b.yc, b.yh) || upload(ctx, &b.mx, b.mxh) ||
             upload(ctx, &b.my, b.myh))
             return bail(SEM_E_CUDA);
@@ -565,6 +607,8 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
     p.NYf = F.NY;
     p.NZf = F.NZ;
     p.NXc = C.NX;
+    p.PXf = F.PX;
+    p.PXc = C.PX;
     p.NYc = C.NY;
     p.Nf = F.N;
     p.Nc = C.N;
@@ -703,7 +747,8 @@ sem_status sem_step(sem_ctx* ctx, int n_steps) {
     ctx->last_launches = launches;
     if (ctx->flags & SEM_F_NAN_CHECK) {
         CU(cudaMemsetAsync(ctx->d_flag, 0, 8, ctx->stream));
-        for (auto& b : ctx->boxes) sem::launch_nonfinite(b.P[1 - ctx->cur], b.ndof(), ctx->d_flag, ctx->stream);
+        for (auto& b : ctx->boxes)
+            sem::launch_nonfinite(b.P[1 - ctx->cur], b.NX, b.PX, b.NY * b.NZ, ctx->d_flag, ctx->stream);
         unsigned long long f = 0;
         CU(cudaMemcpyAsync(&f, ctx->d_flag, 8, cudaMemcpyDeviceToHost, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
@@ -725,7 +770,8 @@ sem_status sem_read_pressure(sem_ctx* ctx, int box, double* host, size_t n) {
     if (box < 0 || box >= (int)ctx->boxes.size() || !host) return fail(ctx, SEM_E_ARG, "bad box / buffer");
     Box& b = ctx->boxes[box];
     if (n != (size_t)b.ndof()) return fail(ctx, SEM_E_ARG, "n must equal the box node count");
-    CU(cudaMemcpyAsync(host, b.P[1 - ctx->cur], n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpy2DAsync(host, b.NX * 8, b.P[1 - ctx->cur], b.PX * 8, b.NX * 8, b.NY * b.NZ, cudaMemcpyDeviceToHost,
+                         ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return SEM_OK;
 }
@@ -743,7 +789,7 @@ sem_status sem_read_pressure_at(sem_ctx* ctx, int box, const long long* ids, siz
     CU(cudaMallocAsync(&dids, n * sizeof(long long), ctx->stream));
     CU(cudaMallocAsync(&dout, n * sizeof(double), ctx->stream));
     CU(cudaMemcpyAsync(dids, ids, n * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
-    sem::launch_gather(b.P[1 - ctx->cur], dids, (long long)n, dout, ctx->stream);
+    sem::launch_gather(b.P[1 - ctx->cur], dids, (long long)n, b.NX, b.PX, dout, ctx->stream);
     CU(cudaMemcpyAsync(out, dout, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaFreeAsync(dids, ctx->stream));
     CU(cudaFreeAsync(dout, ctx->stream));
@@ -773,9 +819,9 @@ sem_status sem_write_state(sem_ctx* ctx, int box, const double* p, const double*
     // p^S lives in P[1-cur]; p^{S+1} = p^S + dt w^S in P[cur]; w^0 = p'^0 + dt/2 p''^0 = p'^0
     double* pprev = b.P[1 - ctx->cur];
     double* pcur = b.P[ctx->cur];
-    CU(cudaMemcpyAsync(pprev, p, n * 8, cudaMemcpyHostToDevice, ctx->stream));
-    CU(cudaMemcpyAsync(b.W, pdot, n * 8, cudaMemcpyHostToDevice, ctx->stream));
-    sem::launch_set_state(pprev, pcur, b.W, nullptr, nullptr, (long long)n, ctx->dt, ctx->stream);
+    CU(cudaMemcpy2DAsync(pprev, b.PX * 8, p, b.NX * 8, b.NX * 8, b.NY * b.NZ, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpy2DAsync(b.W, b.PX * 8, pdot, b.NX * 8, b.NX * 8, b.NY * b.NZ, cudaMemcpyHostToDevice, ctx->stream));
+    sem::launch_set_state(pprev, pcur, b.W, b.NX, b.PX, b.NY * b.NZ, ctx->dt, ctx->stream);
     st = reset_dynamic(ctx);
     if (st) return st;
     CU(cudaStreamSynchronize(ctx->stream));
@@ -787,7 +833,8 @@ sem_status sem_fill_random_state(sem_ctx* ctx, int box, unsigned long long seed,
     if (st) return st;
     if (box < 0 || box >= (int)ctx->boxes.size()) return fail(ctx, SEM_E_ARG, "bad box");
     Box& b = ctx->boxes[box];
-    sem::launch_fill_random(b.P[1 - ctx->cur], b.W, b.P[ctx->cur], b.ndof(), seed, box, ps, vs, ctx->dt, ctx->stream);
+    sem::launch_fill_random(b.P[1 - ctx->cur], b.W, b.P[ctx->cur], b.NX, b.PX, b.NY * b.NZ, seed, box, ps, vs, ctx->dt,
+                            ctx->stream);
     st = reset_dynamic(ctx);
     if (st) return st;
     CU(cudaStreamSynchronize(ctx->stream));

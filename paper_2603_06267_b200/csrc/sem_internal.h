@@ -1,5 +1,6 @@
 // Internal declarations of libsem (host setup <-> kernels).  Not part of the ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -12,7 +13,27 @@ namespace sem {
 constexpr int kMaxN = 8;          // supported GLL degrees 1..8
 constexpr int kRows = kMaxN + 3;  // row classes per direction: R[0..N-1], L, B0, BN
 constexpr int kMaxModes = 8;
-constexpr int kTX = 32;           // volume kernel tile width in x (one warp)
+constexpr int kPref = 3;          // volume kernel: planes prefetched beyond the z-stencil window
+
+// Volume kernel tile geometry for degree N: one warp spans a row of
+// TXE = N floor(31/N) computed nodes (whole elements); lane 31 is the "virtual left neighbour"
+// that evaluates the left-element row of lane 0's shared node from the halo.
+// TMA box x-starts must be 16 B aligned: TXE is even and the x halo is NH = N rounded up to even.
+__host__ __device__ constexpr int vol_txe(int N) { return (N * (31 / N)) % 2 ? N * (31 / N) - N : N * (31 / N); }
+__host__ __device__ constexpr int vol_nh(int N) { return N + (N & 1); }
+__host__ __device__ constexpr int vol_pbox_w(int N) { return vol_txe(N) + 2 * vol_nh(N); }
+__host__ __device__ constexpr int vol_wbox_w(int N) { return vol_txe(N); }
+__host__ __device__ constexpr int vol_depth(int N) { return N + 2 + kPref; }
+// slot = [P tile | pad to 128 B | W tile | pad to 128 B]: TMA destinations must be 128 B aligned
+__host__ __device__ constexpr int vol_pbytes_aligned(int N, int TY) {
+    return ((vol_pbox_w(N) * (TY + 2 * N) * 8 + 127) / 128) * 128;
+}
+__host__ __device__ constexpr int vol_slot_bytes(int N, int TY) {
+    return vol_pbytes_aligned(N, TY) + ((vol_wbox_w(N) * TY * 8 + 127) / 128) * 128;
+}
+__host__ __device__ constexpr int vol_smem_bytes(int N, int TY) {
+    return vol_depth(N) * vol_slot_bytes(N, TY) + vol_depth(N) * 8 + 128;
+}
 
 // Row-class indices inside a direction table.
 //   R[a]  interior node with local index a (a = 0: shared, right element), base = i - a
@@ -35,11 +56,13 @@ struct BoxTables {
 };
 
 struct VolParams {
+    CUtensorMap tmP;                // TMA map of p^{n+1} (3D: NX, NY, NZ; row pitch PX)
+    CUtensorMap tmW;                // TMA map of w^n
     BoxTables tab;
-    const double* __restrict__ P;   // p^{n+1}
     double* __restrict__ Pn;        // p^{n+2} (output)
     double* __restrict__ W;         // w^n in, w^{n+1} out (in place)
     long long NX, NY, NZ;           // node counts of the (local) box
+    long long PX;                   // row pitch (doubles) of the device layout
     int nelz;
     double dt;
     // lumped ABC: C_ii / M_ii at boundary nodes of absorbing faces (0 if rigid)
@@ -70,7 +93,7 @@ struct ModalParams {
     int literal;
     double dt;
     const double* __restrict__ P;   // plane z = 0 of the PMUT box (p^{n+1} or p^n if literal)
-    long long NX;
+    long long NX, PX;               // F is compact [NY][NX]; P has row pitch PX
     const int* __restrict__ rect;   // [k][4] = i0, j0, ni, nj
     const double* __restrict__ sx;  // [k][m][lmax] S factors along x (unweighted)
     const double* __restrict__ sy;
@@ -96,6 +119,7 @@ struct IfaceParams {
     const double* __restrict__ Pf;  // fine box p^{n+1}
     const double* __restrict__ Pc;  // coarse box p^{n+1}
     long long NXf, NYf, NZf, NXc, NYc;
+    long long PXf, PXc;             // row pitches of the pitched volume layouts
     int Nf, Nc, R, nelcx, nelcy;
     double gamma, cf2, cc2;
     double dfT[kMaxN + 1];          // (2/h_f) D_f[N_f][c]: d/dz at the fine top face
@@ -116,7 +140,9 @@ struct Box {
     sem_box_desc d{};
     int N = 0;
     long long NX = 0, NY = 0, NZ = 0;
+    long long PX = 0;       // device row pitch (doubles): NX rounded up to 8 (TMA needs 16 B strides)
     double h[3] = {0, 0, 0};
+    CUtensorMap tmP[2], tmW;
     double* P[2] = {nullptr, nullptr};
     double* W = nullptr;
     double* xc = nullptr;
@@ -129,6 +155,7 @@ struct Box {
     double* tau = nullptr;  // interface outputs on this box's face lattice
     double* sig = nullptr;
     long long ndof() const { return NX * NY * NZ; }
+    long long nalloc() const { return PX * NY * NZ; }
 };
 
 struct Pmut {
@@ -191,10 +218,16 @@ namespace sem {
 void launch_volume(const VolParams& p, int N, cudaStream_t s);
 void launch_modal(const ModalParams& p, cudaStream_t s);
 void launch_iface(const IfaceParams& p, cudaStream_t s);
-void launch_fill_random(double* p, double* w, double* pn, long long n, unsigned long long seed, int box,
-                        double ps, double vs, double dt, cudaStream_t s);
-void launch_set_state(double* pprev, double* pcur, double* w, const double* p0, const double* v0,
-                      long long n, double dt, cudaStream_t s);
-void launch_gather(const double* src, const long long* ids, long long n, double* out, cudaStream_t s);
-void launch_nonfinite(const double* p, long long n, unsigned long long* flag, cudaStream_t s);
+void launch_fill_random(double* p, double* w, double* pn, long long NX, long long PX, long long rows,
+                        unsigned long long seed, int box, double ps, double vs, double dt, cudaStream_t s);
+void launch_set_state(const double* pprev, double* pcur, const double* w, long long NX, long long PX, long long rows,
+                      double dt, cudaStream_t s);
+void launch_gather(const double* src, const long long* ids, long long n, long long NX, long long PX, double* out,
+                   cudaStream_t s);
+void launch_nonfinite(const double* p, long long NX, long long PX, long long rows, unsigned long long* flag,
+                      cudaStream_t s);
+int volume_smem_bytes(int N);
+int volume_tile_y();
+void volume_prepare(int N);
+unsigned volume_blocks(int N, long long NX, long long NY);
 }  // namespace sem

@@ -165,6 +165,30 @@ def config(i: int, **over):
     return _finish(rec)
 
 
+def crop_config(i: int, n_side: int, **over):
+    """A lateral crop of configs 2-4: n_side x n_side PMUTs with the config's full depth, N, h,
+    interface, modes and drive law (the bounded CPU sample of bench.py's cpu_baseline)."""
+    if i not in (2, 3, 4):
+        raise ValueError("crop only for the two-box configs 2-4")
+    full = config(i)
+    boxes = _two_box(n_side, full["boxes"][0]["nel"][2], full["boxes"][1]["nel"][2])
+    cen = _grid_centers(n_side, PITCH, 75 * UM)
+    pmf = full["pmut"]
+    modes = [tuple(m) for m in pmf["mode_mn"]]
+    freqs = FREQS_6 if i == 3 else FREQS_3
+    if i == 3:
+        half = n_side * PITCH / 2
+        pm = _pmut(cen, modes, freqs, _scatter(n_side * n_side, full["seed"]), _focus_delay(cen, (half, half, 4.0e-3)))
+    elif i == 2:
+        pm = _pmut(cen, modes, freqs, _scatter(n_side * n_side, full["seed"]), _steer_delay(cen))
+    else:
+        pm = _pmut(cen, modes, freqs, _scatter(n_side * n_side, full["seed"]), np.zeros(n_side * n_side), rx=True)
+    rec = {"name": f"cfg{i}crop{n_side}", "boxes": boxes, "pmut": pm, "n_steps": full["n_steps"],
+           "seed": full["seed"], "interface": full["interface"], "plane_wave": full["plane_wave"]}
+    rec.update(over)
+    return _finish(rec)
+
+
 def config_names():
     return [f"cfg{i}" for i in range(5)]
 
