@@ -84,10 +84,10 @@ __device__ __forceinline__ void vol_issue(const VolParams& p, unsigned char* rin
 template <int N>
 struct VolThread {
     double cR[N + 1];     // x row of this lane's node (right element, or B0); zeros if none
-    double cyR[N + 1];    // y row (right element or B0)
+    int ry;               // y row class (warp-uniform): 0..N-1, row_B0, or -1 (upper boundary: left only)
     double fL;            // factor on the left-element x row received from lane-1 (0, 1, or 2 at BN)
     double dxy;           // lateral ABC C_ii / M_ii
-    double fv, tauv, sigv, pwx, pwy;
+    int fc;               // face-lattice index iy NX + ix (edge-layer inputs are loaded on demand)
     int xb;               // smem column of the right element's first node (lane 31: left element of lane 0)
     int own;              // smem offset of the own node in the P plane
     int wown;             // smem offset in the W plane
@@ -97,11 +97,49 @@ struct VolThread {
     bool valid;
 };
 
+// Ring position of a plane: slot = z mod D and the parity of its fill, advanced incrementally.
+struct RingPos {
+    int slot;
+    uint32_t par;
+    template <int D>
+    __device__ __forceinline__ void advance() {
+        if (++slot == D) {
+            slot = 0;
+            par ^= 1u;
+        }
+    }
+};
+
+template <int N, int TY, int R>
+__device__ __forceinline__ double y_row(const BoxTables& T, const double* __restrict__ s) {
+    using G = VolGeo<N, TY>;
+    double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+    for (int b = 0; b <= N; b += 2) y0 = fma(T.G[1][R][b], s[b * G::SW], y0);
+#pragma unroll
+    for (int b = 1; b <= N; b += 2) y1 = fma(T.G[1][R][b], s[b * G::SW], y1);
+    return y0 + y1;
+}
+
+template <int N, int TY, int R = 0>
+__device__ __forceinline__ double y_row_dispatch(const BoxTables& T, int ry, const double* __restrict__ s) {
+    if constexpr (R < N) {
+        if (ry == R) return y_row<N, TY, R>(T, s);
+        return y_row_dispatch<N, TY, R + 1>(T, ry, s);
+    } else {
+        if (ry == row_B0(N)) return y_row<N, TY, row_B0(N)>(T, s);
+        return 0.0;
+    }
+}
+
+// Layer kinds (compile time): bit 0 = first element layer (z = 0 face), bit 1 = last (z = N nel_z face).
+constexpr int kFirst = 1, kLast = 2;
+
 // One plane: a = -(M^-1 K p)_i - C_ii/M_ii w_i + extras;  w <- w + dt a;  p <- p + dt w.
-template <int N, int TY, int C, bool EDGE>
+template <int N, int TY, int C, int F>
 __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>& t, const double* __restrict__ sP,
-                                          const double* __restrict__ sW, const double (&zw)[2 * N + 1], long long iz,
-                                          int ez, double t1, double* __restrict__ outP, double* __restrict__ outW) {
+                                          const double* __restrict__ sW, const double (&zw)[2 * N + 1], int ez,
+                                          double* __restrict__ outP, double* __restrict__ outW) {
     using G = VolGeo<N, TY>;
     const BoxTables& T = p.tab;
     // ---- x: right-element row with per-lane coefficients, left-element row (uniform) by lane-1
@@ -114,61 +152,56 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
         xr = fma(t.cR[b], v[b], xr);
         xl = fma(T.G[0][row_L(N)][b], v[b], xl);
     }
-    const unsigned FULL = 0xffffffffu;
-    const double xlr = __shfl_sync(FULL, xl, (threadIdx.x + 31) & 31);
-    double acc = fma(t.fL, xlr, xr);
-    // ---- y: warp-uniform row class
-    double yr = 0.0;
-#pragma unroll
-    for (int b = 0; b <= N; ++b) yr = fma(t.cyR[b], sP[t.yb + b * G::SW], yr);
+    const double xlr = __shfl_sync(0xffffffffu, xl, (threadIdx.x + 31) & 31);
+    // ---- y: warp-uniform row class dispatched to compile-time rows (constant-bank coefficients)
+    const double yr = y_row_dispatch<N, TY>(T, t.ry, sP + t.yb);
+    double acc = fma(t.fL, xlr, xr) + yr;
     if (t.yLf) {
         double yl = 0.0;
 #pragma unroll
         for (int b = 0; b <= N; ++b) yl = fma(T.G[1][row_L(N)][b], sP[t.yl + b * G::SW], yl);
-        acc = fma((double)t.yLf, yl, acc);
+        acc = fma(t.yLf == 2 ? 2.0 : 1.0, yl, acc);
     }
-    acc += yr;
     // ---- z: register window zw[k] = p(z0 - N + k), compile-time rows
-    double zp = 0.0;
-    if (C == N) {   // top boundary plane: left element only, BN = 2 L
+    double z0 = 0.0, z1 = 0.0;
+    if constexpr (C == N) {   // top boundary plane: left element only, BN = 2 L
 #pragma unroll
-        for (int b = 0; b <= N; ++b) zp = fma(T.G[2][row_L(N)][b], zw[N + b], zp);
-        zp *= 2.0;
-    } else if (C == 0) {
-        if (EDGE && ez == 0) {
+        for (int b = 0; b <= N; b += 2) z0 = fma(T.G[2][row_L(N)][b], zw[N + b], z0);
 #pragma unroll
-            for (int b = 0; b <= N; ++b) zp = fma(T.G[2][row_B0(N)][b], zw[N + b], zp);
-        } else {
+        for (int b = 1; b <= N; b += 2) z1 = fma(T.G[2][row_L(N)][b], zw[N + b], z1);
+        z0 = 2.0 * z0;
+        z1 = 2.0 * z1;
+    } else if constexpr (C == 0 && (F & kFirst)) {
 #pragma unroll
-            for (int b = 0; b <= N; ++b) zp = fma(T.G[2][0][b], zw[N + b], zp);
-            double zl = 0.0;
+        for (int b = 0; b <= N; b += 2) z0 = fma(T.G[2][row_B0(N)][b], zw[N + b], z0);
 #pragma unroll
-            for (int b = 0; b <= N; ++b) zl = fma(T.G[2][row_L(N)][b], zw[b], zl);
-            zp += zl;
-        }
+        for (int b = 1; b <= N; b += 2) z1 = fma(T.G[2][row_B0(N)][b], zw[N + b], z1);
+    } else if constexpr (C == 0) {
+#pragma unroll
+        for (int b = 0; b <= N; ++b) z0 = fma(T.G[2][0][b], zw[N + b], z0);
+#pragma unroll
+        for (int b = 0; b <= N; ++b) z1 = fma(T.G[2][row_L(N)][b], zw[b], z1);
     } else {
 #pragma unroll
-        for (int b = 0; b <= N; ++b) zp = fma(T.G[2][C][b], zw[N + b], zp);
+        for (int b = 0; b <= N; b += 2) z0 = fma(T.G[2][C][b], zw[N + b], z0);
+#pragma unroll
+        for (int b = 1; b <= N; b += 2) z1 = fma(T.G[2][C][b], zw[N + b], z1);
     }
-    double a = -(acc + zp);
+    double a = -(acc + (z0 + z1));
     const double wv = sW[t.wown];
     const double pv = zw[N + C];
     double damp = t.dxy;
-    if (EDGE) {
-        if (iz == 0) {
-            damp += p.damp[4];
-            a = fma(p.kF, t.fv, a);
-        }
-        if (iz == p.NZ - 1) damp += p.damp[5];
-        if (p.iface_side > 0 && iz >= p.NZ - 1 - N) {
-            const int cc = (int)(iz - (p.NZ - 1 - N));
-            a -= t.tauv * T.ktau[cc] + t.sigv * T.ksig[cc];
-        } else if (p.iface_side < 0 && iz <= N) {
-            const int cc = (int)iz;
-            a -= t.tauv * T.ktau[cc] + t.sigv * T.ksig[cc];
-        }
-        if (p.pw_on && iz == p.NZ - 1) {
-            const double tau = t1 - (p.pw_k[0] * (t.pwx - p.pw_xref[0]) + p.pw_k[1] * (t.pwy - p.pw_xref[1]) +
+    if constexpr ((F & kFirst) && C == 0) {      // z = 0 face: ABC and PMUT forcing (Eq. 11)
+        damp += p.damp[4];
+        if (p.F && t.valid) a = fma(p.kF, __ldg(p.F + t.fc), a);
+    }
+    if constexpr ((F & kLast) && C == N) {       // z = top face: ABC and incident plane wave (R13)
+        damp += p.damp[5];
+        if (p.pw_on && t.valid) {
+            const int ixp = t.fc % (int)p.NX, iyp = t.fc / (int)p.NX;
+            const double t1 = (double)(__ldcg(p.step) + 1) * p.dt;
+            const double tau = t1 - (p.pw_k[0] * (__ldg(p.xc + ixp) - p.pw_xref[0]) +
+                                     p.pw_k[1] * (__ldg(p.yc + iyp) - p.pw_xref[1]) +
                                      p.pw_k[2] * (p.pw_ztop - p.pw_xref[2])) / p.pw_c;
             const double u = tau - p.pw_t0;
             const double is2 = 1.0 / (p.pw_sigma * p.pw_sigma);
@@ -176,8 +209,22 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
             sincos(p.pw_om * u, &sn, &cs);
             a += p.pw_fac * (exp(-0.5 * u * u * is2) * (-u * is2 * sn + p.pw_om * cs));
         }
-    } else if (C == 0 && p.iface_side < 0 && iz == N) {
-        a -= t.sigv * T.ksig[N];   // coarse-side layer term on the shared plane z = N
+    }
+    // SIPG layer terms (Eq. 7): fine side on the last element layer, coarse side on the first
+    if constexpr (F & kLast) {
+        if (p.iface_side > 0 && t.valid) {
+            a -= __ldg(p.sig + t.fc) * T.ksig[C];
+            if constexpr (C == N) a -= __ldg(p.tau + t.fc) * T.ktau[N];
+        }
+    }
+    if constexpr (F & kFirst) {
+        if (p.iface_side < 0 && t.valid) {
+            a -= __ldg(p.sig + t.fc) * T.ksig[C];
+            if constexpr (C == 0) a -= __ldg(p.tau + t.fc) * T.ktau[0];
+        }
+    } else if constexpr (C == 0) {
+        if (p.iface_side < 0 && ez == 1 && t.valid)
+            a -= __ldg(p.sig + t.fc) * T.ksig[N];   // shared plane z = N of the first layer
     }
     a = fma(-damp, wv, a);
     const double wn = fma(p.dt, a, wv);
@@ -190,59 +237,59 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
 
 // One element layer: planes z0 .. z0+N-1 (plus the top plane N nel_z on the last layer), unrolled by
 // compile-time recursion over the local plane index C so that every z row and window index is a
-// constant.
-template <int N, int TY, bool EDGE, int C>
+// constant.  cur tracks the ring position of plane iz.
+template <int N, int TY, int F, int C>
 __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
-                                               uint32_t bars, int ez, bool last, int tx0, int ty0, double t1,
-                                               const double (&zw)[2 * N + 1], double (&nxt)[N], double*& outP,
-                                               double*& outW) {
-    if constexpr (C <= N) {
+                                               uint32_t bars, int ez, int tx0, int ty0, const double (&zw)[2 * N + 1],
+                                               double*& outP, double*& outW, RingPos& cur) {
+    if constexpr (C < N || (C == N && (F & kLast))) {
         using G = VolGeo<N, TY>;
-        if (C == N && !last) return;
         const int NZ = (int)p.NZ;
-        const int z0 = N * ez;
-        const int iz = z0 + C;
-        if constexpr (C < N) {   // the next layer's plane z0 + N + 1 + C into the window queue
-            const int zn = z0 + N + 1 + C;
-            nxt[C] = 0.0;
-            if (zn < NZ) {
-                const int sn = zn % G::D;
-                mbar_wait(bars + 8u * sn, (uint32_t)((zn / G::D) & 1));
-                nxt[C] = reinterpret_cast<const double*>(ring + sn * G::SLOT)[t.own];
-            }
-        }
-        const int sl = iz % G::D;
-        const double* sP = reinterpret_cast<const double*>(ring + sl * G::SLOT);
-        const double* sW = reinterpret_cast<const double*>(ring + sl * G::SLOT + G::POFF);
-        vol_plane<N, TY, C, EDGE>(p, t, sP, sW, zw, iz, ez, t1, outP, outW);
+        const int iz = N * ez + C;
+        const double* sP = reinterpret_cast<const double*>(ring + cur.slot * G::SLOT);
+        const double* sW = reinterpret_cast<const double*>(ring + cur.slot * G::SLOT + G::POFF);
+        vol_plane<N, TY, C, F>(p, t, sP, sW, zw, ez, outP, outW);
         const long long PS = p.PX * p.NY;
         outP += PS;
         outW += PS;
-        __syncthreads();   // every warp is done with slot sl: refill it with plane iz + D
-        if (threadIdx.x == 0 && threadIdx.y == 0 && iz + G::D < NZ)
-            vol_issue<N, TY>(p, ring, bars, sl, iz + G::D, tx0, ty0);
-        vol_layer_step<N, TY, EDGE, C + 1>(p, t, ring, bars, ez, last, tx0, ty0, t1, zw, nxt, outP, outW);
+        __syncthreads();   // every warp is done with this slot: refill it with plane iz + D
+        // the producer rotates over the warps so no warp carries every TMA issue
+        if (threadIdx.y == (iz % TY) && threadIdx.x == 0 && iz + G::D < NZ)
+            vol_issue<N, TY>(p, ring, bars, cur.slot, iz + G::D, tx0, ty0);
+        cur.template advance<G::D>();
+        vol_layer_step<N, TY, F, C + 1>(p, t, ring, bars, ez, tx0, ty0, zw, outP, outW, cur);
     }
 }
 
-template <int N, int TY, bool EDGE>
+// Layer, then slide the window: zw <- planes z0 .. z0 + 2N (read from the ring; plane z0+N+1+j is
+// resident because slots are only refilled after their own plane has been processed).
+template <int N, int TY, int F>
 __device__ __forceinline__ void vol_layer(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
-                                          uint32_t bars, int ez, int tx0, int ty0, double t1, double (&zw)[2 * N + 1],
-                                          double*& outP, double*& outW) {
-    double nxt[N];
-    const bool last = (ez == p.nelz - 1);
-    vol_layer_step<N, TY, EDGE, 0>(p, t, ring, bars, ez, last, tx0, ty0, t1, zw, nxt, outP, outW);
+                                          uint32_t bars, int ez, int tx0, int ty0, double (&zw)[2 * N + 1],
+                                          double*& outP, double*& outW, RingPos& cur, RingPos& nx) {
+    using G = VolGeo<N, TY>;
+    vol_layer_step<N, TY, F, 0>(p, t, ring, bars, ez, tx0, ty0, zw, outP, outW, cur);
+    if constexpr (!(F & kLast)) {
 #pragma unroll
-    for (int k = 0; k <= N; ++k) zw[k] = zw[k + N];
+        for (int k = 0; k <= N; ++k) zw[k] = zw[k + N];
+        const int NZ = (int)p.NZ;
 #pragma unroll
-    for (int j = 0; j < N; ++j) zw[N + 1 + j] = nxt[j];
+        for (int j = 0; j < N; ++j) {
+            zw[N + 1 + j] = 0.0;
+            if (N * ez + N + 1 + j < NZ) {
+                mbar_wait(bars + 8u * nx.slot, nx.par);
+                zw[N + 1 + j] = reinterpret_cast<const double*>(ring + nx.slot * G::SLOT)[t.own];
+            }
+            nx.template advance<G::D>();
+        }
+    }
 }
 
 template <int N, int TY>
 __global__ void __launch_bounds__(32 * TY) vol_kernel(const __grid_constant__ VolParams p) {
     using G = VolGeo<N, TY>;
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char* ring = smem_raw;   // direct indexing keeps the shared address space (LDS, not generic LD)
     const uint32_t bars = smem_u32(ring + G::D * G::SLOT);
     const int lane = threadIdx.x, ly = threadIdx.y;
     const int tx0 = blockIdx.x * G::TXE, ty0 = blockIdx.y * TY;
@@ -274,43 +321,29 @@ __global__ void __launch_bounds__(32 * TY) vol_kernel(const __grid_constant__ Vo
     }
     t.xb = (ly + N) * G::SW + (node_lane ? lane - a + G::NH : G::NH - N);
     const int ay = (int)(iy % N);
-    int ryR = -1;
+    t.ry = -1;
     t.yLf = 0;
     if (iy < NY) {
-        if (iy == 0) ryR = row_B0(N);
-        else if (iy < NY - 1) ryR = ay;
+        if (iy == 0) t.ry = row_B0(N);
+        else if (iy < NY - 1) t.ry = ay;
         if (ay == 0 && iy > 0) t.yLf = (iy == NY - 1) ? 2 : 1;
     }
 #pragma unroll
-    for (int b = 0; b <= N; ++b) {
-        t.cR[b] = rxR >= 0 ? T.G[0][rxR][b] : 0.0;
-        t.cyR[b] = ryR >= 0 ? T.G[1][ryR][b] : 0.0;
-    }
+    for (int b = 0; b <= N; ++b) t.cR[b] = rxR >= 0 ? T.G[0][rxR][b] : 0.0;
     const int col = node_lane ? lane + G::NH : 0;
     t.own = (ly + N) * G::SW + col;
     t.wown = ly * G::WW + (node_lane ? lane : 0);
     t.yb = (ly + N - ay) * G::SW + col;
     t.yl = ly * G::SW + col;
     t.dxy = 0.0;
-    t.fv = t.tauv = t.sigv = t.pwx = t.pwy = 0.0;
+    t.fc = t.valid ? (int)(iy * NX + ix) : 0;
     if (t.valid) {
         if (ix == 0) t.dxy += p.damp[0];
         if (ix == NX - 1) t.dxy += p.damp[1];
         if (iy == 0) t.dxy += p.damp[2];
         if (iy == NY - 1) t.dxy += p.damp[3];
-        const long long fc = iy * NX + ix;
-        if (p.F) t.fv = p.F[fc];
-        if (p.iface_side != 0) {
-            t.tauv = p.tau[fc];
-            t.sigv = p.sig[fc];
-        }
-        if (p.pw_on) {
-            t.pwx = p.xc[ix];
-            t.pwy = p.yc[iy];
-        }
     }
-    const long long n = __ldcg(p.step);
-    const double t1 = (double)(n + 1) * p.dt;
+    const long long n0 = __ldcg(p.step);   // step index of this launch (bumped by the last block)
     const long long off = t.valid ? iy * p.PX + ix : 0;
     double* outP = p.Pn + off;
     double* outW = p.W + off;
@@ -329,11 +362,14 @@ __global__ void __launch_bounds__(32 * TY) vol_kernel(const __grid_constant__ Vo
     }
 
     const int nelz = p.nelz;
-    for (int ez = 0; ez < nelz; ++ez) {
-        if (ez == 0 || ez == nelz - 1)
-            vol_layer<N, TY, true>(p, t, ring, bars, ez, tx0, ty0, t1, zw, outP, outW);
-        else
-            vol_layer<N, TY, false>(p, t, ring, bars, ez, tx0, ty0, t1, zw, outP, outW);
+    RingPos cur{0, 0u}, nx{(N + 1) % G::D, (uint32_t)(((N + 1) / G::D) & 1)};
+    if (nelz == 1) {
+        vol_layer<N, TY, kFirst | kLast>(p, t, ring, bars, 0, tx0, ty0, zw, outP, outW, cur, nx);
+    } else {
+        vol_layer<N, TY, kFirst>(p, t, ring, bars, 0, tx0, ty0, zw, outP, outW, cur, nx);
+        for (int ez = 1; ez < nelz - 1; ++ez)
+            vol_layer<N, TY, 0>(p, t, ring, bars, ez, tx0, ty0, zw, outP, outW, cur, nx);
+        vol_layer<N, TY, kLast>(p, t, ring, bars, nelz - 1, tx0, ty0, zw, outP, outW, cur, nx);
     }
 
     if (p.bump_step) {
@@ -341,7 +377,7 @@ __global__ void __launch_bounds__(32 * TY) vol_kernel(const __grid_constant__ Vo
             __threadfence();
             const unsigned prev = atomicAdd(p.done, 1u);
             if (prev == p.total_blocks - 1) {
-                *p.step = n + 1;
+                *p.step = n0 + 1;
                 *p.done = 0u;
                 __threadfence();
             }

@@ -40,9 +40,9 @@ __host__ __device__ constexpr int vol_smem_bytes(int N, int TY) {
 //   L     interior shared node (a = 0), left element, base = i - N
 //   B0    box lower boundary node (i = 0), right element only
 //   BN    box upper boundary node (i = N nel), left element only
-__host__ __device__ inline int row_L(int N) { return N; }
-__host__ __device__ inline int row_B0(int N) { return N + 1; }
-__host__ __device__ inline int row_BN(int N) { return N + 2; }
+__host__ __device__ constexpr int row_L(int N) { return N; }
+__host__ __device__ constexpr int row_B0(int N) { return N + 1; }
+__host__ __device__ constexpr int row_BN(int N) { return N + 2; }
 
 // Per-box coefficient tables, passed by value inside VolParams (kernel parameter constant bank,
 // per launch: contexts never share them).
