@@ -29,6 +29,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -252,10 +255,10 @@ __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThre
         const long long PS = p.PX * p.NY;
         outP += PS;
         outW += PS;
-        __syncthreads();   // every warp is done with this slot: refill it with plane iz + D
-        // the producer rotates over the warps so no warp carries every TMA issue
-        if (threadIdx.y == (iz % TY) && threadIdx.x == 0 && iz + G::D < NZ)
-            vol_issue<N, TY>(p, ring, bars, cur.slot, iz + G::D, tx0, ty0);
+        // release the slot: one arrival per consumer warp on its "empty" barrier (no block-wide
+        // barrier: warps drift across planes and hide each other's latency; the producer warp refills)
+        __syncwarp();
+        if (threadIdx.x == 0) mbar_arrive(bars + 8u * (G::D + cur.slot));
         cur.template advance<G::D>();
         vol_layer_step<N, TY, F, C + 1>(p, t, ring, bars, ez, tx0, ty0, zw, outP, outW, cur);
     }
@@ -285,8 +288,10 @@ __device__ __forceinline__ void vol_layer(const VolParams& p, const VolThread<N>
     }
 }
 
+// Block = TY consumer warps (one tile row each) + 1 producer warp (threadIdx.y == TY) that streams the
+// planes with TMA as soon as all consumers released a ring slot.
 template <int N, int TY>
-__global__ void __launch_bounds__(32 * TY) vol_kernel(const __grid_constant__ VolParams p) {
+__global__ void __launch_bounds__(32 * (TY + 1)) vol_kernel(const __grid_constant__ VolParams p) {
     using G = VolGeo<N, TY>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char* ring = smem_raw;   // direct indexing keeps the shared address space (LDS, not generic LD)
@@ -297,13 +302,30 @@ __global__ void __launch_bounds__(32 * TY) vol_kernel(const __grid_constant__ Vo
     const int NZ = (int)p.NZ;
 
     if (lane == 0 && ly == 0) {
-        for (int s = 0; s < G::D; ++s) mbar_init(bars + 8u * s, 1);
+        for (int s = 0; s < G::D; ++s) {
+            mbar_init(bars + 8u * s, 1);               // full: TMA transaction bytes
+            mbar_init(bars + 8u * (G::D + s), TY);     // empty: one arrival per consumer warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
-    if (lane == 0 && ly == 0)
-        for (int s = 0; s < G::D && s < NZ; ++s) vol_issue<N, TY>(p, ring, bars, s, s, tx0, ty0);
+    if (ly == TY) {   // producer warp
+        if (lane == 0) {
+            for (int z = 0; z < G::D && z < NZ; ++z) vol_issue<N, TY>(p, ring, bars, z, z, tx0, ty0);
+            int slot = 0;
+            uint32_t par = 0;
+            for (int z = G::D; z < NZ; ++z) {   // plane z reuses the slot of plane z - D
+                mbar_wait(bars + 8u * (G::D + slot), par);
+                vol_issue<N, TY>(p, ring, bars, slot, z, tx0, ty0);
+                if (++slot == G::D) {
+                    slot = 0;
+                    par ^= 1u;
+                }
+            }
+        }
+        return;
+    }
 
     // ---- thread setup (overlaps the first TMA loads)
     const BoxTables& T = p.tab;
@@ -385,7 +407,7 @@ __global__ void __launch_bounds__(32 * TY) vol_kernel(const __grid_constant__ Vo
     }
 }
 
-constexpr int kTY = 16;
+constexpr int kTY = 15;   // consumer rows per CTA (+1 producer warp = 512 threads)
 
 template <int N>
 static void prepare_vol_N() {
@@ -410,7 +432,7 @@ template <int N>
 static void launch_vol_N(const VolParams& p, cudaStream_t s) {
     using G = VolGeo<N, kTY>;
     const int smem = vol_smem_bytes(N, kTY);
-    dim3 blk(32, kTY);
+    dim3 blk(32, kTY + 1);
     dim3 grd((unsigned)((p.NX + G::TXE - 1) / G::TXE), (unsigned)((p.NY + kTY - 1) / kTY));
     vol_kernel<N, kTY><<<grd, blk, smem, s>>>(p);
 }

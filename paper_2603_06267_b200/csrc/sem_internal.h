@@ -32,7 +32,7 @@ __host__ __device__ constexpr int vol_slot_bytes(int N, int TY) {
     return vol_pbytes_aligned(N, TY) + ((vol_wbox_w(N) * TY * 8 + 127) / 128) * 128;
 }
 __host__ __device__ constexpr int vol_smem_bytes(int N, int TY) {
-    return vol_depth(N) * vol_slot_bytes(N, TY) + vol_depth(N) * 8 + 128;
+    return vol_depth(N) * vol_slot_bytes(N, TY) + 2 * vol_depth(N) * 8 + 128;   // ring + full/empty barriers
 }
 
 // Row-class indices inside a direction table.
