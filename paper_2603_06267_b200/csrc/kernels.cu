@@ -16,7 +16,16 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "gll_constexpr.h"
 #include "sem_internal.h"
+
+// Volume-kernel tiling (tuned on B200, see profiles/): consumer rows per CTA and minimum CTAs per SM.
+#ifndef SEM_KTY
+#define SEM_KTY 11
+#endif
+#ifndef SEM_MINB
+#define SEM_MINB 1
+#endif
 
 namespace sem {
 
@@ -86,9 +95,10 @@ __device__ __forceinline__ void vol_issue(const VolParams& p, unsigned char* rin
 // Per-thread state of the volume kernel.
 template <int N>
 struct VolThread {
-    double cR[N + 1];     // x row of this lane's node (right element, or B0); zeros if none
-    int ry;               // y row class (warp-uniform): 0..N-1, row_B0, or -1 (upper boundary: left only)
-    double fL;            // factor on the left-element x row received from lane-1 (0, 1, or 2 at BN)
+    double cR[N + 1];     // x row of this lane's node (right element, or B0), scaled; zeros if none
+    double cyR[N + 1];    // y row of this warp's node row (right element or B0), scaled; zeros if none
+    double fL;            // s_x * factor on the left-element x row received from lane-1 (0, 1, or 2 at BN)
+    double yLs;           // s_y * factor on the left-element y row (0, 1, or 2 at BN), warp-uniform
     double dxy;           // lateral ABC C_ii / M_ii
     int fc;               // face-lattice index iy NX + ix (edge-layer inputs are loaded on demand)
     int xb;               // smem column of the right element's first node (lane 31: left element of lane 0)
@@ -96,7 +106,6 @@ struct VolThread {
     int wown;             // smem offset in the W plane
     int yb;               // smem offset of the right element's first row (x col of the own node)
     int yl;               // smem offset of the left element's first row
-    int yLf;              // left-element y row factor (0, 1, 2), warp-uniform
     bool valid;
 };
 
@@ -113,27 +122,9 @@ struct RingPos {
     }
 };
 
-template <int N, int TY, int R>
-__device__ __forceinline__ double y_row(const BoxTables& T, const double* __restrict__ s) {
-    using G = VolGeo<N, TY>;
-    double y0 = 0.0, y1 = 0.0;
-#pragma unroll
-    for (int b = 0; b <= N; b += 2) y0 = fma(T.G[1][R][b], s[b * G::SW], y0);
-#pragma unroll
-    for (int b = 1; b <= N; b += 2) y1 = fma(T.G[1][R][b], s[b * G::SW], y1);
-    return y0 + y1;
-}
-
-template <int N, int TY, int R = 0>
-__device__ __forceinline__ double y_row_dispatch(const BoxTables& T, int ry, const double* __restrict__ s) {
-    if constexpr (R < N) {
-        if (ry == R) return y_row<N, TY, R>(T, s);
-        return y_row_dispatch<N, TY, R + 1>(T, ry, s);
-    } else {
-        if (ry == row_B0(N)) return y_row<N, TY, row_B0(N)>(T, s);
-        return 0.0;
-    }
-}
+// compile-time reference rows, materialised as device constants (folded for constant indices)
+template <int N>
+__device__ constexpr gllc::Tables<N> kRef = gllc::make_tables<N>();
 
 // Layer kinds (compile time): bit 0 = first element layer (z = 0 face), bit 1 = last (z = N nel_z face).
 constexpr int kFirst = 1, kLast = 2;
@@ -145,7 +136,20 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
                                           double* __restrict__ outP, double* __restrict__ outW) {
     using G = VolGeo<N, TY>;
     const BoxTables& T = p.tab;
-    // ---- x: right-element row with per-lane coefficients, left-element row (uniform) by lane-1
+#ifdef SEM_MEMONLY   // diagnostic build: same data movement, no stencil arithmetic
+    {
+        const double wv = sW[t.wown];
+        const double pv = zw[N + C];
+        if (t.valid) {
+            __stcs(outW, wv);
+            __stcs(outP, fma(p.dt, wv, pv));
+        }
+        return;
+    }
+#endif
+    // ---- x: right-element row with per-lane (scaled) coefficients; the left-element row of a shared
+    //      node uses the compile-time reference row L and is evaluated by lane-1, then shuffled
+    const auto& RT = kRef<N>;
     double v[N + 1];
 #pragma unroll
     for (int b = 0; b <= N; ++b) v[b] = sP[t.xb + b];
@@ -153,44 +157,47 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
 #pragma unroll
     for (int b = 0; b <= N; ++b) {
         xr = fma(t.cR[b], v[b], xr);
-        xl = fma(T.G[0][row_L(N)][b], v[b], xl);
+        xl = fma(RT.L[b], v[b], xl);
     }
     const double xlr = __shfl_sync(0xffffffffu, xl, (threadIdx.x + 31) & 31);
-    // ---- y: warp-uniform row class dispatched to compile-time rows (constant-bank coefficients)
-    const double yr = y_row_dispatch<N, TY>(T, t.ry, sP + t.yb);
-    double acc = fma(t.fL, xlr, xr) + yr;
-    if (t.yLf) {
+    // ---- y: per-warp row (registers, scaled); left row of a shared node: reference L, scaled
+    double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+    for (int b = 0; b <= N; b += 2) y0 = fma(t.cyR[b], sP[t.yb + b * G::SW], y0);
+#pragma unroll
+    for (int b = 1; b <= N; b += 2) y1 = fma(t.cyR[b], sP[t.yb + b * G::SW], y1);
+    double acc = fma(t.fL, xlr, xr) + (y0 + y1);
+    if (t.yLs != 0.0) {
         double yl = 0.0;
 #pragma unroll
-        for (int b = 0; b <= N; ++b) yl = fma(T.G[1][row_L(N)][b], sP[t.yl + b * G::SW], yl);
-        acc = fma(t.yLf == 2 ? 2.0 : 1.0, yl, acc);
+        for (int b = 0; b <= N; ++b) yl = fma(RT.L[b], sP[t.yl + b * G::SW], yl);
+        acc = fma(t.yLs, yl, acc);
     }
-    // ---- z: register window zw[k] = p(z0 - N + k), compile-time rows
+    // ---- z: register window zw[k] = p(z0 - N + k), compile-time reference rows, scaled once
     double z0 = 0.0, z1 = 0.0;
     if constexpr (C == N) {   // top boundary plane: left element only, BN = 2 L
 #pragma unroll
-        for (int b = 0; b <= N; b += 2) z0 = fma(T.G[2][row_L(N)][b], zw[N + b], z0);
+        for (int b = 0; b <= N; b += 2) z0 = fma(2.0 * RT.L[b], zw[N + b], z0);
 #pragma unroll
-        for (int b = 1; b <= N; b += 2) z1 = fma(T.G[2][row_L(N)][b], zw[N + b], z1);
-        z0 = 2.0 * z0;
-        z1 = 2.0 * z1;
-    } else if constexpr (C == 0 && (F & kFirst)) {
+        for (int b = 1; b <= N; b += 2) z1 = fma(2.0 * RT.L[b], zw[N + b], z1);
+    } else if constexpr (C == 0 && (F & kFirst)) {   // bottom boundary plane: B0 = 2 R0
 #pragma unroll
-        for (int b = 0; b <= N; b += 2) z0 = fma(T.G[2][row_B0(N)][b], zw[N + b], z0);
+        for (int b = 0; b <= N; b += 2) z0 = fma(2.0 * RT.R[0][b], zw[N + b], z0);
 #pragma unroll
-        for (int b = 1; b <= N; b += 2) z1 = fma(T.G[2][row_B0(N)][b], zw[N + b], z1);
+        for (int b = 1; b <= N; b += 2) z1 = fma(2.0 * RT.R[0][b], zw[N + b], z1);
     } else if constexpr (C == 0) {
 #pragma unroll
-        for (int b = 0; b <= N; ++b) z0 = fma(T.G[2][0][b], zw[N + b], z0);
+        for (int b = 0; b <= N; ++b) z0 = fma(RT.R[0][b], zw[N + b], z0);
 #pragma unroll
-        for (int b = 0; b <= N; ++b) z1 = fma(T.G[2][row_L(N)][b], zw[b], z1);
+        for (int b = 0; b <= N; ++b) z1 = fma(RT.L[b], zw[b], z1);
     } else {
 #pragma unroll
-        for (int b = 0; b <= N; b += 2) z0 = fma(T.G[2][C][b], zw[N + b], z0);
+        for (int b = 0; b <= N; b += 2) z0 = fma(RT.R[C][b], zw[N + b], z0);
 #pragma unroll
-        for (int b = 1; b <= N; b += 2) z1 = fma(T.G[2][C][b], zw[N + b], z1);
+        for (int b = 1; b <= N; b += 2) z1 = fma(RT.R[C][b], zw[N + b], z1);
     }
-    double a = -(acc + (z0 + z1));
+    acc = fma(p.sdir[2], z0 + z1, acc);
+    double a = -acc;
     const double wv = sW[t.wown];
     const double pv = zw[N + C];
     double damp = t.dxy;
@@ -291,7 +298,7 @@ __device__ __forceinline__ void vol_layer(const VolParams& p, const VolThread<N>
 // Block = TY consumer warps (one tile row each) + 1 producer warp (threadIdx.y == TY) that streams the
 // planes with TMA as soon as all consumers released a ring slot.
 template <int N, int TY>
-__global__ void __launch_bounds__(32 * (TY + 1)) vol_kernel(const __grid_constant__ VolParams p) {
+__global__ void __launch_bounds__(32 * (TY + 1), SEM_MINB) vol_kernel(const __grid_constant__ VolParams p) {
     using G = VolGeo<N, TY>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char* ring = smem_raw;   // direct indexing keeps the shared address space (LDS, not generic LD)
@@ -316,7 +323,7 @@ __global__ void __launch_bounds__(32 * (TY + 1)) vol_kernel(const __grid_constan
             int slot = 0;
             uint32_t par = 0;
             for (int z = G::D; z < NZ; ++z) {   // plane z reuses the slot of plane z - D
-                mbar_wait(bars + 8u * (G::D + slot), par);
+                while (!mbar_try_wait(bars + 8u * (G::D + slot), par)) __nanosleep(64);   // leave issue slots to consumers
                 vol_issue<N, TY>(p, ring, bars, slot, z, tx0, ty0);
                 if (++slot == G::D) {
                     slot = 0;
@@ -343,15 +350,19 @@ __global__ void __launch_bounds__(32 * (TY + 1)) vol_kernel(const __grid_constan
     }
     t.xb = (ly + N) * G::SW + (node_lane ? lane - a + G::NH : G::NH - N);
     const int ay = (int)(iy % N);
-    t.ry = -1;
-    t.yLf = 0;
+    int ryR = -1;
+    t.yLs = 0.0;
     if (iy < NY) {
-        if (iy == 0) t.ry = row_B0(N);
-        else if (iy < NY - 1) t.ry = ay;
-        if (ay == 0 && iy > 0) t.yLf = (iy == NY - 1) ? 2 : 1;
+        if (iy == 0) ryR = row_B0(N);
+        else if (iy < NY - 1) ryR = ay;
+        if (ay == 0 && iy > 0) t.yLs = (iy == NY - 1) ? 2.0 * p.sdir[1] : p.sdir[1];
     }
+    t.fL *= p.sdir[0];
 #pragma unroll
-    for (int b = 0; b <= N; ++b) t.cR[b] = rxR >= 0 ? T.G[0][rxR][b] : 0.0;
+    for (int b = 0; b <= N; ++b) {
+        t.cR[b] = rxR >= 0 ? T.G[0][rxR][b] : 0.0;
+        t.cyR[b] = ryR >= 0 ? T.G[1][ryR][b] : 0.0;
+    }
     const int col = node_lane ? lane + G::NH : 0;
     t.own = (ly + N) * G::SW + col;
     t.wown = ly * G::WW + (node_lane ? lane : 0);
@@ -407,7 +418,7 @@ __global__ void __launch_bounds__(32 * (TY + 1)) vol_kernel(const __grid_constan
     }
 }
 
-constexpr int kTY = 15;   // consumer rows per CTA (+1 producer warp = 512 threads)
+constexpr int kTY = SEM_KTY;   // consumer rows per CTA (+1 producer warp)
 
 template <int N>
 static void prepare_vol_N() {

@@ -250,6 +250,7 @@ sem::VolParams vol_params(sem_ctx* ctx, int bi, int cur) {
     p.NY = b.NY;
     p.NZ = b.NZ;
     p.PX = b.PX;
+    for (int d = 0; d < 3; ++d) p.sdir[d] = b.d.c * b.d.c * (2.0 / b.h[d]) * (2.0 / b.h[d]);
     p.nelz = b.d.nel[2];
     p.dt = ctx->dt;
     std::vector<double> x, w;

@@ -13,7 +13,10 @@ namespace sem {
 constexpr int kMaxN = 8;          // supported GLL degrees 1..8
 constexpr int kRows = kMaxN + 3;  // row classes per direction: R[0..N-1], L, B0, BN
 constexpr int kMaxModes = 8;
-constexpr int kPref = 3;          // volume kernel: planes prefetched beyond the z-stencil window
+#ifndef SEM_KPREF
+#define SEM_KPREF 6
+#endif
+constexpr int kPref = SEM_KPREF;  // volume kernel: planes prefetched beyond the z-stencil window
 
 // Volume kernel tile geometry for degree N: one warp spans a row of
 // TXE = N floor(31/N) computed nodes (whole elements); lane 31 is the "virtual left neighbour"
@@ -63,6 +66,7 @@ struct VolParams {
     double* __restrict__ W;         // w^n in, w^{n+1} out (in place)
     long long NX, NY, NZ;           // node counts of the (local) box
     long long PX;                   // row pitch (doubles) of the device layout
+    double sdir[3];                 // s_d = c^2 (2/h_d)^2: scale of the compile-time reference rows
     int nelz;
     double dt;
     // lumped ABC: C_ii / M_ii at boundary nodes of absorbing faces (0 if rigid)

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsem.so")
+LIB_PATH = os.environ.get("SEM_LIB") or os.path.join(_HERE, "lib", "libsem.so")
 
 SEM_F_COUPLING_LITERAL = 1 << 0
 SEM_F_NAN_CHECK = 1 << 1
