@@ -323,7 +323,9 @@ class System:
         # reference point: the face corner the wavefront reaches first (min k.x), reading R13
         corners = np.array([[x, y, self.pw_xyz[0, 2]] for x in (self.pw_xyz[:, 0].min(), self.pw_xyz[:, 0].max())
                             for y in (self.pw_xyz[:, 1].min(), self.pw_xyz[:, 1].max())])
-        self.pw_xref = corners[np.argmin(corners @ kd)]
+        # a lateral crop of a larger box (tests) passes the full box's reference corner explicitly
+        self.pw_xref = (np.asarray(pw["x_ref"], dtype=np.float64) if pw.get("x_ref") is not None
+                        else corners[np.argmin(corners @ kd)])
         self.pw_k = kd
         self.pw_n = nrm
         self.pw_c = box.c
