@@ -156,18 +156,28 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from paper_2603_06267_b200.sem import (Simulation, sem_kernel_time, sem_last_launch_count, sem_read_modal,
-                                           sem_read_pressure_ptr, sem_set_profiling, sem_write_state_ptr)
+    from paper_2603_06267_b200.sem import (SEM_F_NO_GRAPH, Simulation, sem_kernel_time, sem_last_launch_count,
+                                           sem_nccl_unique_id, sem_read_modal, sem_read_pressure_ptr,
+                                           sem_set_profiling, sem_write_state_ptr)
     from sem_inputs import config
 
     rec = config(args.config)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     nccl_id = None
+    flags = 0
     if world > 1:
-        raise SystemExit("slab decomposition not built into libsem yet")
-    sim = Simulation(rec, device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_unique_id=nccl_id)
-    ndof_total = sum(sim.ndof)
+        # x-slab decomposition: libsem's own NCCL communicator for the per-step
+        # cut-plane exchange; the id is created on rank 0 and broadcast through torch.distributed
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(sem_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+        flags |= SEM_F_NO_GRAPH
+    sim = Simulation(rec, device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_unique_id=nccl_id,
+                     flags=flags)
+    ndof_total = sum(sim.ndof)      # global node count (every rank holds one x-slab of it)
 
     # ---- device-resident timed region ----------------------------------------------------------
     sim.step(args.warmup)
@@ -197,11 +207,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = ndof_total * world * args.steps / (ms / 1e3) / 1e9
+    value = ndof_total * args.steps / (ms / 1e3) / 1e9     # strong scaling: fixed global problem
 
     peak, peak_kind = _peaks()
     vol_step_ms = vol_ms / max(vol_n, 1)
-    achieved = BYTES_PER_DOF * ndof_total / (vol_step_ms / 1e3) / 1e9
+    achieved = BYTES_PER_DOF * ndof_total / world / (vol_step_ms / 1e3) / 1e9   # this rank's slab
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}.json")
     if os.path.exists(tpath):
@@ -227,11 +237,15 @@ def main():
         sim.step(args.steps)
         launches_e2e = sem_last_launch_count(sim.ctx)
         for b in range(len(sim.ndof)):
-            sem_read_pressure_ptr(sim.ctx, b, ho[b].data_ptr(), sim.ndof[b])
+            sem_read_pressure_ptr(sim.ctx, b, ho[b].data_ptr(), sim.ndof[b])   # collective: rank 0 assembles
         if nm:
             sem_read_modal(sim.ctx, nm)
         torch.cuda.synchronize()
         t_e2e = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
         h2d = 16.0 * ndof_total
         d2h = 8.0 * ndof_total + 16.0 * nm
         e2e = {"value": ndof_total * args.steps / t_e2e / 1e9, "unit": UNIT,

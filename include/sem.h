@@ -56,7 +56,10 @@ typedef enum {
 enum {
     SEM_F_COUPLING_LITERAL = 1 << 0, /* g(p^n, phi^n) exactly as printed (unstable at cfg masses)  */
     SEM_F_NAN_CHECK = 1 << 1,        /* check p for NaN/Inf after every sem_step call              */
-    SEM_F_NO_GRAPH = 1 << 2          /* launch kernels directly instead of a captured CUDA graph   */
+    SEM_F_NO_GRAPH = 1 << 2,         /* launch kernels directly instead of a captured CUDA graph   */
+    SEM_F_EMULATE_SLABS = 1 << 3     /* world > 1 in ONE context on one device: every x-slab of the
+                                        decomposition lives here and the per-step exchange is a
+                                        device copy instead of NCCL (verifies the slab path on 1 GPU) */
 };
 
 /* One axis-aligned box of hexahedral GLL elements of degree `degree` (1..8). */
@@ -76,16 +79,26 @@ typedef struct {
     double dt;                   /* time step [s], caller-computed (reading R8)          */
     int device;                  /* CUDA device ordinal                                  */
     void* stream;                /* cudaStream_t to enqueue on; NULL -> library stream   */
-    int rank, world;             /* slab decomposition along x; world == 1 -> no NCCL    */
+    int rank, world;             /* x-slab decomposition: rank's slab = elements
+                                    [r nel_x/world, (r+1) nel_x/world) of every box (nel_x must be
+                                    divisible by world; cuts must miss the membranes and align with
+                                    the coarse elements of an interface -> SEM_E_PARTITION)       */
     const void* nccl_unique_id;  /* ncclUniqueId (128 bytes) when world > 1, else NULL  */
     int flags;                   /* SEM_F_*                                              */
 } sem_mesh_desc;
 
 /* Create the context: validates boxes, builds the 1D GLL tables and allocates p (two time
- * levels), w = p' + dt/2 p'' (one level) per box, zero-initialised.
- * Errors: SEM_E_ARG (bad descriptor), SEM_E_PARTITION (world > 1 and nel_x not divisible),
- * SEM_E_CUDA / SEM_E_OOM.  *out is NULL on error. */
+ * levels), w = p' + dt/2 p'' (one level) per box (this rank's x-slab), zero-initialised
+ * (P:L609-610).  With world > 1 (and no SEM_F_EMULATE_SLABS) every rank calls it with the same
+ * global boxes and the ncclUniqueId from sem_nccl_unique_id on rank 0; each step then exchanges
+ * one cut plane per box with each x-neighbour.
+ * Errors: SEM_E_ARG (bad descriptor), SEM_E_PARTITION (nel_x not divisible by world),
+ * SEM_E_NCCL, SEM_E_CUDA / SEM_E_OOM.  *out is NULL on error. */
 sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out);
+
+/* 128-byte ncclUniqueId for world > 1 (rank 0 calls it and broadcasts the bytes).
+ * NCCL is loaded with dlopen("libnccl.so.2"); SEM_E_NCCL if it is unavailable. */
+sem_status sem_nccl_unique_id(void* out128);
 
 /* PMUT array on face `face` (only 4 = -z) of box `box` (Eqs. 2-3, 5, 11-12).
  * Mode shapes S_{k,m}(x,y) = sin(m pi x'/a) sin(n pi y'/a) on the square membrane of side a
@@ -138,15 +151,18 @@ sem_status sem_step(sem_ctx* ctx, int n_steps);
 /* Block until all enqueued work finished; reports asynchronous errors. */
 sem_status sem_sync(sem_ctx* ctx);
 
-/* p^S of box `box` after S steps into host[n] (n must equal the box's node count).
- * Synchronising.  Shared DG interface nodes are reported once per side. */
+/* p^S of box `box` after S steps into host[n] (n must equal the box's global node count).
+ * Synchronising.  Shared DG interface nodes are reported once per side.  With world > 1 this is
+ * collective: every rank calls it, rank 0 receives the assembled field (host may be NULL elsewhere). */
 sem_status sem_read_pressure(sem_ctx* ctx, int box, double* host, size_t n);
 
-/* p^S at n sampled node ids (layout above) of `box` into out[n] (host).  Synchronising. */
+/* p^S at n sampled global node ids (layout above) of `box` into out[n] (host).  Synchronising.
+ * Single-process only (world 1 or SEM_F_EMULATE_SLABS): SEM_E_STATE under NCCL. */
 sem_status sem_read_pressure_at(sem_ctx* ctx, int box, const long long* ids, size_t n, double* out);
 
-/* q^S, q'^S [n_pmut*n_modes] and phi_k(t^S) [n_pmut] (received voltage for RX, drive for TX).
- * n must equal n_pmut*n_modes.  Any pointer may be NULL.  Synchronising. */
+/* q^S, q'^S [n_pmut*n_modes] and phi_k(t^S) [n_pmut] (received voltage for RX, drive for TX), in
+ * the global PMUT order.  n must equal n_pmut*n_modes.  Any pointer may be NULL.  Synchronising;
+ * collective with world > 1 (rank 0 receives). */
 sem_status sem_read_modal(sem_ctx* ctx, double* q, double* qdot, double* v_rx, size_t n);
 
 /* Test hook: set p^0, p'^0 of `box` from host arrays [n] (p''^0 = 0; reading R20),

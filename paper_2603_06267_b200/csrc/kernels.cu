@@ -344,9 +344,11 @@ __global__ void __launch_bounds__(32 * (TY + 1), SEM_MINB) vol_kernel(const __gr
     int rxR = -1;
     t.fL = 0.0;
     if (t.valid) {
-        if (ix == 0) rxR = row_B0(N);
+        // box faces: B0 = 2 R0 / BN = 2 L; slab cuts (multi-GPU): the shared node keeps its interior
+        // rows R0 (right side) / L (left side) and the other side's part is added by cut_fixup_kernel
+        if (ix == 0) rxR = p.cutL ? 0 : row_B0(N);
         else if (ix < NX - 1) rxR = a;
-        if (a == 0 && ix > 0) t.fL = (ix == NX - 1) ? 2.0 : 1.0;
+        if (a == 0 && ix > 0) t.fL = (ix == NX - 1 && !p.cutR) ? 2.0 : 1.0;
     }
     t.xb = (ly + N) * G::SW + (node_lane ? lane - a + G::NH : G::NH - N);
     const int ay = (int)(iy % N);
@@ -675,6 +677,7 @@ __global__ void iface_gather_x(const __grid_constant__ IfaceParams p) {
     const int NfR = p.Nf * p.R;
     long long lo, hi;
     gather_range(jx, p.Nc, NfR, p.NXf, lo, hi);
+    if (p.skip_ix0 && lo == 0) lo = 1;   // the fine cut line is counted by the left slab only
     double s1 = 0.0, s2 = 0.0;
     for (long long ix = lo; ix <= hi; ++ix) {
         const double w = gather_weight(p, ix, jx, NfR, p.nelcx);
@@ -713,22 +716,71 @@ __device__ __forceinline__ double cb_uniform(unsigned long long seed, int box, i
 }
 
 __global__ void fill_random_kernel(double* pprev, double* w, double* pcur, long long NX, long long PX, long long rows,
-                                   unsigned long long seed, int box, double ps, double vs, double dt) {
+                                   long long gx0, long long NXg, unsigned long long seed, int box, double ps,
+                                   double vs, double dt) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= NX * rows) return;
     const long long ix = i % NX, r = i / NX, d = r * PX + ix;
-    const double p0 = ps * cb_uniform(seed, box, 0, i);
-    const double v0 = vs * cb_uniform(seed, box, 1, i);
+    const long long gid = (ix + gx0) + NXg * r;   // global lexicographic id (slab-independent field)
+    const double p0 = ps * cb_uniform(seed, box, 0, gid);
+    const double v0 = vs * cb_uniform(seed, box, 1, gid);
     pprev[d] = p0;
     w[d] = v0;
     pcur[d] = p0 + dt * v0;     // p^1 = p^0 + dt p'^0 (+ dt^2/2 p''^0 = 0)
 }
 
 void launch_fill_random(double* pprev, double* w, double* pcur, long long NX, long long PX, long long rows,
-                        unsigned long long seed, int box, double ps, double vs, double dt, cudaStream_t s) {
+                        long long gx0, long long NXg, unsigned long long seed, int box, double ps, double vs, double dt,
+                        cudaStream_t s) {
     const long long n = NX * rows;
-    fill_random_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pprev, w, pcur, NX, PX, rows, seed, box, ps, vs,
-                                                                   dt);
+    fill_random_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pprev, w, pcur, NX, PX, rows, gx0, NXg, seed, box,
+                                                                   ps, vs, dt);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Slab decomposition along x (multi-GPU): partial rows at the cut planes and the fix-up after the
+// exchange.  A shared cut node's x row is R0 (right slab) + L (left slab); each
+// slab evaluates its own part inside vol_kernel and sends it to the neighbour, which adds it here.
+// ------------------------------------------------------------------------------------------------
+__global__ void cut_partial_kernel(const CutParams c) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long n = c.NY * c.NZ;
+    if (i < n) {
+        const long long iy = i % c.NY, iz = i / c.NY;
+        const double* col = c.P + (iz * c.NY + iy) * c.PX + (c.side ? c.NX - 1 - c.N : 0);
+        double s = 0.0;
+        for (int b = 0; b <= c.N; ++b) s = fma(c.row[b], col[b], s);
+        c.out[i] = s;
+    } else if (i < n + c.NYt) {   // coarse SIPG partial sums at the cut column
+        const long long jy = i - n;
+        const long long jx = c.side ? c.NXt - 1 : 0;
+        c.out[n + jy] = c.tau[jy * c.NXt + jx];
+        c.out[n + c.NYt + jy] = c.sig[jy * c.NXt + jx];
+    }
+}
+
+__global__ void cut_fixup_kernel(const CutParams c) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long n = c.NY * c.NZ;
+    if (i >= n) return;
+    const long long iy = i % c.NY, iz = i / c.NY;
+    double da = -c.in[i];
+    if (c.NYt > 0 && iz <= c.N)   // coarse-side SIPG layer terms of the neighbour's fine points
+        da -= c.in[n + iy] * c.ktau[iz] + c.in[n + c.NYt + iy] * c.ksig[iz];
+    const long long d = (iz * c.NY + iy) * c.PX + (c.side ? c.NX - 1 : 0);
+    const double dw = c.dt * da;
+    c.W[d] += dw;
+    c.Pn[d] = fma(c.dt, dw, c.Pn[d]);
+}
+
+void launch_cut_partial(const CutParams& c, cudaStream_t s) {
+    const long long n = c.NY * c.NZ + c.NYt;
+    cut_partial_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c);
+}
+
+void launch_cut_fixup(const CutParams& c, cudaStream_t s) {
+    const long long n = c.NY * c.NZ;
+    cut_fixup_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c);
 }
 
 __global__ void set_state_kernel(const double* pprev, double* pcur, const double* w, long long NX, long long PX,
@@ -745,18 +797,13 @@ void launch_set_state(const double* pprev, double* pcur, const double* w, long l
     set_state_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pprev, pcur, w, NX, PX, rows, dt);
 }
 
-__global__ void gather_kernel(const double* src, const long long* ids, long long n, long long NX, long long PX,
-                              double* out) {
+__global__ void gather_kernel(const double* src, const long long* idx, long long n, double* out) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
-        const long long id = ids[i];
-        out[i] = src[(id / NX) * PX + id % NX];
-    }
+    if (i < n) out[i] = src[idx[i]];
 }
 
-void launch_gather(const double* src, const long long* ids, long long n, long long NX, long long PX, double* out,
-                   cudaStream_t s) {
-    gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, ids, n, NX, PX, out);
+void launch_gather(const double* src, const long long* idx, long long n, double* out, cudaStream_t s) {
+    gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, idx, n, out);
 }
 
 __global__ void nonfinite_kernel(const double* p, long long NX, long long PX, long long rows, unsigned long long* flag) {

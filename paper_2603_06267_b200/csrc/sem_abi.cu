@@ -5,6 +5,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -15,10 +17,6 @@
 #include <vector>
 
 #include "sem_internal.h"
-
-namespace sem {
-int volume_tile_y();
-}
 
 using sem::Box;
 
@@ -238,8 +236,88 @@ sem_status check_box(sem_ctx* ctx, const sem_box_desc& d) {
     return SEM_OK;
 }
 
-sem::VolParams vol_params(sem_ctx* ctx, int bi, int cur) {
-    Box& b = ctx->boxes[bi];
+// ------------------------------------------------------------------------------------------------
+// NCCL through dlopen (only needed for world > 1 without emulation; torch normally has it loaded)
+// ------------------------------------------------------------------------------------------------
+struct NcclUid { char internal[128]; };
+struct NcclApi {
+    bool ok = false;
+    int (*getUniqueId)(NcclUid*) = nullptr;
+    int (*commInitRank)(void**, int, NcclUid, int) = nullptr;
+    int (*commDestroy)(void*) = nullptr;
+    int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*groupStart)() = nullptr;
+    int (*groupEnd)() = nullptr;
+    const char* (*errStr)(int) = nullptr;
+};
+constexpr int kNcclDouble = 8;   // ncclFloat64 in nccl.h (ncclDouble == ncclFloat64 == 8)
+
+NcclApi& nccl_api() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.getUniqueId = (int (*)(NcclUid*))dlsym(h, "ncclGetUniqueId");
+            api.commInitRank = (int (*)(void**, int, NcclUid, int))dlsym(h, "ncclCommInitRank");
+            api.commDestroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
+            api.send = (int (*)(const void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclSend");
+            api.recv = (int (*)(void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclRecv");
+            api.groupStart = (int (*)())dlsym(h, "ncclGroupStart");
+            api.groupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
+            api.errStr = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+            api.ok = api.getUniqueId && api.commInitRank && api.send && api.recv && api.groupStart && api.groupEnd;
+        }
+    }
+    return api;
+}
+
+#define NC(call)                                                                                  \
+    do {                                                                                          \
+        int r_ = (call);                                                                          \
+        if (r_ != 0)                                                                              \
+            return fail(ctx, SEM_E_NCCL, std::string(#call) + ": " +                              \
+                                             (nccl_api().errStr ? nccl_api().errStr(r_) : "?"));  \
+    } while (0)
+
+// ------------------------------------------------------------------------------------------------
+// Slabs
+// ------------------------------------------------------------------------------------------------
+bool nccl_mode(const sem_ctx* ctx) { return ctx->world > 1 && !ctx->emulate; }
+
+// Slab `slab` of global box g: elements [ex0, ex0 + nel_loc) along x.  1D tables (coordinates, face
+// masses) are taken from the global lattice, so a cut node keeps its interior (two-sided) mass.
+Box make_slab(const sem_box_desc& g, long long ex0, long long nel_loc, bool cutL, bool cutR) {
+    Box gb;
+    gb.d = g;
+    gb.N = g.degree;
+    gb.NX = (long long)gb.N * g.nel[0] + 1;
+    gb.NY = (long long)gb.N * g.nel[1] + 1;
+    gb.NZ = (long long)gb.N * g.nel[2] + 1;
+    for (int k = 0; k < 3; ++k) gb.h[k] = g.extent[k] / g.nel[k];
+    build_tables(gb);
+    Box b = gb;
+    b.d.origin[0] = g.origin[0] + gb.h[0] * (double)ex0;
+    b.d.extent[0] = gb.h[0] * (double)nel_loc;
+    b.d.nel[0] = (int)nel_loc;
+    if (cutL) b.d.bc[0] = SEM_BC_RIGID;
+    if (cutR) b.d.bc[1] = SEM_BC_RIGID;
+    b.NX = (long long)b.N * nel_loc + 1;
+    b.PX = (b.NX + 7) / 8 * 8;
+    b.gx0 = (long long)b.N * ex0;
+    b.NXg = gb.NX;
+    b.cutL = cutL;
+    b.cutR = cutR;
+    b.xh.assign(gb.xh.begin() + b.gx0, gb.xh.begin() + b.gx0 + b.NX);
+    b.mxh.assign(gb.mxh.begin() + b.gx0, gb.mxh.begin() + b.gx0 + b.NX);
+    return b;
+}
+
+sem::VolParams vol_params(sem_ctx* ctx, sem::Part& pt, int bi, int cur) {
+    Box& b = pt.boxes[bi];
     sem::VolParams p{};
     p.tmP = b.tmP[cur];
     p.tmW = b.tmW;
@@ -259,8 +337,10 @@ sem::VolParams vol_params(sem_ctx* ctx, int bi, int cur) {
         const int d = f / 2;
         p.damp[f] = (b.d.bc[f] == SEM_BC_ABSORBING) ? b.d.c / (0.5 * b.h[d] * w[0]) : 0.0;
     }
-    if (ctx->pm.on && ctx->pm.box == bi) {
-        p.F = ctx->pm.F;
+    p.cutL = b.cutL ? 1 : 0;
+    p.cutR = b.cutR ? 1 : 0;
+    if (pt.pm.on && pt.pm.box == bi) {
+        p.F = pt.pm.F;
         p.kF = 1.0 / b.mzh[0];
     }
     p.iface_side = b.iface_side;
@@ -285,15 +365,16 @@ sem::VolParams vol_params(sem_ctx* ctx, int bi, int cur) {
     p.step = ctx->d_step;
     p.done = ctx->d_done;
     unsigned tot = 0;
-    for (auto& bb : ctx->boxes) tot += sem::volume_blocks(bb.N, bb.NX, bb.NY);
+    for (auto& q : ctx->parts)
+        for (auto& bb : q.boxes) tot += sem::volume_blocks(bb.N, bb.NX, bb.NY);
     p.total_blocks = tot;
     p.bump_step = 1;
     return p;
 }
 
-sem::ModalParams modal_params(sem_ctx* ctx, int cur) {
-    sem::Pmut& pm = ctx->pm;
-    Box& b = ctx->boxes[pm.box];
+sem::ModalParams modal_params(sem_ctx* ctx, sem::Part& pt, int cur) {
+    sem::Pmut& pm = pt.pm;
+    Box& b = pt.boxes[pm.box];
     sem::ModalParams p{};
     p.n_pmut = pm.n_pmut;
     p.n_modes = pm.n_modes;
@@ -330,8 +411,40 @@ sem::ModalParams modal_params(sem_ctx* ctx, int cur) {
     return p;
 }
 
-// enqueue one step with parity `cur` on `s`; returns number of kernel launches
-int enqueue_step(sem_ctx* ctx, int cur, cudaStream_t s, bool prof) {
+// partial rows (side 0: this slab's first plane, R0 row; side 1: last plane, L row) of box bi
+sem::CutParams cut_params(sem_ctx* ctx, sem::Part& pt, int side, int bi, int cur) {
+    Box& b = pt.boxes[bi];
+    sem::CutParams c{};
+    c.side = side;
+    c.N = b.N;
+    c.NX = b.NX;
+    c.NY = b.NY;
+    c.NZ = b.NZ;
+    c.PX = b.PX;
+    c.P = b.P[cur];
+    c.Pn = b.P[1 - cur];
+    c.W = b.W;
+    const int row = side == 0 ? 0 : sem::row_L(b.N);
+    for (int k = 0; k <= b.N; ++k) c.row[k] = b.tab.G[0][row][k];
+    c.dt = ctx->dt;
+    if (b.iface_side < 0) {   // coarse box of the interface: SIPG partials travel with it
+        c.NXt = b.NX;
+        c.NYt = b.NY;
+        c.tau = b.tau;
+        c.sig = b.sig;
+        for (int k = 0; k <= b.N; ++k) {
+            c.ktau[k] = b.tab.ktau[k];
+            c.ksig[k] = b.tab.ksig[k];
+        }
+    }
+    c.out = pt.send[side] + pt.xoff[bi];
+    c.in = pt.recv[side] + pt.xoff[bi];
+    return c;
+}
+
+// enqueue one step with parity `cur` on ctx->stream; returns the number of kernel launches
+int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
+    cudaStream_t s = ctx->stream;
     int nl = 0;
     auto mark = [&](int which, bool begin) {
         if (!prof) return;
@@ -344,47 +457,93 @@ int enqueue_step(sem_ctx* ctx, int cur, cudaStream_t s, bool prof) {
             ctx->ev_pool.pop_back();
         }
         cudaEventRecord(e, s);
-        if (begin) {
-            pend = e;
-        } else {
-            ctx->ev_pending.push_back({which, {pend, e}});
-        }
+        if (begin) pend = e;
+        else ctx->ev_pending.push_back({which, {pend, e}});
     };
-    if (ctx->pm.on) {
-        mark(2, true);
-        sem::launch_modal(modal_params(ctx, cur), s);
-        mark(2, false);
-        ++nl;
-    }
-    if (ctx->itf.on) {
-        sem::IfaceParams ip = ctx->itf.prm;
-        ip.Pf = ctx->boxes[ctx->itf.fine].P[cur];
-        ip.Pc = ctx->boxes[ctx->itf.coarse].P[cur];
+    mark(2, true);
+    for (auto& pt : ctx->parts)
+        if (pt.pm.on) {
+            sem::launch_modal(modal_params(ctx, pt, cur), s);
+            ++nl;
+        }
+    mark(2, false);
+    if (ctx->itf_on) {
         mark(1, true);
-        sem::launch_iface(ip, s);
+        for (auto& pt : ctx->parts) {
+            sem::IfaceParams ip = pt.itf.prm;
+            ip.Pf = pt.boxes[pt.itf.fine].P[cur];
+            ip.Pc = pt.boxes[pt.itf.coarse].P[cur];
+            sem::launch_iface(ip, s);
+            nl += 4;
+        }
         mark(1, false);
-        nl += 4;
+    }
+    const bool slabs = ctx->world > 1;
+    if (slabs) {
+        for (auto& pt : ctx->parts)
+            for (int side = 0; side < 2; ++side)
+                if (side == 0 ? pt.cutL : pt.cutR)
+                    for (int bi = 0; bi < (int)pt.boxes.size(); ++bi) {
+                        sem::launch_cut_partial(cut_params(ctx, pt, side, bi, cur), s);
+                        ++nl;
+                    }
+        if (ctx->emulate) {   // device copies between the slabs of this context
+            for (size_t r = 0; r < ctx->parts.size(); ++r) {
+                sem::Part& pt = ctx->parts[r];
+                const size_t bytes = (size_t)pt.xcount * 8;
+                if (pt.cutL) cudaMemcpyAsync(pt.recv[0], ctx->parts[r - 1].send[1], bytes, cudaMemcpyDeviceToDevice, s);
+                if (pt.cutR) cudaMemcpyAsync(pt.recv[1], ctx->parts[r + 1].send[0], bytes, cudaMemcpyDeviceToDevice, s);
+            }
+        } else {              // NCCL on the comm stream, overlapped with the volume kernels
+            NcclApi& api = nccl_api();
+            sem::Part& pt = ctx->parts[0];
+            cudaEventRecord(ctx->ev_fork, s);
+            cudaStreamWaitEvent(ctx->comm, ctx->ev_fork, 0);
+            api.groupStart();
+            if (pt.cutL) {
+                api.send(pt.send[0], pt.xcount, kNcclDouble, ctx->rank - 1, ctx->nccl, ctx->comm);
+                api.recv(pt.recv[0], pt.xcount, kNcclDouble, ctx->rank - 1, ctx->nccl, ctx->comm);
+            }
+            if (pt.cutR) {
+                api.send(pt.send[1], pt.xcount, kNcclDouble, ctx->rank + 1, ctx->nccl, ctx->comm);
+                api.recv(pt.recv[1], pt.xcount, kNcclDouble, ctx->rank + 1, ctx->nccl, ctx->comm);
+            }
+            api.groupEnd();
+            cudaEventRecord(ctx->ev_join, ctx->comm);
+        }
     }
     mark(0, true);
-    for (int bi = 0; bi < (int)ctx->boxes.size(); ++bi) {
-        sem::launch_volume(vol_params(ctx, bi, cur), ctx->boxes[bi].N, s);
-        ++nl;
-    }
+    for (auto& pt : ctx->parts)
+        for (int bi = 0; bi < (int)pt.boxes.size(); ++bi) {
+            sem::launch_volume(vol_params(ctx, pt, bi, cur), pt.boxes[bi].N, s);
+            ++nl;
+        }
     mark(0, false);
+    if (slabs) {
+        if (!ctx->emulate) cudaStreamWaitEvent(s, ctx->ev_join, 0);
+        for (auto& pt : ctx->parts)
+            for (int side = 0; side < 2; ++side)
+                if (side == 0 ? pt.cutL : pt.cutR)
+                    for (int bi = 0; bi < (int)pt.boxes.size(); ++bi) {
+                        sem::launch_cut_fixup(cut_params(ctx, pt, side, bi, cur), s);
+                        ++nl;
+                    }
+    }
     return nl;
 }
 
 sem_status reset_dynamic(sem_ctx* ctx) {
     CU(cudaMemsetAsync(ctx->d_step, 0, sizeof(long long), ctx->stream));
     CU(cudaMemsetAsync(ctx->d_done, 0, sizeof(unsigned), ctx->stream));
-    if (ctx->pm.on) {
-        const size_t nm = (size_t)ctx->pm.n_pmut * ctx->pm.n_modes;
-        CU(cudaMemsetAsync(ctx->pm.q, 0, nm * sizeof(double), ctx->stream));
-        CU(cudaMemsetAsync(ctx->pm.qd, 0, nm * sizeof(double), ctx->stream));
-        CU(cudaMemsetAsync(ctx->pm.qdd, 0, nm * sizeof(double), ctx->stream));
-        CU(cudaMemsetAsync(ctx->pm.phi, 0, ctx->pm.n_pmut * sizeof(double), ctx->stream));
-        Box& b = ctx->boxes[ctx->pm.box];
-        CU(cudaMemsetAsync(ctx->pm.F, 0, b.NX * b.NY * sizeof(double), ctx->stream));
+    for (auto& pt : ctx->parts) {
+        if (!pt.pm.on) continue;
+        const size_t nm = (size_t)pt.pm.n_pmut * pt.pm.n_modes;
+        CU(cudaMemsetAsync(pt.pm.q, 0, nm * sizeof(double), ctx->stream));
+        CU(cudaMemsetAsync(pt.pm.qd, 0, nm * sizeof(double), ctx->stream));
+        CU(cudaMemsetAsync(pt.pm.qdd, 0, nm * sizeof(double), ctx->stream));
+        CU(cudaMemsetAsync(pt.pm.phi, 0, pt.pm.n_pmut * sizeof(double), ctx->stream));
+        Box& b = pt.boxes[pt.pm.box];
+        CU(cudaMemsetAsync(pt.pm.F, 0, b.NX * b.NY * sizeof(double), ctx->stream));
     }
     ctx->step = 0;
     return SEM_OK;
@@ -406,9 +565,61 @@ sem_status check_ctx(sem_ctx* ctx) {
     return SEM_OK;
 }
 
+// owner slab of global lattice column gx of box bi (a shared cut column belongs to the left slab)
+int owner_part(sem_ctx* ctx, int bi, long long gx) {
+    for (size_t r = 0; r < ctx->parts.size(); ++r) {
+        const Box& b = ctx->parts[r].boxes[bi];
+        if (gx >= b.gx0 && gx < b.gx0 + b.NX) return (int)r;
+    }
+    return -1;
+}
+
+sem_status setup_part_buffers(sem_ctx* ctx, sem::Part& pt) {
+    for (auto& b : pt.boxes) {
+        const size_t n = (size_t)b.nalloc();
+        if (dalloc(ctx, &b.P[0], n) || dalloc(ctx, &b.P[1], n) || dalloc(ctx, &b.W, n)) return SEM_E_OOM;
+        CU(cudaMemset(b.P[0], 0, n * 8));
+        CU(cudaMemset(b.P[1], 0, n * 8));
+        CU(cudaMemset(b.W, 0, n * 8));
+        if (upload(ctx, &b.xc, b.xh) || upload(ctx, &b.yc, b.yh) || upload(ctx, &b.mx, b.mxh) ||
+            upload(ctx, &b.my, b.myh))
+            return SEM_E_CUDA;
+        sem::volume_prepare(b.N);
+        const int TY = sem::volume_tile_y();
+        if (!make_map(&b.tmP[0], b.P[0], b, sem::vol_pbox_w(b.N), TY + 2 * b.N) ||
+            !make_map(&b.tmP[1], b.P[1], b, sem::vol_pbox_w(b.N), TY + 2 * b.N) ||
+            !make_map(&b.tmW, b.W, b, sem::vol_wbox_w(b.N), TY))
+            return fail(ctx, SEM_E_CUDA, "cuTensorMapEncodeTiled failed");
+    }
+    // exchange buffers: per box one NY x NZ plane (+ 2 NY for the coarse SIPG column, sized always)
+    pt.xoff.clear();
+    long long off = 0;
+    for (auto& b : pt.boxes) {
+        pt.xoff.push_back(off);
+        off += b.NY * b.NZ + 2 * b.NY;
+    }
+    pt.xcount = off;
+    for (int s = 0; s < 2; ++s) {
+        if (dalloc(ctx, &pt.send[s], (size_t)off) || dalloc(ctx, &pt.recv[s], (size_t)off)) return SEM_E_OOM;
+        CU(cudaMemset(pt.send[s], 0, (size_t)off * 8));
+        CU(cudaMemset(pt.recv[s], 0, (size_t)off * 8));
+    }
+    return SEM_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+sem_status sem_nccl_unique_id(void* out) {
+    if (!out) return SEM_E_ARG;
+    NcclApi& api = nccl_api();
+    if (!api.ok) return SEM_E_NCCL;
+    NcclUid id;
+    if (api.getUniqueId(&id) != 0) return SEM_E_NCCL;
+    std::memcpy(out, &id, sizeof(id));
+    return SEM_OK;
+}
 
 sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
     if (!out) return SEM_E_ARG;
@@ -417,16 +628,19 @@ sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
     sem_ctx* ctx = new (std::nothrow) sem_ctx();
     if (!ctx) return SEM_E_OOM;
     auto bail = [&](sem_status st) {
+        if (!ctx->err.empty()) fprintf(stderr, "libsem: sem_mesh_create: %s\n", ctx->err.c_str());
         sem_destroy(ctx);
         return st;
     };
     if (!(desc->dt > 0) || !std::isfinite(desc->dt)) return bail(SEM_E_ARG);
-    if (desc->world != 1 || desc->rank != 0) return bail(SEM_E_PARTITION);
+    if (desc->world < 1 || desc->rank < 0 || desc->rank >= desc->world) return bail(SEM_E_ARG);
     ctx->device = desc->device;
     ctx->flags = desc->flags;
     ctx->dt = desc->dt;
     ctx->rank = desc->rank;
     ctx->world = desc->world;
+    ctx->emulate = desc->world > 1 && (desc->flags & SEM_F_EMULATE_SLABS);
+    if (ctx->emulate && desc->rank != 0) return bail(SEM_E_ARG);
     if (cudaSetDevice(ctx->device) != cudaSuccess) return bail(SEM_E_CUDA);
     if (desc->stream) {
         ctx->stream = (cudaStream_t)desc->stream;
@@ -436,37 +650,54 @@ sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
     }
     for (int i = 0; i < desc->n_boxes; ++i) {
         if (check_box(ctx, desc->boxes[i]) != SEM_OK) return bail(SEM_E_ARG);
-        Box b;
-        b.d = desc->boxes[i];
-        b.N = b.d.degree;
-        b.NX = (long long)b.N * b.d.nel[0] + 1;
-        b.NY = (long long)b.N * b.d.nel[1] + 1;
-        b.NZ = (long long)b.N * b.d.nel[2] + 1;
-        b.PX = (b.NX + 7) / 8 * 8;
-        for (int k = 0; k < 3; ++k) b.h[k] = b.d.extent[k] / b.d.nel[k];
-        build_tables(b);
-        ctx->boxes.push_back(b);
+        const sem_box_desc& g = desc->boxes[i];
+        ctx->gdesc.push_back(g);
+        ctx->gNX.push_back((long long)g.degree * g.nel[0] + 1);
+        ctx->gNY.push_back((long long)g.degree * g.nel[1] + 1);
+        ctx->gNZ.push_back((long long)g.degree * g.nel[2] + 1);
     }
-    for (size_t i = 0; i < ctx->boxes.size(); ++i) {
-        Box& b = ctx->boxes[i];
-        const size_t n = (size_t)b.nalloc();
-        if (dalloc(ctx, &b.P[0], n) || dalloc(ctx, &b.P[1], n) || dalloc(ctx, &b.W, n)) return bail(SEM_E_OOM);
-        if (cudaMemset(b.P[0], 0, n * 8) || cudaMemset(b.P[1], 0, n * 8) || cudaMemset(b.W, 0, n * 8))
-            return bail(SEM_E_CUDA);
-        const int TY = sem::volume_tile_y();
-        sem::volume_prepare(b.N);
-        if (!make_map(&b.tmP[0], b.P[0], b, sem::vol_pbox_w(b.N), TY + 2 * b.N) ||
-            !make_map(&b.tmP[1], b.P[1], b, sem::vol_pbox_w(b.N), TY + 2 * b.N) ||
-            !make_map(&b.tmW, b.W, b, sem::vol_wbox_w(b.N), TY)) {
-            fprintf(stderr, "libsem: cuTensorMapEncodeTiled failed\n");
-            return bail(SEM_E_CUDA);
+    // slab decomposition along x: equal element counts per slab, the same slab boundaries for all
+    // boxes (box b's element count must be a multiple of the world size)
+    const int G = ctx->world;
+    for (auto& g : ctx->gdesc)
+        if (g.nel[0] % G) {
+            ctx->err = "nel_x of every box must be divisible by the number of slabs";
+            return bail(SEM_E_PARTITION);
         }
-        if (upload(ctx, &b.xc, b.xh) || upload(ctx, &b.yc, b.yh) || upload(ctx, &b.mx, b.mxh) ||
-            upload(ctx, &b.my, b.myh))
-            return bail(SEM_E_CUDA);
+    const int first = ctx->emulate ? 0 : ctx->rank;
+    const int last = ctx->emulate ? G - 1 : ctx->rank;
+    for (int r = first; r <= last; ++r) {
+        sem::Part pt;
+        pt.slab = r;
+        pt.cutL = r > 0;
+        pt.cutR = r < G - 1;
+        for (auto& g : ctx->gdesc) {
+            const long long nloc = g.nel[0] / G;
+            pt.boxes.push_back(make_slab(g, nloc * r, nloc, pt.cutL, pt.cutR));
+        }
+        ctx->parts.push_back(pt);
     }
+    for (auto& pt : ctx->parts)
+        if (setup_part_buffers(ctx, pt) != SEM_OK) return bail(SEM_E_OOM);
     if (dalloc(ctx, &ctx->d_step, 1) || dalloc(ctx, &ctx->d_done, 1) || dalloc(ctx, &ctx->d_flag, 1))
         return bail(SEM_E_OOM);
+    if (cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return bail(SEM_E_CUDA);
+    if (nccl_mode(ctx)) {
+        NcclApi& api = nccl_api();
+        if (!api.ok || !desc->nccl_unique_id) {
+            ctx->err = "world > 1 needs NCCL (libnccl.so.2) and an ncclUniqueId";
+            return bail(SEM_E_NCCL);
+        }
+        if (cudaStreamCreateWithFlags(&ctx->comm, cudaStreamNonBlocking) != cudaSuccess) return bail(SEM_E_CUDA);
+        NcclUid id;
+        std::memcpy(&id, desc->nccl_unique_id, sizeof(id));
+        if (api.commInitRank(&ctx->nccl, G, id, ctx->rank) != 0) {
+            ctx->err = "ncclCommInitRank failed";
+            return bail(SEM_E_NCCL);
+        }
+    }
     if (reset_dynamic(ctx) != SEM_OK) return bail(SEM_E_CUDA);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return bail(SEM_E_CUDA);
     *out = ctx;
@@ -477,8 +708,8 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
     sem_status st = check_ctx(ctx);
     if (st) return st;
     if (!pd) return fail(ctx, SEM_E_ARG, "null pmut desc");
-    if (ctx->pm.on) return fail(ctx, SEM_E_STATE, "PMUT array already attached");
-    if (pd->box < 0 || pd->box >= (int)ctx->boxes.size()) return fail(ctx, SEM_E_ARG, "bad box");
+    if (ctx->n_pmut) return fail(ctx, SEM_E_STATE, "PMUT array already attached");
+    if (pd->box < 0 || pd->box >= (int)ctx->gdesc.size()) return fail(ctx, SEM_E_ARG, "bad box");
     if (pd->face != 4) return fail(ctx, SEM_E_ARG, "PMUTs supported on the -z face only");
     if (pd->n_pmut < 1 || pd->n_modes < 1 || pd->n_modes > sem::kMaxModes)
         return fail(ctx, SEM_E_ARG, "n_pmut >= 1 and 1 <= n_modes <= 8 required");
@@ -487,86 +718,115 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
         return fail(ctx, SEM_E_ARG, "missing PMUT arrays");
     if (pd->rx && !(pd->capacitance > 0)) return fail(ctx, SEM_E_ARG, "RX requires capacitance > 0");
     if (pd->n_cycles < 1 || !(pd->f0_hz > 0)) return fail(ctx, SEM_E_ARG, "bad drive");
-    Box& b = ctx->boxes[pd->box];
-    if (b.d.bc[4] == SEM_BC_INTERFACE) return fail(ctx, SEM_E_ARG, "PMUT face is an interface");
+    const sem_box_desc& g = ctx->gdesc[pd->box];
+    if (g.bc[4] == SEM_BC_INTERFACE) return fail(ctx, SEM_E_ARG, "PMUT face is an interface");
+    for (int m = 0; m < pd->n_modes; ++m)
+        if (!(pd->modal_mass[m] > 0)) return fail(ctx, SEM_E_ARG, "modal mass must be > 0");
     const int K = pd->n_pmut, M = pd->n_modes;
     const double a = pd->side;
-    std::vector<int> rect(4 * K);
-    std::vector<int> occ((size_t)b.NX * b.NY, -1);
-    int lmax = 1;
-    std::vector<std::vector<long long>> xi(K), yi(K);
+    // membranes must lie on the face, must not overlap, and must not touch a slab cut (they are never
+    // split across GPUs: the paper's membrane-preserving partition)
+    const double hx = g.extent[0] / g.nel[0];
+    const int G = ctx->world;
+    std::vector<double> cuts;
+    for (int r = 1; r < G; ++r) cuts.push_back(g.origin[0] + hx * (double)(g.nel[0] / G) * r);
+    ctx->pm_lists.assign(G, {});
     for (int k = 0; k < K; ++k) {
         const double x0 = pd->center[2 * k] - 0.5 * a, y0 = pd->center[2 * k + 1] - 0.5 * a;
-        for (long long i = 0; i < b.NX; ++i) {
-            const double xl = b.xh[i] - x0;
-            if (xl >= 0 && xl <= a) xi[k].push_back(i);
-        }
-        for (long long j = 0; j < b.NY; ++j) {
-            const double yl = b.yh[j] - y0;
-            if (yl >= 0 && yl <= a) yi[k].push_back(j);
-        }
-        if (xi[k].empty() || yi[k].empty()) return fail(ctx, SEM_E_ARG, "membrane with no face node (or off the face)");
-        if (x0 < b.d.origin[0] - 1e-12 * a || y0 < b.d.origin[1] - 1e-12 * a ||
-            x0 + a > b.d.origin[0] + b.d.extent[0] + 1e-12 * a || y0 + a > b.d.origin[1] + b.d.extent[1] + 1e-12 * a)
+        if (x0 < g.origin[0] - 1e-12 * a || y0 < g.origin[1] - 1e-12 * a ||
+            x0 + a > g.origin[0] + g.extent[0] + 1e-12 * a || y0 + a > g.origin[1] + g.extent[1] + 1e-12 * a)
             return fail(ctx, SEM_E_ARG, "membrane off the face");
-        rect[4 * k] = (int)xi[k].front();
-        rect[4 * k + 1] = (int)yi[k].front();
-        rect[4 * k + 2] = (int)xi[k].size();
-        rect[4 * k + 3] = (int)yi[k].size();
-        lmax = std::max<int>(lmax, std::max(rect[4 * k + 2], rect[4 * k + 3]));
-        for (long long j : yi[k])
-            for (long long i : xi[k]) {
-                int& o = occ[(size_t)j * b.NX + i];
-                if (o >= 0) return fail(ctx, SEM_E_ARG, "membranes overlap");
-                o = k;
-            }
-    }
-    std::vector<double> sx((size_t)K * M * lmax, 0.0), sy((size_t)K * M * lmax, 0.0), wx((size_t)K * lmax, 0.0),
-        wy((size_t)K * lmax, 0.0), om2((size_t)K * M), tzw((size_t)K * M), im(M), et(M), dl(K);
-    for (int k = 0; k < K; ++k) {
-        const double x0 = pd->center[2 * k] - 0.5 * a, y0 = pd->center[2 * k + 1] - 0.5 * a;
-        for (int m = 0; m < M; ++m) {
-            const int mm = pd->mode_mn[2 * m], nn = pd->mode_mn[2 * m + 1];
-            for (size_t i = 0; i < xi[k].size(); ++i)
-                sx[((size_t)k * M + m) * lmax + i] = std::sin(mm * M_PI * (b.xh[xi[k][i]] - x0) / a);
-            for (size_t j = 0; j < yi[k].size(); ++j)
-                sy[((size_t)k * M + m) * lmax + j] = std::sin(nn * M_PI * (b.yh[yi[k][j]] - y0) / a);
-            const double om = 2.0 * M_PI * pd->freq_hz[(size_t)k * M + m];
-            om2[(size_t)k * M + m] = om * om;
-            tzw[(size_t)k * M + m] = 2.0 * pd->damping_ratio[m] * om;
+        int slab = 0;
+        for (size_t c = 0; c < cuts.size(); ++c) {
+            if (x0 <= cuts[c] + 1e-9 * hx && x0 + a >= cuts[c] - 1e-9 * hx)
+                return fail(ctx, SEM_E_PARTITION, "a slab cut crosses a membrane");
+            if (x0 > cuts[c]) slab = (int)c + 1;
         }
-        for (size_t i = 0; i < xi[k].size(); ++i) wx[(size_t)k * lmax + i] = b.mxh[xi[k][i]];
-        for (size_t j = 0; j < yi[k].size(); ++j) wy[(size_t)k * lmax + j] = b.myh[yi[k][j]];
-        dl[k] = pd->delay_s[k];
+        ctx->pm_lists[slab].push_back(k);
     }
-    for (int m = 0; m < M; ++m) {
-        if (!(pd->modal_mass[m] > 0)) return fail(ctx, SEM_E_ARG, "modal mass must be > 0");
-        im[m] = 1.0 / pd->modal_mass[m];
-        et[m] = pd->eta[m];
+    for (auto& pt : ctx->parts) {
+        Box& b = pt.boxes[pd->box];
+        const std::vector<int>& ks = ctx->pm_lists[pt.slab];
+        pt.pm_global = ks;
+        if (ks.empty()) continue;
+        const int KL = (int)ks.size();
+        std::vector<int> rect(4 * KL);
+        std::vector<int> occ((size_t)b.NX * b.NY, -1);
+        int lmax = 1;
+        std::vector<std::vector<long long>> xi(KL), yi(KL);
+        for (int l = 0; l < KL; ++l) {
+            const int k = ks[l];
+            const double x0 = pd->center[2 * k] - 0.5 * a, y0 = pd->center[2 * k + 1] - 0.5 * a;
+            for (long long i = 0; i < b.NX; ++i) {
+                const double xl = b.xh[i] - x0;
+                if (xl >= 0 && xl <= a) xi[l].push_back(i);
+            }
+            for (long long j = 0; j < b.NY; ++j) {
+                const double yl = b.yh[j] - y0;
+                if (yl >= 0 && yl <= a) yi[l].push_back(j);
+            }
+            if (xi[l].empty() || yi[l].empty()) return fail(ctx, SEM_E_ARG, "membrane with no face node");
+            rect[4 * l] = (int)xi[l].front();
+            rect[4 * l + 1] = (int)yi[l].front();
+            rect[4 * l + 2] = (int)xi[l].size();
+            rect[4 * l + 3] = (int)yi[l].size();
+            lmax = std::max<int>(lmax, std::max(rect[4 * l + 2], rect[4 * l + 3]));
+            for (long long j : yi[l])
+                for (long long i : xi[l]) {
+                    int& o = occ[(size_t)j * b.NX + i];
+                    if (o >= 0) return fail(ctx, SEM_E_ARG, "membranes overlap");
+                    o = l;
+                }
+        }
+        std::vector<double> sx((size_t)KL * M * lmax, 0.0), sy((size_t)KL * M * lmax, 0.0), wx((size_t)KL * lmax, 0.0),
+            wy((size_t)KL * lmax, 0.0), om2((size_t)KL * M), tzw((size_t)KL * M), im(M), et(M), dl(KL);
+        for (int l = 0; l < KL; ++l) {
+            const int k = ks[l];
+            const double x0 = pd->center[2 * k] - 0.5 * a, y0 = pd->center[2 * k + 1] - 0.5 * a;
+            for (int m = 0; m < M; ++m) {
+                const int mm = pd->mode_mn[2 * m], nn = pd->mode_mn[2 * m + 1];
+                for (size_t i = 0; i < xi[l].size(); ++i)
+                    sx[((size_t)l * M + m) * lmax + i] = std::sin(mm * M_PI * (b.xh[xi[l][i]] - x0) / a);
+                for (size_t j = 0; j < yi[l].size(); ++j)
+                    sy[((size_t)l * M + m) * lmax + j] = std::sin(nn * M_PI * (b.yh[yi[l][j]] - y0) / a);
+                const double om = 2.0 * M_PI * pd->freq_hz[(size_t)k * M + m];
+                om2[(size_t)l * M + m] = om * om;
+                tzw[(size_t)l * M + m] = 2.0 * pd->damping_ratio[m] * om;
+            }
+            for (size_t i = 0; i < xi[l].size(); ++i) wx[(size_t)l * lmax + i] = b.mxh[xi[l][i]];
+            for (size_t j = 0; j < yi[l].size(); ++j) wy[(size_t)l * lmax + j] = b.myh[yi[l][j]];
+            dl[l] = pd->delay_s[k];
+        }
+        for (int m = 0; m < M; ++m) {
+            im[m] = 1.0 / pd->modal_mass[m];
+            et[m] = pd->eta[m];
+        }
+        sem::Pmut& pm = pt.pm;
+        pm.box = pd->box;
+        pm.n_pmut = KL;
+        pm.n_modes = M;
+        pm.lmax = lmax;
+        if (upload(ctx, &pm.rect, rect) || upload(ctx, &pm.sx, sx) || upload(ctx, &pm.sy, sy) ||
+            upload(ctx, &pm.wx, wx) || upload(ctx, &pm.wy, wy) || upload(ctx, &pm.omega2, om2) ||
+            upload(ctx, &pm.twozw, tzw) || upload(ctx, &pm.invmass, im) || upload(ctx, &pm.eta, et) ||
+            upload(ctx, &pm.delay, dl))
+            return SEM_E_CUDA;
+        const size_t nm = (size_t)KL * M;
+        if (dalloc(ctx, &pm.q, nm) || dalloc(ctx, &pm.qd, nm) || dalloc(ctx, &pm.qdd, nm) || dalloc(ctx, &pm.phi, KL) ||
+            dalloc(ctx, &pm.F, (size_t)b.NX * b.NY))
+            return SEM_E_OOM;
+        pm.amp = pd->amp_v;
+        pm.om0 = 2.0 * M_PI * pd->f0_hz;
+        pm.ncyc = pd->n_cycles;
+        pm.t_end = pd->n_cycles / pd->f0_hz;
+        pm.t_switch = pd->t_switch;
+        pm.rx = pd->rx ? 1 : 0;
+        pm.invC = pd->rx ? 1.0 / pd->capacitance : 0.0;
+        pm.kappa = b.d.rho * b.d.c * b.d.c;   // kappa = rho c^2
+        pm.on = true;
     }
-    sem::Pmut& pm = ctx->pm;
-    pm.box = pd->box;
-    pm.n_pmut = K;
-    pm.n_modes = M;
-    pm.lmax = lmax;
-    if (upload(ctx, &pm.rect, rect) || upload(ctx, &pm.sx, sx) || upload(ctx, &pm.sy, sy) ||
-        upload(ctx, &pm.wx, wx) || upload(ctx, &pm.wy, wy) || upload(ctx, &pm.omega2, om2) ||
-        upload(ctx, &pm.twozw, tzw) || upload(ctx, &pm.invmass, im) || upload(ctx, &pm.eta, et) ||
-        upload(ctx, &pm.delay, dl))
-        return SEM_E_CUDA;
-    const size_t nm = (size_t)K * M;
-    if (dalloc(ctx, &pm.q, nm) || dalloc(ctx, &pm.qd, nm) || dalloc(ctx, &pm.qdd, nm) || dalloc(ctx, &pm.phi, K) ||
-        dalloc(ctx, &pm.F, (size_t)b.NX * b.NY))
-        return SEM_E_OOM;
-    pm.amp = pd->amp_v;
-    pm.om0 = 2.0 * M_PI * pd->f0_hz;
-    pm.ncyc = pd->n_cycles;
-    pm.t_end = pd->n_cycles / pd->f0_hz;
-    pm.t_switch = pd->t_switch;
-    pm.rx = pd->rx ? 1 : 0;
-    pm.invC = pd->rx ? 1.0 / pd->capacitance : 0.0;
-    pm.kappa = b.d.rho * b.d.c * b.d.c;   // kappa = rho c^2
-    pm.on = true;
+    ctx->n_pmut = K;
+    ctx->n_modes = M;
     drop_graphs(ctx);
     st = reset_dynamic(ctx);
     if (st) return st;
@@ -577,95 +837,104 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
 sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, double alpha, int quad_rule) {
     sem_status st = check_ctx(ctx);
     if (st) return st;
-    if (ctx->itf.on) return fail(ctx, SEM_E_STATE, "interface already built");
+    if (ctx->itf_on) return fail(ctx, SEM_E_STATE, "interface already built");
     if (quad_rule != 0) return fail(ctx, SEM_E_ARG, "only quad_rule 0 (fine-face GLL nodes) is implemented");
-    const int nb = (int)ctx->boxes.size();
+    const int nb = (int)ctx->gdesc.size();
     if (fine_box < 0 || coarse_box < 0 || fine_box >= nb || coarse_box >= nb || fine_box == coarse_box)
         return fail(ctx, SEM_E_ARG, "bad box indices");
     if (!(alpha > 0)) return fail(ctx, SEM_E_ARG, "penalty alpha must be > 0");
-    Box& F = ctx->boxes[fine_box];
-    Box& C = ctx->boxes[coarse_box];
-    if (F.d.bc[5] != SEM_BC_INTERFACE || C.d.bc[4] != SEM_BC_INTERFACE)
+    const sem_box_desc& gF = ctx->gdesc[fine_box];
+    const sem_box_desc& gC = ctx->gdesc[coarse_box];
+    if (gF.bc[5] != SEM_BC_INTERFACE || gC.bc[4] != SEM_BC_INTERFACE)
         return fail(ctx, SEM_E_ARG, "fine +z and coarse -z faces must be tagged SEM_BC_INTERFACE");
-    const double tol = 1e-9 * std::max(F.h[0], C.h[0]);
+    const double hF[3] = {gF.extent[0] / gF.nel[0], gF.extent[1] / gF.nel[1], gF.extent[2] / gF.nel[2]};
+    const double hC[3] = {gC.extent[0] / gC.nel[0], gC.extent[1] / gC.nel[1], gC.extent[2] / gC.nel[2]};
+    const double tol = 1e-9 * std::max(hF[0], hC[0]);
     for (int k = 0; k < 2; ++k) {
-        if (std::fabs(F.d.origin[k] - C.d.origin[k]) > tol || std::fabs(F.d.extent[k] - C.d.extent[k]) > tol)
+        if (std::fabs(gF.origin[k] - gC.origin[k]) > tol || std::fabs(gF.extent[k] - gC.extent[k]) > tol)
             return fail(ctx, SEM_E_UNMATCHED, "interface faces do not coincide laterally");
     }
-    if (std::fabs(F.d.origin[2] + F.d.extent[2] - C.d.origin[2]) > tol)
+    if (std::fabs(gF.origin[2] + gF.extent[2] - gC.origin[2]) > tol)
         return fail(ctx, SEM_E_UNMATCHED, "boxes do not touch in z");
-    if (F.d.nel[0] % C.d.nel[0] || F.d.nel[1] % C.d.nel[1] ||
-        F.d.nel[0] / C.d.nel[0] != F.d.nel[1] / C.d.nel[1])
+    if (gF.nel[0] % gC.nel[0] || gF.nel[1] % gC.nel[1] || gF.nel[0] / gC.nel[0] != gF.nel[1] / gC.nel[1])
         return fail(ctx, SEM_E_UNMATCHED, "fine lattice does not nest in the coarse one (need h_c = R h_f)");
-    const int R = F.d.nel[0] / C.d.nel[0];
+    const int R = gF.nel[0] / gC.nel[0];
     std::vector<double> xf, wf, xc, wc;
-    gll_rule(F.N, xf, wf);
-    gll_rule(C.N, xc, wc);
+    gll_rule(gF.degree, xf, wf);
+    gll_rule(gC.degree, xc, wc);
     const std::vector<double> Df = deriv_matrix(xf), Dc = deriv_matrix(xc);
-    sem::IfaceParams& p = ctx->itf.prm;
-    p = sem::IfaceParams{};
-    p.NXf = F.NX;
-    p.NYf = F.NY;
-    p.NZf = F.NZ;
-    p.NXc = C.NX;
-    p.PXf = F.PX;
-    p.PXc = C.PX;
-    p.NYc = C.NY;
-    p.Nf = F.N;
-    p.Nc = C.N;
-    p.R = R;
-    p.nelcx = C.d.nel[0];
-    p.nelcy = C.d.nel[1];
-    const double cbar = 2.0 * F.d.c * C.d.c / (F.d.c + C.d.c);
-    const double hmin = std::min(std::min(std::min(F.h[0], F.h[1]), F.h[2]), std::min(std::min(C.h[0], C.h[1]), C.h[2]));
-    p.gamma = alpha * cbar * cbar * std::max(F.N, C.N) * std::max(F.N, C.N) / hmin;
-    p.cf2 = F.d.c * F.d.c;
-    p.cc2 = C.d.c * C.d.c;
-    for (int c = 0; c <= F.N; ++c) p.dfT[c] = (2.0 / F.h[2]) * Df[F.N * (F.N + 1) + c];
-    for (int c = 0; c <= C.N; ++c) p.dcB[c] = (2.0 / C.h[2]) * Dc[0 * (C.N + 1) + c];
-    const int NfR = F.N * R;
-    std::vector<double> I((size_t)(NfR + 1) * (C.N + 1), 0.0);
+    const int Nf = gF.degree, Nc = gC.degree, NfR = Nf * R;
+    std::vector<double> I((size_t)(NfR + 1) * (Nc + 1), 0.0);
     for (int q = 0; q <= NfR; ++q) {
-        int r = q / F.N, a = q % F.N;
+        int r = q / Nf, a = q % Nf;
         if (q == NfR) {
             r = R - 1;
-            a = F.N;
+            a = Nf;
         }
         const double xm = (2.0 * r + xf[a] + 1.0) / R - 1.0;   // x_hat^- of the fine node
         const std::vector<double> l = lagrange_at(xc, xm);
-        for (int b = 0; b <= C.N; ++b) I[(size_t)q * (C.N + 1) + b] = l[b];
+        for (int b = 0; b <= Nc; ++b) I[(size_t)q * (Nc + 1) + b] = l[b];
     }
-    double* dI = nullptr;
-    if (upload(ctx, &dI, I)) return SEM_E_CUDA;
-    p.I = dI;
-    p.mxf = F.mx;
-    p.myf = F.my;
-    p.mxc = C.mx;
-    p.myc = C.my;
-    const size_t nf = (size_t)F.NX * F.NY, nc = (size_t)C.NX * C.NY, nh = (size_t)F.NX * C.NY;
-    if (dalloc(ctx, &p.trc, nc) || dalloc(ctx, &p.drc, nc) || dalloc(ctx, &p.tauf, nf) || dalloc(ctx, &p.sigf, nf) ||
-        dalloc(ctx, &p.g1, nf) || dalloc(ctx, &p.g2, nf) || dalloc(ctx, &p.h1, nh) || dalloc(ctx, &p.h2, nh) ||
-        dalloc(ctx, &p.tauc, nc) || dalloc(ctx, &p.sigc, nc))
-        return SEM_E_OOM;
-    // layer coefficients: a -= tau ktau[c] + sigma ksig[c]
-    F.iface_side = +1;
-    F.tau = p.tauf;
-    F.sig = p.sigf;
-    for (int c = 0; c <= F.N; ++c) {
-        const long long iz = F.NZ - 1 - F.N + c;
-        F.tab.ksig[c] = (2.0 / F.h[2]) * Df[F.N * (F.N + 1) + c] / F.mzh[iz];
-        F.tab.ktau[c] = (c == F.N) ? 1.0 / F.mzh[iz] : 0.0;
+    const double cbar = 2.0 * gF.c * gC.c / (gF.c + gC.c);
+    const double hmin = std::min(std::min(std::min(hF[0], hF[1]), hF[2]), std::min(std::min(hC[0], hC[1]), hC[2]));
+    const double gamma = alpha * cbar * cbar * std::max(Nf, Nc) * std::max(Nf, Nc) / hmin;
+    for (auto& pt : ctx->parts) {
+        Box& F = pt.boxes[fine_box];
+        Box& C = pt.boxes[coarse_box];
+        if ((F.gx0 / Nf) % R) return fail(ctx, SEM_E_PARTITION, "slab cut not aligned to the coarse elements");
+        sem::IfaceParams& p = pt.itf.prm;
+        p = sem::IfaceParams{};
+        p.NXf = F.NX;
+        p.NYf = F.NY;
+        p.NZf = F.NZ;
+        p.NXc = C.NX;
+        p.NYc = C.NY;
+        p.PXf = F.PX;
+        p.PXc = C.PX;
+        p.Nf = Nf;
+        p.Nc = Nc;
+        p.R = R;
+        p.nelcx = C.d.nel[0];
+        p.nelcy = C.d.nel[1];
+        p.gamma = gamma;
+        p.cf2 = gF.c * gF.c;
+        p.cc2 = gC.c * gC.c;
+        p.skip_ix0 = F.cutL ? 1 : 0;
+        for (int c = 0; c <= Nf; ++c) p.dfT[c] = (2.0 / hF[2]) * Df[Nf * (Nf + 1) + c];
+        for (int c = 0; c <= Nc; ++c) p.dcB[c] = (2.0 / hC[2]) * Dc[0 * (Nc + 1) + c];
+        double* dI = nullptr;
+        if (upload(ctx, &dI, I)) return SEM_E_CUDA;
+        p.I = dI;
+        p.mxf = F.mx;
+        p.myf = F.my;
+        p.mxc = C.mx;
+        p.myc = C.my;
+        const size_t nf = (size_t)F.NX * F.NY, nc = (size_t)C.NX * C.NY, nh = (size_t)F.NX * C.NY;
+        if (dalloc(ctx, &p.trc, nc) || dalloc(ctx, &p.drc, nc) || dalloc(ctx, &p.tauf, nf) ||
+            dalloc(ctx, &p.sigf, nf) || dalloc(ctx, &p.g1, nf) || dalloc(ctx, &p.g2, nf) || dalloc(ctx, &p.h1, nh) ||
+            dalloc(ctx, &p.h2, nh) || dalloc(ctx, &p.tauc, nc) || dalloc(ctx, &p.sigc, nc))
+            return SEM_E_OOM;
+        // layer coefficients: a -= tau ktau[c] + sigma ksig[c]
+        F.iface_side = +1;
+        F.tau = p.tauf;
+        F.sig = p.sigf;
+        for (int c = 0; c <= Nf; ++c) {
+            const long long iz = F.NZ - 1 - Nf + c;
+            F.tab.ksig[c] = (2.0 / hF[2]) * Df[Nf * (Nf + 1) + c] / F.mzh[iz];
+            F.tab.ktau[c] = (c == Nf) ? 1.0 / F.mzh[iz] : 0.0;
+        }
+        C.iface_side = -1;
+        C.tau = p.tauc;
+        C.sig = p.sigc;
+        for (int c = 0; c <= Nc; ++c) {
+            C.tab.ksig[c] = (2.0 / hC[2]) * Dc[0 * (Nc + 1) + c] / C.mzh[c];
+            C.tab.ktau[c] = (c == 0) ? 1.0 / C.mzh[0] : 0.0;
+        }
+        pt.itf.on = true;
+        pt.itf.fine = fine_box;
+        pt.itf.coarse = coarse_box;
     }
-    C.iface_side = -1;
-    C.tau = p.tauc;
-    C.sig = p.sigc;
-    for (int c = 0; c <= C.N; ++c) {
-        C.tab.ksig[c] = (2.0 / C.h[2]) * Dc[0 * (C.N + 1) + c] / C.mzh[c];
-        C.tab.ktau[c] = (c == 0) ? 1.0 / C.mzh[0] : 0.0;
-    }
-    ctx->itf.on = true;
-    ctx->itf.fine = fine_box;
-    ctx->itf.coarse = coarse_box;
+    ctx->itf_on = true;
     drop_graphs(ctx);
     CU(cudaStreamSynchronize(ctx->stream));
     return SEM_OK;
@@ -675,10 +944,10 @@ sem_status sem_plane_wave_source(sem_ctx* ctx, int box, int face, double amp, do
                                  const double dir[3]) {
     sem_status st = check_ctx(ctx);
     if (st) return st;
-    if (box < 0 || box >= (int)ctx->boxes.size() || face != 5 || !dir)
+    if (box < 0 || box >= (int)ctx->gdesc.size() || face != 5 || !dir)
         return fail(ctx, SEM_E_ARG, "plane wave: +z face of an existing box only");
-    Box& b = ctx->boxes[box];
-    if (b.d.bc[5] != SEM_BC_ABSORBING) return fail(ctx, SEM_E_ARG, "plane wave needs an absorbing face");
+    const sem_box_desc& g = ctx->gdesc[box];
+    if (g.bc[5] != SEM_BC_ABSORBING) return fail(ctx, SEM_E_ARG, "plane wave needs an absorbing face");
     const double nk = std::sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
     if (!(nk > 0) || !(sigma > 0)) return fail(ctx, SEM_E_ARG, "bad plane-wave parameters");
     sem::PlaneWave& pw = ctx->pw;
@@ -688,12 +957,13 @@ sem_status sem_plane_wave_source(sem_ctx* ctx, int box, int face, double amp, do
     pw.sigma = sigma;
     pw.t0 = t0;
     for (int k = 0; k < 3; ++k) pw.k[k] = dir[k] / nk;
-    // x_ref: the +z face corner the wavefront reaches first (min k.x), reading R13
-    const double zt = b.d.origin[2] + b.d.extent[2];
+    // x_ref: the corner of the (global) +z face the wavefront reaches first (min k.x), reading R13
+    const double zt = g.origin[2] + g.extent[2];
     double best = std::numeric_limits<double>::infinity();
     for (int i = 0; i < 2; ++i)
         for (int j = 0; j < 2; ++j) {
-            const double x = b.xh[i ? b.NX - 1 : 0], y = b.yh[j ? b.NY - 1 : 0];
+            const double x = i ? g.origin[0] + g.extent[0] : g.origin[0];
+            const double y = j ? g.origin[1] + g.extent[1] : g.origin[1];
             const double kx = pw.k[0] * x + pw.k[1] * y + pw.k[2] * zt;
             if (kx < best) {
                 best = kx;
@@ -716,7 +986,7 @@ sem_status sem_step(sem_ctx* ctx, int n_steps) {
     int left = n_steps;
     while (left > 0) {
         if (direct) {
-            launches += enqueue_step(ctx, ctx->cur, ctx->stream, ctx->profiling);
+            launches += enqueue_step(ctx, ctx->cur, ctx->profiling);
             ctx->cur ^= 1;
             --left;
             continue;
@@ -727,7 +997,7 @@ sem_status sem_step(sem_ctx* ctx, int n_steps) {
             cudaGraph_t graph;
             CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
             int nl = 0;
-            for (int k = 0; k < len; ++k) nl += enqueue_step(ctx, ctx->cur ^ (k & 1), ctx->stream, false);
+            for (int k = 0; k < len; ++k) nl += enqueue_step(ctx, ctx->cur ^ (k & 1), false);
             CU(cudaStreamEndCapture(ctx->stream, &graph));
             cudaError_t e = cudaGraphInstantiate(&g, graph, 0);
             cudaGraphDestroy(graph);
@@ -736,11 +1006,7 @@ sem_status sem_step(sem_ctx* ctx, int n_steps) {
         }
         CU(cudaGraphLaunch(g, ctx->stream));
         launches += ctx->graph_launches[ctx->cur][len - 1];
-        if (len == 2) {
-            /* parity unchanged after two steps */
-        } else {
-            ctx->cur ^= 1;
-        }
+        if (len == 1) ctx->cur ^= 1;
         left -= len;
     }
     CU(cudaGetLastError());
@@ -748,8 +1014,9 @@ sem_status sem_step(sem_ctx* ctx, int n_steps) {
     ctx->last_launches = launches;
     if (ctx->flags & SEM_F_NAN_CHECK) {
         CU(cudaMemsetAsync(ctx->d_flag, 0, 8, ctx->stream));
-        for (auto& b : ctx->boxes)
-            sem::launch_nonfinite(b.P[1 - ctx->cur], b.NX, b.PX, b.NY * b.NZ, ctx->d_flag, ctx->stream);
+        for (auto& pt : ctx->parts)
+            for (auto& b : pt.boxes)
+                sem::launch_nonfinite(b.P[1 - ctx->cur], b.NX, b.PX, b.NY * b.NZ, ctx->d_flag, ctx->stream);
         unsigned long long f = 0;
         CU(cudaMemcpyAsync(&f, ctx->d_flag, 8, cudaMemcpyDeviceToHost, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
@@ -768,11 +1035,39 @@ sem_status sem_sync(sem_ctx* ctx) {
 sem_status sem_read_pressure(sem_ctx* ctx, int box, double* host, size_t n) {
     sem_status st = check_ctx(ctx);
     if (st) return st;
-    if (box < 0 || box >= (int)ctx->boxes.size() || !host) return fail(ctx, SEM_E_ARG, "bad box / buffer");
-    Box& b = ctx->boxes[box];
-    if (n != (size_t)b.ndof()) return fail(ctx, SEM_E_ARG, "n must equal the box node count");
-    CU(cudaMemcpy2DAsync(host, b.NX * 8, b.P[1 - ctx->cur], b.PX * 8, b.NX * 8, b.NY * b.NZ, cudaMemcpyDeviceToHost,
+    if (box < 0 || box >= (int)ctx->gdesc.size()) return fail(ctx, SEM_E_ARG, "bad box");
+    const long long NXg = ctx->gNX[box], rows = ctx->gNY[box] * ctx->gNZ[box];
+    const bool receiver = !nccl_mode(ctx) || ctx->rank == 0;
+    if (receiver && (!host || n != (size_t)(NXg * rows))) return fail(ctx, SEM_E_ARG, "n must equal the box node count");
+    if (!nccl_mode(ctx)) {
+        for (auto& pt : ctx->parts) {
+            Box& b = pt.boxes[box];
+            const long long skip = b.cutL ? 1 : 0;   // the shared cut column is reported by the left slab
+            CU(cudaMemcpy2DAsync(host + b.gx0 + skip, NXg * 8, b.P[1 - ctx->cur] + skip, b.PX * 8,
+                                 (b.NX - skip) * 8, rows, cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        CU(cudaStreamSynchronize(ctx->stream));
+        return SEM_OK;
+    }
+    // NCCL: every rank sends its slab to rank 0, which assembles the global field
+    NcclApi& api = nccl_api();
+    Box& mine = ctx->parts[0].boxes[box];
+    if (ctx->rank != 0) {
+        NC(api.send(mine.P[1 - ctx->cur], (size_t)mine.nalloc(), kNcclDouble, 0, ctx->nccl, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        return SEM_OK;
+    }
+    CU(cudaMemcpy2DAsync(host, NXg * 8, mine.P[1 - ctx->cur], mine.PX * 8, mine.NX * 8, rows, cudaMemcpyDeviceToHost,
                          ctx->stream));
+    double* tmp = nullptr;
+    CU(cudaMallocAsync(&tmp, (size_t)mine.nalloc() * 8, ctx->stream));
+    for (int r = 1; r < ctx->world; ++r) {
+        const long long gx0 = mine.NX - 1 + (long long)(mine.NX - 1) * (r - 1);   // equal slabs
+        NC(api.recv(tmp, (size_t)mine.nalloc(), kNcclDouble, r, ctx->nccl, ctx->stream));
+        CU(cudaMemcpy2DAsync(host + gx0 + 1, NXg * 8, tmp + 1, mine.PX * 8, (mine.NX - 1) * 8, rows,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CU(cudaFreeAsync(tmp, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return SEM_OK;
 }
@@ -780,49 +1075,115 @@ sem_status sem_read_pressure(sem_ctx* ctx, int box, double* host, size_t n) {
 sem_status sem_read_pressure_at(sem_ctx* ctx, int box, const long long* ids, size_t n, double* out) {
     sem_status st = check_ctx(ctx);
     if (st) return st;
-    if (box < 0 || box >= (int)ctx->boxes.size() || (n && (!ids || !out))) return fail(ctx, SEM_E_ARG, "bad args");
+    if (box < 0 || box >= (int)ctx->gdesc.size() || (n && (!ids || !out))) return fail(ctx, SEM_E_ARG, "bad args");
+    if (nccl_mode(ctx)) return fail(ctx, SEM_E_STATE, "sampled readout is single-process only (world 1 or emulated)");
     if (n == 0) return SEM_OK;
-    Box& b = ctx->boxes[box];
-    for (size_t i = 0; i < n; ++i)
-        if (ids[i] < 0 || ids[i] >= b.ndof()) return fail(ctx, SEM_E_ARG, "node id out of range");
-    long long* dids = nullptr;
-    double* dout = nullptr;
-    CU(cudaMallocAsync(&dids, n * sizeof(long long), ctx->stream));
-    CU(cudaMallocAsync(&dout, n * sizeof(double), ctx->stream));
-    CU(cudaMemcpyAsync(dids, ids, n * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
-    sem::launch_gather(b.P[1 - ctx->cur], dids, (long long)n, b.NX, b.PX, dout, ctx->stream);
-    CU(cudaMemcpyAsync(out, dout, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaFreeAsync(dids, ctx->stream));
-    CU(cudaFreeAsync(dout, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+    const long long NXg = ctx->gNX[box], total = NXg * ctx->gNY[box] * ctx->gNZ[box];
+    std::vector<std::vector<long long>> idx(ctx->parts.size()), pos(ctx->parts.size());
+    for (size_t i = 0; i < n; ++i) {
+        if (ids[i] < 0 || ids[i] >= total) return fail(ctx, SEM_E_ARG, "node id out of range");
+        const long long gx = ids[i] % NXg, row = ids[i] / NXg;
+        const int r = owner_part(ctx, box, gx);
+        const Box& b = ctx->parts[r].boxes[box];
+        idx[r].push_back(row * b.PX + (gx - b.gx0));
+        pos[r].push_back((long long)i);
+    }
+    std::vector<double> tmp(n);
+    for (size_t r = 0; r < ctx->parts.size(); ++r) {
+        const size_t m = idx[r].size();
+        if (!m) continue;
+        long long* didx = nullptr;
+        double* dout = nullptr;
+        CU(cudaMallocAsync(&didx, m * sizeof(long long), ctx->stream));
+        CU(cudaMallocAsync(&dout, m * sizeof(double), ctx->stream));
+        CU(cudaMemcpyAsync(didx, idx[r].data(), m * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+        sem::launch_gather(ctx->parts[r].boxes[box].P[1 - ctx->cur], didx, (long long)m, dout, ctx->stream);
+        std::vector<double> got(m);
+        CU(cudaMemcpyAsync(got.data(), dout, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaFreeAsync(didx, ctx->stream));
+        CU(cudaFreeAsync(dout, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        for (size_t j = 0; j < m; ++j) out[pos[r][j]] = got[j];
+    }
     return SEM_OK;
 }
 
 sem_status sem_read_modal(sem_ctx* ctx, double* q, double* qdot, double* v_rx, size_t n) {
     sem_status st = check_ctx(ctx);
     if (st) return st;
-    if (!ctx->pm.on) return fail(ctx, SEM_E_STATE, "no PMUT array attached");
-    const size_t nm = (size_t)ctx->pm.n_pmut * ctx->pm.n_modes;
-    if (n != nm) return fail(ctx, SEM_E_ARG, "n must equal n_pmut * n_modes");
-    if (q) CU(cudaMemcpyAsync(q, ctx->pm.q, nm * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    if (qdot) CU(cudaMemcpyAsync(qdot, ctx->pm.qd, nm * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    if (v_rx) CU(cudaMemcpyAsync(v_rx, ctx->pm.phi, ctx->pm.n_pmut * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+    if (!ctx->n_pmut) return fail(ctx, SEM_E_STATE, "no PMUT array attached");
+    const int M = ctx->n_modes;
+    const size_t nm = (size_t)ctx->n_pmut * M;
+    const bool receiver = !nccl_mode(ctx) || ctx->rank == 0;
+    if (receiver && n != nm) return fail(ctx, SEM_E_ARG, "n must equal n_pmut * n_modes");
+    double* outs[3] = {q, qdot, v_rx};
+    auto scatter = [&](const std::vector<int>& ks, const std::vector<double>& buf, int which) {
+        const int per = which == 2 ? 1 : M;
+        if (!outs[which]) return;
+        for (size_t l = 0; l < ks.size(); ++l)
+            for (int m = 0; m < per; ++m) outs[which][(size_t)ks[l] * per + m] = buf[l * per + m];
+    };
+    if (!nccl_mode(ctx)) {
+        for (auto& pt : ctx->parts) {
+            if (!pt.pm.on) continue;
+            const size_t KL = pt.pm_global.size();
+            const double* src[3] = {pt.pm.q, pt.pm.qd, pt.pm.phi};
+            for (int w = 0; w < 3; ++w) {
+                std::vector<double> buf(KL * (w == 2 ? 1 : M));
+                CU(cudaMemcpyAsync(buf.data(), src[w], buf.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+                CU(cudaStreamSynchronize(ctx->stream));
+                scatter(pt.pm_global, buf, w);
+            }
+        }
+        return SEM_OK;
+    }
+    NcclApi& api = nccl_api();
+    sem::Part& pt = ctx->parts[0];
+    const double* src[3] = {pt.pm.q, pt.pm.qd, pt.pm.phi};
+    if (ctx->rank != 0) {
+        for (int w = 0; w < 3; ++w) {
+            const size_t cnt = pt.pm_global.size() * (w == 2 ? 1 : M);
+            if (cnt) NC(api.send(src[w], cnt, kNcclDouble, 0, ctx->nccl, ctx->stream));
+        }
+        CU(cudaStreamSynchronize(ctx->stream));
+        return SEM_OK;
+    }
+    for (int r = 0; r < ctx->world; ++r) {
+        const std::vector<int>& ks = ctx->pm_lists[r];
+        for (int w = 0; w < 3; ++w) {
+            const size_t cnt = ks.size() * (w == 2 ? 1 : M);
+            if (!cnt) continue;
+            std::vector<double> buf(cnt);
+            if (r == 0) {
+                CU(cudaMemcpyAsync(buf.data(), src[w], cnt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            } else {
+                double* tmp = nullptr;
+                CU(cudaMallocAsync(&tmp, cnt * 8, ctx->stream));
+                NC(api.recv(tmp, cnt, kNcclDouble, r, ctx->nccl, ctx->stream));
+                CU(cudaMemcpyAsync(buf.data(), tmp, cnt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+                CU(cudaFreeAsync(tmp, ctx->stream));
+            }
+            CU(cudaStreamSynchronize(ctx->stream));
+            scatter(ks, buf, w);
+        }
+    }
     return SEM_OK;
 }
 
 sem_status sem_write_state(sem_ctx* ctx, int box, const double* p, const double* pdot, size_t n) {
     sem_status st = check_ctx(ctx);
     if (st) return st;
-    if (box < 0 || box >= (int)ctx->boxes.size() || !p || !pdot) return fail(ctx, SEM_E_ARG, "bad args");
-    Box& b = ctx->boxes[box];
-    if (n != (size_t)b.ndof()) return fail(ctx, SEM_E_ARG, "n must equal the box node count");
+    if (box < 0 || box >= (int)ctx->gdesc.size() || !p || !pdot) return fail(ctx, SEM_E_ARG, "bad args");
+    const long long NXg = ctx->gNX[box], rows = ctx->gNY[box] * ctx->gNZ[box];
+    if (n != (size_t)(NXg * rows)) return fail(ctx, SEM_E_ARG, "n must equal the box node count");
     // p^S lives in P[1-cur]; p^{S+1} = p^S + dt w^S in P[cur]; w^0 = p'^0 + dt/2 p''^0 = p'^0
-    double* pprev = b.P[1 - ctx->cur];
-    double* pcur = b.P[ctx->cur];
-    CU(cudaMemcpy2DAsync(pprev, b.PX * 8, p, b.NX * 8, b.NX * 8, b.NY * b.NZ, cudaMemcpyHostToDevice, ctx->stream));
-    CU(cudaMemcpy2DAsync(b.W, b.PX * 8, pdot, b.NX * 8, b.NX * 8, b.NY * b.NZ, cudaMemcpyHostToDevice, ctx->stream));
-    sem::launch_set_state(pprev, pcur, b.W, b.NX, b.PX, b.NY * b.NZ, ctx->dt, ctx->stream);
+    for (auto& pt : ctx->parts) {
+        Box& b = pt.boxes[box];
+        double* pprev = b.P[1 - ctx->cur];
+        CU(cudaMemcpy2DAsync(pprev, b.PX * 8, p + b.gx0, NXg * 8, b.NX * 8, rows, cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpy2DAsync(b.W, b.PX * 8, pdot + b.gx0, NXg * 8, b.NX * 8, rows, cudaMemcpyHostToDevice, ctx->stream));
+        sem::launch_set_state(pprev, b.P[ctx->cur], b.W, b.NX, b.PX, rows, ctx->dt, ctx->stream);
+    }
     st = reset_dynamic(ctx);
     if (st) return st;
     CU(cudaStreamSynchronize(ctx->stream));
@@ -832,10 +1193,12 @@ sem_status sem_write_state(sem_ctx* ctx, int box, const double* p, const double*
 sem_status sem_fill_random_state(sem_ctx* ctx, int box, unsigned long long seed, double ps, double vs) {
     sem_status st = check_ctx(ctx);
     if (st) return st;
-    if (box < 0 || box >= (int)ctx->boxes.size()) return fail(ctx, SEM_E_ARG, "bad box");
-    Box& b = ctx->boxes[box];
-    sem::launch_fill_random(b.P[1 - ctx->cur], b.W, b.P[ctx->cur], b.NX, b.PX, b.NY * b.NZ, seed, box, ps, vs, ctx->dt,
-                            ctx->stream);
+    if (box < 0 || box >= (int)ctx->gdesc.size()) return fail(ctx, SEM_E_ARG, "bad box");
+    for (auto& pt : ctx->parts) {
+        Box& b = pt.boxes[box];
+        sem::launch_fill_random(b.P[1 - ctx->cur], b.W, b.P[ctx->cur], b.NX, b.PX, b.NY * b.NZ, b.gx0, b.NXg, seed, box,
+                                ps, vs, ctx->dt, ctx->stream);
+    }
     st = reset_dynamic(ctx);
     if (st) return st;
     CU(cudaStreamSynchronize(ctx->stream));
@@ -846,7 +1209,7 @@ sem_status sem_query(sem_ctx* ctx, long long* n_dof, long long* step, double* t)
     sem_status st = check_ctx(ctx);
     if (st) return st;
     long long nd = 0;
-    for (auto& b : ctx->boxes) nd += b.ndof();
+    for (size_t b = 0; b < ctx->gdesc.size(); ++b) nd += ctx->gNX[b] * ctx->gNY[b] * ctx->gNZ[b];
     if (n_dof) *n_dof = nd;
     if (step) *step = ctx->step;
     if (t) *t = ctx->step * ctx->dt;
@@ -902,12 +1265,16 @@ void sem_destroy(sem_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     drop_graphs(ctx);
+    if (ctx->nccl && nccl_api().commDestroy) nccl_api().commDestroy(ctx->nccl);
     for (void* p : ctx->allocs) cudaFree(p);
     for (auto& pe : ctx->ev_pending) {
         cudaEventDestroy(pe.second.first);
         cudaEventDestroy(pe.second.second);
     }
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->comm) cudaStreamDestroy(ctx->comm);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

@@ -74,6 +74,8 @@ struct VolParams {
     // PMUT forcing plane on z = 0 (F = kappa sum_m qdd S), scaled by kF = 1 / m_z(0)
     const double* __restrict__ F;
     double kF;
+    // slab cuts (multi-GPU): this slab's -x / +x face is an internal cut, not a box face
+    int cutL, cutR;
     // DG interface layer: side = +1 (this box's +z face is Gamma_I, fine side),
     // -1 (its -z face, coarse side), 0 none; tau / sigma on the face lattice [NX*NY]
     int iface_side;
@@ -138,6 +140,26 @@ struct IfaceParams {
     double* g1; double* g2;         // fine weighted terms for the coarse gather
     double* h1; double* h2;         // [NYc][NXf] after the y gather
     double* tauc; double* sigc;     // coarse outputs [NXc*NYc]
+    int skip_ix0;                   // slab with a left cut: the shared fine cut line belongs to the left slab
+};
+
+// One side of one slab cut for one box (partial rows before, fix-up after the exchange).
+struct CutParams {
+    int side;                       // 0: cut at ix = 0 (neighbour on the left), 1: at ix = NX-1
+    int N;
+    long long NX, NY, NZ, PX;
+    const double* P;                // p^{n+1} (partial)
+    double* Pn;                     // p^{n+2}, w^{n+1} (fix-up)
+    double* W;
+    double row[kMaxN + 1];          // R0 (side 0) or L (side 1), scaled by c^2 (2/h_x)^2
+    double dt;
+    // coarse box of an interface: SIPG partials at the cut column (NYt > 0)
+    long long NXt, NYt;
+    const double* tau;
+    const double* sig;
+    double ktau[kMaxN + 1], ksig[kMaxN + 1];
+    double* out;                    // send buffer: [NY*NZ plane][NYt tau][NYt sigma]
+    const double* in;               // receive buffer, same layout
 };
 
 struct Box {
@@ -154,7 +176,10 @@ struct Box {
     double* mx = nullptr;  // face mass factors along x [NX] = (h_x/2) w_asm
     double* my = nullptr;
     BoxTables tab{};
-    std::vector<double> xh, yh, mxh, myh, mzh;  // host copies
+    std::vector<double> xh, yh, mxh, myh, mzh;  // host copies (global-lattice values for slab nodes)
+    long long gx0 = 0;      // global lattice x index of local ix = 0 (slab decomposition)
+    long long NXg = 0;      // global lattice NX of the box
+    bool cutL = false, cutR = false;  // -x / +x face of this slab is an internal cut
     int iface_side = 0;
     double* tau = nullptr;  // interface outputs on this box's face lattice
     double* sig = nullptr;
@@ -188,22 +213,42 @@ struct PlaneWave {
 
 }  // namespace sem
 
+namespace sem {
+// One x-slab of the decomposition (one rank; all slabs live in one context under emulation).
+struct Part {
+    int slab = 0;
+    std::vector<Box> boxes;
+    Pmut pm;
+    std::vector<int> pm_global;   // global PMUT index of each local PMUT
+    Iface itf;
+    bool cutL = false, cutR = false;
+    double* send[2] = {nullptr, nullptr};   // [0] to the left neighbour, [1] to the right
+    double* recv[2] = {nullptr, nullptr};
+    long long xcount = 0;                   // doubles per neighbour message
+    std::vector<long long> xoff;            // offset of box b's block in a message
+};
+}  // namespace sem
+
 struct sem_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t comm = nullptr;   // NCCL stream (world > 1, not emulated)
     bool own_stream = false;
     int flags = 0;
     int rank = 0, world = 1;
+    bool emulate = false;          // all slabs in this context, exchange by device copies
     double dt = 0;
-    std::vector<sem::Box> boxes;
-    sem::Pmut pm;
-    sem::Iface itf;
+    std::vector<sem_box_desc> gdesc;               // global boxes as given
+    std::vector<long long> gNX, gNY, gNZ;          // global lattice sizes
+    std::vector<sem::Part> parts;
+    int n_pmut = 0, n_modes = 0;                   // global PMUT array
+    std::vector<std::vector<int>> pm_lists;        // global PMUT indices per slab
+    bool itf_on = false;
     sem::PlaneWave pw;
     int cur = 0;                 // P[cur] = p^{step+1}, P[1-cur] = p^{step}
     long long step = 0;          // host mirror of the device counter
     long long* d_step = nullptr;
     unsigned int* d_done = nullptr;
-    double* d_scratch = nullptr; // readback / reductions
     unsigned long long* d_flag = nullptr;
     cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [parity][1 or 2 steps]
     long long graph_launches[2][2] = {{0, 0}, {0, 0}};
@@ -213,6 +258,8 @@ struct sem_ctx {
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
     double kt_ms[3] = {0, 0, 0};
     long long kt_n[3] = {0, 0, 0};
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    void* nccl = nullptr;        // ncclComm_t
     std::string err;
     std::vector<void*> allocs;
 };
@@ -223,11 +270,13 @@ void launch_volume(const VolParams& p, int N, cudaStream_t s);
 void launch_modal(const ModalParams& p, cudaStream_t s);
 void launch_iface(const IfaceParams& p, cudaStream_t s);
 void launch_fill_random(double* p, double* w, double* pn, long long NX, long long PX, long long rows,
-                        unsigned long long seed, int box, double ps, double vs, double dt, cudaStream_t s);
+                        long long gx0, long long NXg, unsigned long long seed, int box, double ps, double vs,
+                        double dt, cudaStream_t s);
+void launch_cut_partial(const CutParams& c, cudaStream_t s);
+void launch_cut_fixup(const CutParams& c, cudaStream_t s);
 void launch_set_state(const double* pprev, double* pcur, const double* w, long long NX, long long PX, long long rows,
                       double dt, cudaStream_t s);
-void launch_gather(const double* src, const long long* ids, long long n, long long NX, long long PX, double* out,
-                   cudaStream_t s);
+void launch_gather(const double* src, const long long* idx, long long n, double* out, cudaStream_t s);
 void launch_nonfinite(const double* p, long long NX, long long PX, long long rows, unsigned long long* flag,
                       cudaStream_t s);
 int volume_smem_bytes(int N);

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("SEM_LIB") or os.path.join(_HERE, "lib", "libsem.so")
 SEM_F_COUPLING_LITERAL = 1 << 0
 SEM_F_NAN_CHECK = 1 << 1
 SEM_F_NO_GRAPH = 1 << 2
+SEM_F_EMULATE_SLABS = 1 << 3
 
 _STATUS = {0: "SEM_OK", -1: "SEM_E_ARG", -2: "SEM_E_CUDA", -3: "SEM_E_NCCL", -4: "SEM_E_STATE",
            -5: "SEM_E_NONFINITE", -6: "SEM_E_PARTITION", -7: "SEM_E_UNMATCHED", -8: "SEM_E_OOM"}
@@ -58,6 +59,7 @@ def _load():
     P = C.c_void_p
     sig = {
         "sem_mesh_create": [C.POINTER(MeshDesc), C.POINTER(P)],
+        "sem_nccl_unique_id": [C.c_void_p],
         "sem_pmut_attach": [P, C.POINTER(PmutDesc)],
         "sem_dg_interface_build": [P, C.c_int, C.c_int, C.c_double, C.c_int],
         "sem_plane_wave_source": [P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
@@ -86,7 +88,7 @@ def _load():
 
 
 LIB = _load()
-EXPORTED = ("sem_mesh_create", "sem_pmut_attach", "sem_dg_interface_build", "sem_plane_wave_source",
+EXPORTED = ("sem_mesh_create", "sem_nccl_unique_id", "sem_pmut_attach", "sem_dg_interface_build", "sem_plane_wave_source",
             "sem_step", "sem_sync", "sem_read_pressure", "sem_read_pressure_at", "sem_read_modal",
             "sem_write_state", "sem_fill_random_state", "sem_query", "sem_set_profiling", "sem_kernel_time",
             "sem_last_launch_count", "sem_last_error", "sem_destroy")
@@ -120,6 +122,15 @@ def sem_mesh_create(boxes, dt, device=0, stream=None, rank=0, world=1, nccl_uniq
     if st != 0:
         raise SemError(st, "sem_mesh_create failed (descriptor rejected or CUDA unavailable)")
     return out
+
+
+def sem_nccl_unique_id():
+    """128-byte ncclUniqueId (rank 0; broadcast it to the other ranks)."""
+    buf = C.create_string_buffer(128)
+    st = LIB.sem_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if st != 0:
+        raise SemError(st, "sem_nccl_unique_id failed (libnccl.so.2 not loadable?)")
+    return buf.raw
 
 
 def sem_pmut_attach(ctx, pm):
