@@ -129,6 +129,13 @@ typedef struct {
 } sem_pmut_desc;
 sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pm);
 
+/* Host-only (no device touched): the x-slab plan of `world` slabs for these global boxes and (optional)
+ * PMUT array.  slab_x0[world+1] receives the box-0 element index where each slab starts.
+ * SEM_E_PARTITION if nel_x is not divisible by world, a cut crosses a membrane, or a cut is not
+ * aligned with the coarse elements of a 2:1 interface (box 0 +z / box 1 -z tagged INTERFACE). */
+sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, const sem_pmut_desc* pm,
+                         long long* slab_x0);
+
 /* Non-conforming SIPG interface between the +z face of `fine_box` and the -z face of
  * `coarse_box` (Eq. 7's three Gamma_I sums), gamma_F = penalty_alpha cbar^2
  * max(N+, N-)^2 / min(h+, h-) with cbar the harmonic mean of c (reading R7).

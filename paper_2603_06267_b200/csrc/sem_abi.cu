@@ -288,6 +288,33 @@ NcclApi& nccl_api() {
 // ------------------------------------------------------------------------------------------------
 bool nccl_mode(const sem_ctx* ctx) { return ctx->world > 1 && !ctx->emulate; }
 
+// ---- partition rules (shared by sem_mesh_create / sem_pmut_attach / sem_dg_interface_build and the
+//      host-only sem_slab_plan): G equal x-slabs of every box, cuts at the same x for all boxes
+const char* slabs_divisible(const sem_box_desc* boxes, int n, int G) {
+    for (int i = 0; i < n; ++i)
+        if (boxes[i].nel[0] % G) return "nel_x of every box must be divisible by the number of slabs";
+    return nullptr;
+}
+
+// slab owning a membrane spanning [x0, x0 + a] on box g; -1 if a cut crosses or touches it (membranes
+// are never split across GPUs: the paper's membrane-preserving partition)
+int membrane_slab(const sem_box_desc& g, int G, double x0, double a) {
+    const double hx = g.extent[0] / g.nel[0];
+    int slab = 0;
+    for (int r = 1; r < G; ++r) {
+        const double cut = g.origin[0] + hx * (double)(g.nel[0] / G) * r;
+        if (x0 <= cut + 1e-9 * hx && x0 + a >= cut - 1e-9 * hx) return -1;
+        if (x0 > cut) slab = r;
+    }
+    return slab;
+}
+
+// cuts must fall on coarse-element boundaries so every 2:1 interface face pair is slab-local
+bool interface_aligned(const sem_box_desc& F, const sem_box_desc& C, int G) {
+    const int R = F.nel[0] / C.nel[0];
+    return R >= 1 && (F.nel[0] / G) % R == 0;
+}
+
 // Slab `slab` of global box g: elements [ex0, ex0 + nel_loc) along x.  1D tables (coordinates, face
 // masses) are taken from the global lattice, so a cut node keeps its interior (two-sided) mass.
 Box make_slab(const sem_box_desc& g, long long ex0, long long nel_loc, bool cutL, bool cutR) {
@@ -621,6 +648,24 @@ sem_status sem_nccl_unique_id(void* out) {
     return SEM_OK;
 }
 
+sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, const sem_pmut_desc* pm,
+                         long long* slab_x0) {
+    if (!boxes || n_boxes < 1 || n_boxes > 2 || world < 1) return SEM_E_ARG;
+    if (slabs_divisible(boxes, n_boxes, world)) return SEM_E_PARTITION;
+    if (n_boxes == 2 && boxes[0].bc[5] == SEM_BC_INTERFACE && boxes[1].bc[4] == SEM_BC_INTERFACE &&
+        !interface_aligned(boxes[0], boxes[1], world))
+        return SEM_E_PARTITION;
+    if (pm) {
+        if (pm->box < 0 || pm->box >= n_boxes || !pm->center) return SEM_E_ARG;
+        for (int k = 0; k < pm->n_pmut; ++k)
+            if (membrane_slab(boxes[pm->box], world, pm->center[2 * k] - 0.5 * pm->side, pm->side) < 0)
+                return SEM_E_PARTITION;
+    }
+    if (slab_x0)
+        for (int r = 0; r <= world; ++r) slab_x0[r] = (long long)(boxes[0].nel[0] / world) * r;
+    return SEM_OK;
+}
+
 sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
     if (!out) return SEM_E_ARG;
     *out = nullptr;
@@ -659,11 +704,10 @@ sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
     // slab decomposition along x: equal element counts per slab, the same slab boundaries for all
     // boxes (box b's element count must be a multiple of the world size)
     const int G = ctx->world;
-    for (auto& g : ctx->gdesc)
-        if (g.nel[0] % G) {
-            ctx->err = "nel_x of every box must be divisible by the number of slabs";
-            return bail(SEM_E_PARTITION);
-        }
+    if (const char* why = slabs_divisible(ctx->gdesc.data(), (int)ctx->gdesc.size(), G)) {
+        ctx->err = why;
+        return bail(SEM_E_PARTITION);
+    }
     const int first = ctx->emulate ? 0 : ctx->rank;
     const int last = ctx->emulate ? G - 1 : ctx->rank;
     for (int r = first; r <= last; ++r) {
@@ -724,24 +768,16 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
         if (!(pd->modal_mass[m] > 0)) return fail(ctx, SEM_E_ARG, "modal mass must be > 0");
     const int K = pd->n_pmut, M = pd->n_modes;
     const double a = pd->side;
-    // membranes must lie on the face, must not overlap, and must not touch a slab cut (they are never
-    // split across GPUs: the paper's membrane-preserving partition)
-    const double hx = g.extent[0] / g.nel[0];
+    // membranes must lie on the face, must not overlap, and must not touch a slab cut
     const int G = ctx->world;
-    std::vector<double> cuts;
-    for (int r = 1; r < G; ++r) cuts.push_back(g.origin[0] + hx * (double)(g.nel[0] / G) * r);
     ctx->pm_lists.assign(G, {});
     for (int k = 0; k < K; ++k) {
         const double x0 = pd->center[2 * k] - 0.5 * a, y0 = pd->center[2 * k + 1] - 0.5 * a;
         if (x0 < g.origin[0] - 1e-12 * a || y0 < g.origin[1] - 1e-12 * a ||
             x0 + a > g.origin[0] + g.extent[0] + 1e-12 * a || y0 + a > g.origin[1] + g.extent[1] + 1e-12 * a)
             return fail(ctx, SEM_E_ARG, "membrane off the face");
-        int slab = 0;
-        for (size_t c = 0; c < cuts.size(); ++c) {
-            if (x0 <= cuts[c] + 1e-9 * hx && x0 + a >= cuts[c] - 1e-9 * hx)
-                return fail(ctx, SEM_E_PARTITION, "a slab cut crosses a membrane");
-            if (x0 > cuts[c]) slab = (int)c + 1;
-        }
+        const int slab = membrane_slab(g, G, x0, a);
+        if (slab < 0) return fail(ctx, SEM_E_PARTITION, "a slab cut crosses a membrane");
         ctx->pm_lists[slab].push_back(k);
     }
     for (auto& pt : ctx->parts) {
@@ -859,6 +895,8 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
     if (gF.nel[0] % gC.nel[0] || gF.nel[1] % gC.nel[1] || gF.nel[0] / gC.nel[0] != gF.nel[1] / gC.nel[1])
         return fail(ctx, SEM_E_UNMATCHED, "fine lattice does not nest in the coarse one (need h_c = R h_f)");
     const int R = gF.nel[0] / gC.nel[0];
+    if (!interface_aligned(gF, gC, ctx->world))
+        return fail(ctx, SEM_E_PARTITION, "slab cut not aligned to the coarse elements");
     std::vector<double> xf, wf, xc, wc;
     gll_rule(gF.degree, xf, wf);
     gll_rule(gC.degree, xc, wc);
@@ -881,7 +919,6 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
     for (auto& pt : ctx->parts) {
         Box& F = pt.boxes[fine_box];
         Box& C = pt.boxes[coarse_box];
-        if ((F.gx0 / Nf) % R) return fail(ctx, SEM_E_PARTITION, "slab cut not aligned to the coarse elements");
         sem::IfaceParams& p = pt.itf.prm;
         p = sem::IfaceParams{};
         p.NXf = F.NX;

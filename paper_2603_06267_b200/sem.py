@@ -60,6 +60,7 @@ def _load():
     sig = {
         "sem_mesh_create": [C.POINTER(MeshDesc), C.POINTER(P)],
         "sem_nccl_unique_id": [C.c_void_p],
+        "sem_slab_plan": [C.POINTER(BoxDesc), C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_longlong)],
         "sem_pmut_attach": [P, C.POINTER(PmutDesc)],
         "sem_dg_interface_build": [P, C.c_int, C.c_int, C.c_double, C.c_int],
         "sem_plane_wave_source": [P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
@@ -88,7 +89,7 @@ def _load():
 
 
 LIB = _load()
-EXPORTED = ("sem_mesh_create", "sem_nccl_unique_id", "sem_pmut_attach", "sem_dg_interface_build", "sem_plane_wave_source",
+EXPORTED = ("sem_mesh_create", "sem_nccl_unique_id", "sem_slab_plan", "sem_pmut_attach", "sem_dg_interface_build", "sem_plane_wave_source",
             "sem_step", "sem_sync", "sem_read_pressure", "sem_read_pressure_at", "sem_read_modal",
             "sem_write_state", "sem_fill_random_state", "sem_query", "sem_set_profiling", "sem_kernel_time",
             "sem_last_launch_count", "sem_last_error", "sem_destroy")
@@ -105,7 +106,7 @@ def _dptr(a):
 
 
 # ---- thin wrappers with the C names -------------------------------------------------------------
-def sem_mesh_create(boxes, dt, device=0, stream=None, rank=0, world=1, nccl_unique_id=None, flags=0):
+def _box_array(boxes):
     arr = (BoxDesc * len(boxes))()
     for i, b in enumerate(boxes):
         arr[i].origin[:] = [float(v) for v in b["origin"]]
@@ -115,6 +116,23 @@ def sem_mesh_create(boxes, dt, device=0, stream=None, rank=0, world=1, nccl_uniq
         arr[i].c = float(b["c"])
         arr[i].rho = float(b["rho"])
         arr[i].bc[:] = [int(v) for v in b["bc"]]
+    return arr
+
+
+def sem_slab_plan(boxes, world, pm=None):
+    """Host-only partition plan: box-0 element index where each of the `world` slabs starts."""
+    arr = _box_array(boxes)
+    x0 = (C.c_longlong * (world + 1))()
+    pd, keep = (None, None) if pm is None else _pmut_desc(pm)
+    st = LIB.sem_slab_plan(arr, len(boxes), int(world), C.cast(C.byref(pd), C.c_void_p) if pd is not None else None,
+                           x0)
+    if st != 0:
+        raise SemError(st, "sem_slab_plan rejected the partition")
+    return list(x0)
+
+
+def sem_mesh_create(boxes, dt, device=0, stream=None, rank=0, world=1, nccl_unique_id=None, flags=0):
+    arr = _box_array(boxes)
     d = MeshDesc(len(boxes), arr, float(dt), int(device), C.c_void_p(stream) if stream else None, int(rank),
                  int(world), C.cast(C.c_char_p(nccl_unique_id), C.c_void_p) if nccl_unique_id else None, int(flags))
     out = C.c_void_p()
@@ -133,7 +151,7 @@ def sem_nccl_unique_id():
     return buf.raw
 
 
-def sem_pmut_attach(ctx, pm):
+def _pmut_desc(pm):
     K, M = len(pm["centers"]), len(pm["mode_mn"])
     keep = dict(center=np.ascontiguousarray(pm["centers"], np.float64).ravel(),
                 mode=np.ascontiguousarray(pm["mode_mn"], np.int32).ravel(),
@@ -148,6 +166,11 @@ def sem_pmut_attach(ctx, pm):
                  float(pm["t_switch"]) if math.isfinite(pm["t_switch"]) else 1e300,
                  float(pm["capacitance"]), float(pm["amp_v"]), float(pm["f0_hz"]), int(pm["n_cycles"]),
                  _dptr(keep["delay"]))
+    return d, keep
+
+
+def sem_pmut_attach(ctx, pm):
+    d, keep = _pmut_desc(pm)
     _check(ctx, LIB.sem_pmut_attach(ctx, C.byref(d)))
 
 
