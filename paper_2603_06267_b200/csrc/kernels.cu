@@ -65,7 +65,7 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 }
 
 // ------------------------------------------------------------------------------------------------
-// Volume + update kernel
+// Volume + update kernel (persistent, one launch for both boxes of a step)
 // ------------------------------------------------------------------------------------------------
 template <int N, int TY>
 struct VolGeo {
@@ -74,25 +74,31 @@ struct VolGeo {
     static constexpr int SW = vol_pbox_w(N);     // shared P plane pitch (doubles)
     static constexpr int WW = vol_wbox_w(N);     // shared W plane pitch
     static constexpr int SH = TY + 2 * N;
-    static constexpr int D = vol_depth(N);
-    static constexpr int SLOT = vol_slot_bytes(N, TY);
     static constexpr int PBYTES = SW * SH * 8;
     static constexpr int POFF = vol_pbytes_aligned(N, TY);   // W tile offset inside a slot
     static constexpr int WBYTES = WW * TY * 8;
 };
 
-template <int N, int TY>
+// Ring geometry of a launch: depth and slot stride are those of the most demanding box, so that the
+// plane stream of a persistent CTA runs on without a break across tiles and across the two boxes.
+template <int D_, int SLOT_>
+struct Ring {
+    static constexpr int D = D_;
+    static constexpr int SLOT = SLOT_;
+};
+
+template <int N, int TY, class RG>
 __device__ __forceinline__ void vol_issue(const VolParams& p, unsigned char* ring, uint32_t bars, int slot, int z,
                                           int tx0, int ty0) {
     using G = VolGeo<N, TY>;
-    unsigned char* s = ring + slot * G::SLOT;
+    unsigned char* s = ring + slot * RG::SLOT;
     const uint32_t bar = bars + 8u * slot;
     mbar_expect_tx(bar, G::PBYTES + G::WBYTES);
     tma_load_3d(smem_u32(s), &p.tmP, tx0 - G::NH, ty0 - N, z, bar);
     tma_load_3d(smem_u32(s + G::POFF), &p.tmW, tx0, ty0, z, bar);
 }
 
-// Per-thread state of the volume kernel.
+// Per-thread state of the volume kernel (one tile).
 template <int N>
 struct VolThread {
     double cR[N + 1];     // x row of this lane's node (right element, or B0), scaled; zeros if none
@@ -109,10 +115,15 @@ struct VolThread {
     bool valid;
 };
 
-// Ring position of a plane: slot = z mod D and the parity of its fill, advanced incrementally.
+// Ring position of a plane: slot = g mod D and the parity of its fill, advanced incrementally
+// (g counts the planes a CTA has streamed since the launch began).
 struct RingPos {
     int slot;
     uint32_t par;
+    template <int D>
+    __device__ __forceinline__ static RingPos at(unsigned g) {
+        return RingPos{(int)(g % D), (uint32_t)((g / D) & 1u)};
+    }
     template <int D>
     __device__ __forceinline__ void advance() {
         if (++slot == D) {
@@ -248,16 +259,14 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
 // One element layer: planes z0 .. z0+N-1 (plus the top plane N nel_z on the last layer), unrolled by
 // compile-time recursion over the local plane index C so that every z row and window index is a
 // constant.  cur tracks the ring position of plane iz.
-template <int N, int TY, int F, int C>
+template <int N, int TY, class RG, int F, int C>
 __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
-                                               uint32_t bars, int ez, int tx0, int ty0, const double (&zw)[2 * N + 1],
+                                               uint32_t bars, int ez, const double (&zw)[2 * N + 1],
                                                double*& outP, double*& outW, RingPos& cur) {
     if constexpr (C < N || (C == N && (F & kLast))) {
         using G = VolGeo<N, TY>;
-        const int NZ = (int)p.NZ;
-        const int iz = N * ez + C;
-        const double* sP = reinterpret_cast<const double*>(ring + cur.slot * G::SLOT);
-        const double* sW = reinterpret_cast<const double*>(ring + cur.slot * G::SLOT + G::POFF);
+        const double* sP = reinterpret_cast<const double*>(ring + cur.slot * RG::SLOT);
+        const double* sW = reinterpret_cast<const double*>(ring + cur.slot * RG::SLOT + G::POFF);
         vol_plane<N, TY, C, F>(p, t, sP, sW, zw, ez, outP, outW);
         const long long PS = p.PX * p.NY;
         outP += PS;
@@ -265,20 +274,19 @@ __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThre
         // release the slot: one arrival per consumer warp on its "empty" barrier (no block-wide
         // barrier: warps drift across planes and hide each other's latency; the producer warp refills)
         __syncwarp();
-        if (threadIdx.x == 0) mbar_arrive(bars + 8u * (G::D + cur.slot));
-        cur.template advance<G::D>();
-        vol_layer_step<N, TY, F, C + 1>(p, t, ring, bars, ez, tx0, ty0, zw, outP, outW, cur);
+        if (threadIdx.x == 0) mbar_arrive(bars + 8u * (RG::D + cur.slot));
+        cur.template advance<RG::D>();
+        vol_layer_step<N, TY, RG, F, C + 1>(p, t, ring, bars, ez, zw, outP, outW, cur);
     }
 }
 
 // Layer, then slide the window: zw <- planes z0 .. z0 + 2N (read from the ring; plane z0+N+1+j is
 // resident because slots are only refilled after their own plane has been processed).
-template <int N, int TY, int F>
+template <int N, int TY, class RG, int F>
 __device__ __forceinline__ void vol_layer(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
-                                          uint32_t bars, int ez, int tx0, int ty0, double (&zw)[2 * N + 1],
+                                          uint32_t bars, int ez, double (&zw)[2 * N + 1],
                                           double*& outP, double*& outW, RingPos& cur, RingPos& nx) {
-    using G = VolGeo<N, TY>;
-    vol_layer_step<N, TY, F, 0>(p, t, ring, bars, ez, tx0, ty0, zw, outP, outW, cur);
+    vol_layer_step<N, TY, RG, F, 0>(p, t, ring, bars, ez, zw, outP, outW, cur);
     if constexpr (!(F & kLast)) {
 #pragma unroll
         for (int k = 0; k <= N; ++k) zw[k] = zw[k + N];
@@ -288,53 +296,21 @@ __device__ __forceinline__ void vol_layer(const VolParams& p, const VolThread<N>
             zw[N + 1 + j] = 0.0;
             if (N * ez + N + 1 + j < NZ) {
                 mbar_wait(bars + 8u * nx.slot, nx.par);
-                zw[N + 1 + j] = reinterpret_cast<const double*>(ring + nx.slot * G::SLOT)[t.own];
+                zw[N + 1 + j] = reinterpret_cast<const double*>(ring + nx.slot * RG::SLOT)[t.own];
             }
-            nx.template advance<G::D>();
+            nx.template advance<RG::D>();
         }
     }
 }
 
-// Block = TY consumer warps (one tile row each) + 1 producer warp (threadIdx.y == TY) that streams the
-// planes with TMA as soon as all consumers released a ring slot.
-template <int N, int TY>
-__global__ void __launch_bounds__(32 * (TY + 1), SEM_MINB) vol_kernel(const __grid_constant__ VolParams p) {
+// Consumer side of one tile (TXE x TY node column, all z): planes g0 .. g0 + NZ - 1 of the ring.
+template <int N, int TY, class RG>
+__device__ __forceinline__ void vol_tile(const VolParams& p, unsigned char* ring, uint32_t bars, int tx0, int ty0,
+                                         unsigned g0) {
     using G = VolGeo<N, TY>;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    unsigned char* ring = smem_raw;   // direct indexing keeps the shared address space (LDS, not generic LD)
-    const uint32_t bars = smem_u32(ring + G::D * G::SLOT);
     const int lane = threadIdx.x, ly = threadIdx.y;
-    const int tx0 = blockIdx.x * G::TXE, ty0 = blockIdx.y * TY;
     const long long NX = p.NX, NY = p.NY;
     const int NZ = (int)p.NZ;
-
-    if (lane == 0 && ly == 0) {
-        for (int s = 0; s < G::D; ++s) {
-            mbar_init(bars + 8u * s, 1);               // full: TMA transaction bytes
-            mbar_init(bars + 8u * (G::D + s), TY);     // empty: one arrival per consumer warp
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-    if (ly == TY) {   // producer warp
-        if (lane == 0) {
-            for (int z = 0; z < G::D && z < NZ; ++z) vol_issue<N, TY>(p, ring, bars, z, z, tx0, ty0);
-            int slot = 0;
-            uint32_t par = 0;
-            for (int z = G::D; z < NZ; ++z) {   // plane z reuses the slot of plane z - D
-                while (!mbar_try_wait(bars + 8u * (G::D + slot), par)) __nanosleep(64);   // leave issue slots to consumers
-                vol_issue<N, TY>(p, ring, bars, slot, z, tx0, ty0);
-                if (++slot == G::D) {
-                    slot = 0;
-                    par ^= 1u;
-                }
-            }
-        }
-        return;
-    }
-
-    // ---- thread setup (overlaps the first TMA loads)
     const BoxTables& T = p.tab;
     VolThread<N> t;
     const long long ix = tx0 + lane, iy = ty0 + ly;
@@ -378,7 +354,6 @@ __global__ void __launch_bounds__(32 * (TY + 1), SEM_MINB) vol_kernel(const __gr
         if (iy == 0) t.dxy += p.damp[2];
         if (iy == NY - 1) t.dxy += p.damp[3];
     }
-    const long long n0 = __ldcg(p.step);   // step index of this launch (bumped by the last block)
     const long long off = t.valid ? iy * p.PX + ix : 0;
     double* outP = p.Pn + off;
     double* outW = p.W + off;
@@ -387,90 +362,232 @@ __global__ void __launch_bounds__(32 * (TY + 1), SEM_MINB) vol_kernel(const __gr
     double zw[2 * N + 1];
 #pragma unroll
     for (int k = 0; k < N; ++k) zw[k] = 0.0;
+    RingPos w = RingPos::at<RG::D>(g0);
 #pragma unroll
     for (int k = 0; k <= N; ++k) {
         zw[N + k] = 0.0;
         if (k < NZ) {
-            mbar_wait(bars + 8u * (k % G::D), (uint32_t)((k / G::D) & 1));
-            zw[N + k] = reinterpret_cast<const double*>(ring + (k % G::D) * G::SLOT)[t.own];
+            mbar_wait(bars + 8u * w.slot, w.par);
+            zw[N + k] = reinterpret_cast<const double*>(ring + w.slot * RG::SLOT)[t.own];
         }
+        w.template advance<RG::D>();
     }
 
     const int nelz = p.nelz;
-    RingPos cur{0, 0u}, nx{(N + 1) % G::D, (uint32_t)(((N + 1) / G::D) & 1)};
+    RingPos cur = RingPos::at<RG::D>(g0), nx = RingPos::at<RG::D>(g0 + N + 1);
     if (nelz == 1) {
-        vol_layer<N, TY, kFirst | kLast>(p, t, ring, bars, 0, tx0, ty0, zw, outP, outW, cur, nx);
+        vol_layer<N, TY, RG, kFirst | kLast>(p, t, ring, bars, 0, zw, outP, outW, cur, nx);
     } else {
-        vol_layer<N, TY, kFirst>(p, t, ring, bars, 0, tx0, ty0, zw, outP, outW, cur, nx);
+        vol_layer<N, TY, RG, kFirst>(p, t, ring, bars, 0, zw, outP, outW, cur, nx);
         for (int ez = 1; ez < nelz - 1; ++ez)
-            vol_layer<N, TY, 0>(p, t, ring, bars, ez, tx0, ty0, zw, outP, outW, cur, nx);
-        vol_layer<N, TY, kLast>(p, t, ring, bars, nelz - 1, tx0, ty0, zw, outP, outW, cur, nx);
+            vol_layer<N, TY, RG, 0>(p, t, ring, bars, ez, zw, outP, outW, cur, nx);
+        vol_layer<N, TY, RG, kLast>(p, t, ring, bars, nelz - 1, zw, outP, outW, cur, nx);
+    }
+}
+
+// Launch-wide ring of a (N0, N1) pair (N1 = 0: one box).
+template <int N0, int N1, int TY>
+struct PairRing {
+    static constexpr int D = cmax(vol_depth(N0), N1 ? vol_depth(N1) : 0);
+    static constexpr int SLOT = cmax(vol_slot_bytes(N0, TY), N1 ? vol_slot_bytes(N1, TY) : 0);
+    using RG = Ring<D, SLOT>;
+};
+
+// Persistent CTAs (one per SM): TY consumer warps (one tile row each) + 1 producer warp
+// (threadIdx.y == TY).  The producer takes tiles from a launch-wide counter (the boxes' tiles in one
+// list, the larger tiles of box 1 first) and streams every plane of each with TMA into the ring as soon
+// as all consumer warps released a slot; the tile index travels with the first plane of its tile (a
+// per-slot header, published by the mbarrier arrive).  The stream never stops at a tile boundary, so
+// the next tile's first planes are already in flight while the consumers finish the current one.
+template <int N0, int N1, int TY>
+__global__ void __launch_bounds__(32 * (TY + 1), SEM_MINB) vol_kernel(const __grid_constant__ VolLaunch L) {
+    using RG = typename PairRing<N0, N1, TY>::RG;
+    constexpr int D = RG::D;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char* ring = smem_raw;   // direct indexing keeps the shared address space (LDS, not generic LD)
+    const uint32_t bars = smem_u32(ring + D * RG::SLOT);
+    volatile int* tileq = reinterpret_cast<volatile int*>(ring + D * RG::SLOT + 2 * D * 8);
+    const int lane = threadIdx.x, ly = threadIdx.y;
+    const unsigned n1 = N1 ? L.ntiles[1] : 0u;
+    const unsigned ntot = n1 + L.ntiles[0];
+
+    if (lane == 0 && ly == 0) {
+        for (int s = 0; s < D; ++s) {
+            mbar_init(bars + 8u * s, 1);               // full: TMA transaction bytes (or the end marker)
+            mbar_init(bars + 8u * (D + s), TY);        // empty: one arrival per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (ly == TY) {   // producer warp
+        if (lane == 0) {
+            unsigned g = 0;
+            for (;;) {
+                const unsigned tile = atomicAdd(L.sched, 1u);
+                const int box = (N1 > 0 && tile < n1) ? 1 : (tile < ntot ? 0 : -1);
+                if (box < 0) {   // end marker: a header of -1 on the next slot, completed without data
+                    const int slot = (int)(g % D);
+                    if (g >= (unsigned)D)
+                        while (!mbar_try_wait(bars + 8u * (D + slot), ((g / D) - 1u) & 1u)) __nanosleep(64);
+                    tileq[slot] = -1;
+                    mbar_arrive(bars + 8u * slot);
+                    break;
+                }
+                const unsigned lt = box ? tile : tile - n1;
+                const VolParams& p = L.box[box];
+                const int NZ = (int)p.NZ;
+                const int tx0 = (int)(lt % L.ntx[box]) * (box ? vol_txe(N1 ? N1 : 1) : vol_txe(N0));
+                const int ty0 = (int)(lt / L.ntx[box]) * TY;
+                for (int z = 0; z < NZ; ++z, ++g) {   // plane g reuses the slot of plane g - D
+                    const int slot = (int)(g % D);
+                    if (g >= (unsigned)D)
+                        while (!mbar_try_wait(bars + 8u * (D + slot), ((g / D) - 1u) & 1u)) __nanosleep(64);
+                    if (z == 0) tileq[slot] = (int)tile;
+                    if constexpr (N1 > 0) {
+                        if (box) vol_issue<N1, TY, RG>(L.box[1], ring, bars, slot, z, tx0, ty0);
+                        else vol_issue<N0, TY, RG>(L.box[0], ring, bars, slot, z, tx0, ty0);
+                    } else {
+                        vol_issue<N0, TY, RG>(L.box[0], ring, bars, slot, z, tx0, ty0);
+                    }
+                }
+            }
+        }
+        return;
     }
 
-    if (p.bump_step) {
-        if (lane == 0 && ly == 0) {
-            __threadfence();
-            const unsigned prev = atomicAdd(p.done, 1u);
-            if (prev == p.total_blocks - 1) {
-                *p.step = n0 + 1;
-                *p.done = 0u;
-                __threadfence();
+    // consumers: follow the tiles in the order the producer streams them
+    unsigned g = 0;
+    for (;;) {
+        const RingPos h = RingPos::at<D>(g);
+        mbar_wait(bars + 8u * h.slot, h.par);
+        const int tile = tileq[h.slot];
+        if (tile < 0) break;
+        if (N1 > 0 && (unsigned)tile < n1) {
+            if constexpr (N1 > 0) {
+                const VolParams& p = L.box[1];
+                const unsigned lt = (unsigned)tile;
+                vol_tile<N1, TY, RG>(p, ring, bars, (int)(lt % L.ntx[1]) * vol_txe(N1), (int)(lt / L.ntx[1]) * TY, g);
+                g += (unsigned)p.NZ;
             }
+        } else {
+            const VolParams& p = L.box[0];
+            const unsigned lt = (unsigned)tile - n1;
+            vol_tile<N0, TY, RG>(p, ring, bars, (int)(lt % L.ntx[0]) * vol_txe(N0), (int)(lt / L.ntx[0]) * TY, g);
+            g += (unsigned)p.NZ;
+        }
+    }
+
+    // end of the launch: the last CTA resets the tile scheduler and (last launch of the step) bumps the
+    // device step counter.  The named barrier keeps every consumer warp of this CTA (which may still
+    // read the step counter in its last plane) ahead of the bump.
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * TY) : "memory");
+    if (lane == 0 && ly == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(L.sched + 1, 1u);
+        if (prev == gridDim.x - 1) {
+            L.sched[0] = 0u;
+            L.sched[1] = 0u;
+            if (L.bump_step) *L.step += 1;
+            __threadfence();
         }
     }
 }
 
 constexpr int kTY = SEM_KTY;   // consumer rows per CTA (+1 producer warp)
 
-template <int N>
-static void prepare_vol_N() {
-    cudaFuncSetAttribute(vol_kernel<N, kTY>, cudaFuncAttributeMaxDynamicSharedMemorySize, vol_smem_bytes(N, kTY));
-}
+template <int N0, int N1>
+struct VolInst {
+    static int smem() {
+        using R = PairRing<N0, N1, kTY>;
+        return R::D * R::SLOT + 2 * R::D * 8 + R::D * 4 + 128;
+    }
+    static int ctas_per_sm() {   // resident CTAs per SM (occupancy), cached
+        static int occ = -1;
+        if (occ < 0) {
+            cudaFuncSetAttribute(vol_kernel<N0, N1, kTY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem());
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vol_kernel<N0, N1, kTY>, 32 * (kTY + 1),
+                                                              smem()) != cudaSuccess || occ < 1)
+                occ = 1;
+        }
+        return occ;
+    }
+    static void launch(const VolLaunch& L, cudaStream_t s) {
+        static int nsm = 0;
+        if (!nsm) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const unsigned ntot = L.ntiles[0] + (N1 ? L.ntiles[1] : 0u);
+        unsigned grid = (unsigned)(nsm * ctas_per_sm());
+        if (grid > ntot) grid = ntot;
+        vol_kernel<N0, N1, kTY><<<grid, dim3(32, kTY + 1), smem(), s>>>(L);
+    }
+};
 
 void volume_prepare(int N) {
     switch (N) {
-        case 1: prepare_vol_N<1>(); break;
-        case 2: prepare_vol_N<2>(); break;
-        case 3: prepare_vol_N<3>(); break;
-        case 4: prepare_vol_N<4>(); break;
-        case 5: prepare_vol_N<5>(); break;
-        case 6: prepare_vol_N<6>(); break;
-        case 7: prepare_vol_N<7>(); break;
-        case 8: prepare_vol_N<8>(); break;
+        case 1: VolInst<1, 0>::ctas_per_sm(); break;
+        case 2: VolInst<2, 0>::ctas_per_sm(); break;
+        case 3: VolInst<3, 0>::ctas_per_sm(); break;
+        case 4: VolInst<4, 0>::ctas_per_sm(); break;
+        case 5: VolInst<5, 0>::ctas_per_sm(); break;
+        case 6: VolInst<6, 0>::ctas_per_sm(); break;
+        case 7: VolInst<7, 0>::ctas_per_sm(); break;
+        case 8: VolInst<8, 0>::ctas_per_sm(); break;
         default: break;
     }
 }
 
-template <int N>
-static void launch_vol_N(const VolParams& p, cudaStream_t s) {
-    using G = VolGeo<N, kTY>;
-    const int smem = vol_smem_bytes(N, kTY);
-    dim3 blk(32, kTY + 1);
-    dim3 grd((unsigned)((p.NX + G::TXE - 1) / G::TXE), (unsigned)((p.NY + kTY - 1) / kTY));
-    vol_kernel<N, kTY><<<grd, blk, smem, s>>>(p);
+bool volume_pair_supported(int N0, int N1) { return N0 == 5 && N1 == 3; }
+
+void volume_pair_prepare(int N0, int N1) {
+    if (N0 == 5 && N1 == 3) VolInst<5, 3>::ctas_per_sm();
 }
 
-void launch_volume(const VolParams& p, int N, cudaStream_t s) {
+void fill_tiles(VolLaunch& L) {
+    for (int b = 0; b < L.nbox; ++b) {
+        const VolParams& p = L.box[b];
+        const int txe = vol_txe(p.N);
+        L.ntx[b] = (unsigned)((p.NX + txe - 1) / txe);
+        L.ntiles[b] = L.ntx[b] * (unsigned)((p.NY + kTY - 1) / kTY);
+    }
+}
+
+void launch_volume(VolLaunch L, cudaStream_t s) {
+    fill_tiles(L);
+    if (L.nbox == 2) {
+        if (L.box[0].N == 5 && L.box[1].N == 3) VolInst<5, 3>::launch(L, s);
+        return;
+    }
+    switch (L.box[0].N) {
+        case 1: VolInst<1, 0>::launch(L, s); break;
+        case 2: VolInst<2, 0>::launch(L, s); break;
+        case 3: VolInst<3, 0>::launch(L, s); break;
+        case 4: VolInst<4, 0>::launch(L, s); break;
+        case 5: VolInst<5, 0>::launch(L, s); break;
+        case 6: VolInst<6, 0>::launch(L, s); break;
+        case 7: VolInst<7, 0>::launch(L, s); break;
+        case 8: VolInst<8, 0>::launch(L, s); break;
+        default: break;
+    }
+}
+
+int volume_smem_bytes(int N) {
     switch (N) {
-        case 1: launch_vol_N<1>(p, s); break;
-        case 2: launch_vol_N<2>(p, s); break;
-        case 3: launch_vol_N<3>(p, s); break;
-        case 4: launch_vol_N<4>(p, s); break;
-        case 5: launch_vol_N<5>(p, s); break;
-        case 6: launch_vol_N<6>(p, s); break;
-        case 7: launch_vol_N<7>(p, s); break;
-        case 8: launch_vol_N<8>(p, s); break;
-        default: break;
+        case 1: return VolInst<1, 0>::smem();
+        case 2: return VolInst<2, 0>::smem();
+        case 3: return VolInst<3, 0>::smem();
+        case 4: return VolInst<4, 0>::smem();
+        case 5: return VolInst<5, 0>::smem();
+        case 6: return VolInst<6, 0>::smem();
+        case 7: return VolInst<7, 0>::smem();
+        case 8: return VolInst<8, 0>::smem();
+        default: return 0;
     }
 }
-
-int volume_smem_bytes(int N) { return vol_smem_bytes(N, kTY); }
 int volume_tile_y() { return kTY; }
-
-unsigned volume_blocks(int N, long long NX, long long NY) {
-    const int txe = vol_txe(N);
-    return (unsigned)(((NX + txe - 1) / txe) * ((NY + kTY - 1) / kTY));
-}
 
 // ------------------------------------------------------------------------------------------------
 // Modal kernel: one warp per PMUT

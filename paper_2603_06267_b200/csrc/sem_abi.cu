@@ -355,6 +355,7 @@ sem::VolParams vol_params(sem_ctx* ctx, sem::Part& pt, int bi, int cur) {
     p.NY = b.NY;
     p.NZ = b.NZ;
     p.PX = b.PX;
+    p.N = b.N;
     for (int d = 0; d < 3; ++d) p.sdir[d] = b.d.c * b.d.c * (2.0 / b.h[d]) * (2.0 / b.h[d]);
     p.nelz = b.d.nel[2];
     p.dt = ctx->dt;
@@ -390,12 +391,6 @@ sem::VolParams vol_params(sem_ctx* ctx, sem::Part& pt, int bi, int cur) {
         p.yc = b.yc;
     }
     p.step = ctx->d_step;
-    p.done = ctx->d_done;
-    unsigned tot = 0;
-    for (auto& q : ctx->parts)
-        for (auto& bb : q.boxes) tot += sem::volume_blocks(bb.N, bb.NX, bb.NY);
-    p.total_blocks = tot;
-    p.bump_step = 1;
     return p;
 }
 
@@ -540,11 +535,35 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
         }
     }
     mark(0, true);
-    for (auto& pt : ctx->parts)
-        for (int bi = 0; bi < (int)pt.boxes.size(); ++bi) {
-            sem::launch_volume(vol_params(ctx, pt, bi, cur), pt.boxes[bi].N, s);
+    {
+        // persistent volume launches: both boxes of a slab in one launch when the degree pair is
+        // instantiated (5/3 of configs 2-4), else one launch per box; each has its own scheduler pair
+        std::vector<sem::VolLaunch> ls;
+        for (auto& pt : ctx->parts) {
+            const int nb = (int)pt.boxes.size();
+            if (nb == 2 && sem::volume_pair_supported(pt.boxes[0].N, pt.boxes[1].N)) {
+                sem::VolLaunch L{};
+                L.nbox = 2;
+                L.box[0] = vol_params(ctx, pt, 0, cur);
+                L.box[1] = vol_params(ctx, pt, 1, cur);
+                ls.push_back(L);
+            } else {
+                for (int bi = 0; bi < nb; ++bi) {
+                    sem::VolLaunch L{};
+                    L.nbox = 1;
+                    L.box[0] = vol_params(ctx, pt, bi, cur);
+                    ls.push_back(L);
+                }
+            }
+        }
+        for (size_t i = 0; i < ls.size(); ++i) {
+            ls[i].sched = ctx->d_sched + 2 * (i % sem_ctx::kSchedPairs);
+            ls[i].step = ctx->d_step;
+            ls[i].bump_step = i + 1 == ls.size() ? 1 : 0;
+            sem::launch_volume(ls[i], s);
             ++nl;
         }
+    }
     mark(0, false);
     if (slabs) {
         if (!ctx->emulate) cudaStreamWaitEvent(s, ctx->ev_join, 0);
@@ -561,7 +580,7 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
 
 sem_status reset_dynamic(sem_ctx* ctx) {
     CU(cudaMemsetAsync(ctx->d_step, 0, sizeof(long long), ctx->stream));
-    CU(cudaMemsetAsync(ctx->d_done, 0, sizeof(unsigned), ctx->stream));
+    CU(cudaMemsetAsync(ctx->d_sched, 0, 2 * sem_ctx::kSchedPairs * sizeof(unsigned), ctx->stream));
     for (auto& pt : ctx->parts) {
         if (!pt.pm.on) continue;
         const size_t nm = (size_t)pt.pm.n_pmut * pt.pm.n_modes;
@@ -612,6 +631,7 @@ sem_status setup_part_buffers(sem_ctx* ctx, sem::Part& pt) {
             upload(ctx, &b.my, b.myh))
             return SEM_E_CUDA;
         sem::volume_prepare(b.N);
+        if (pt.boxes.size() == 2) sem::volume_pair_prepare(pt.boxes[0].N, pt.boxes[1].N);
         const int TY = sem::volume_tile_y();
         if (!make_map(&b.tmP[0], b.P[0], b, sem::vol_pbox_w(b.N), TY + 2 * b.N) ||
             !make_map(&b.tmP[1], b.P[1], b, sem::vol_pbox_w(b.N), TY + 2 * b.N) ||
@@ -723,7 +743,7 @@ sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
     }
     for (auto& pt : ctx->parts)
         if (setup_part_buffers(ctx, pt) != SEM_OK) return bail(SEM_E_OOM);
-    if (dalloc(ctx, &ctx->d_step, 1) || dalloc(ctx, &ctx->d_done, 1) || dalloc(ctx, &ctx->d_flag, 1))
+    if (dalloc(ctx, &ctx->d_step, 1) || dalloc(ctx, &ctx->d_sched, 2 * sem_ctx::kSchedPairs) || dalloc(ctx, &ctx->d_flag, 1))
         return bail(SEM_E_OOM);
     if (cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)

@@ -22,6 +22,7 @@ constexpr int kPref = SEM_KPREF;  // volume kernel: planes prefetched beyond the
 // TXE = N floor(31/N) computed nodes (whole elements); lane 31 is the "virtual left neighbour"
 // that evaluates the left-element row of lane 0's shared node from the halo.
 // TMA box x-starts must be 16 B aligned: TXE is even and the x halo is NH = N rounded up to even.
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int vol_txe(int N) { return (N * (31 / N)) % 2 ? N * (31 / N) - N : N * (31 / N); }
 __host__ __device__ constexpr int vol_nh(int N) { return N + (N & 1); }
 __host__ __device__ constexpr int vol_pbox_w(int N) { return vol_txe(N) + 2 * vol_nh(N); }
@@ -66,6 +67,7 @@ struct VolParams {
     double* __restrict__ W;         // w^n in, w^{n+1} out (in place)
     long long NX, NY, NZ;           // node counts of the (local) box
     long long PX;                   // row pitch (doubles) of the device layout
+    int N;                          // GLL degree of the box
     double sdir[3];                 // s_d = c^2 (2/h_d)^2: scale of the compile-time reference rows
     int nelz;
     double dt;
@@ -87,10 +89,19 @@ struct VolParams {
     double pw_k[3], pw_xref[3], pw_c, pw_t0, pw_sigma, pw_om, pw_ztop;
     const double* __restrict__ xc; // node x coordinates [NX]
     const double* __restrict__ yc; // node y coordinates [NY]
-    // step bookkeeping (device): t^{n+1} = (step + 1) dt; last block increments step
-    long long* step;
-    unsigned int* done;
-    unsigned int total_blocks;
+    // device step counter: t^{n+1} = (step + 1) dt (read by the plane-wave source)
+    const long long* step;
+};
+
+// One persistent volume launch: one or two boxes (box[1] of degree N1 != N0 shares the launch so
+// that a single plane stream per SM covers the whole step; see vol_kernel).
+struct VolLaunch {
+    VolParams box[2];
+    int nbox;                       // 1 or 2
+    unsigned ntx[2];                // tiles along x per box (filled by launch_volume)
+    unsigned ntiles[2];             // tiles per box
+    unsigned int* sched;            // [0] next tile, [1] finished CTAs; reset by the launch's last CTA
+    long long* step;                // device step counter, bumped by the last CTA if bump_step
     int bump_step;                  // 1 for the last volume launch of a step
 };
 
@@ -248,7 +259,8 @@ struct sem_ctx {
     int cur = 0;                 // P[cur] = p^{step+1}, P[1-cur] = p^{step}
     long long step = 0;          // host mirror of the device counter
     long long* d_step = nullptr;
-    unsigned int* d_done = nullptr;
+    unsigned int* d_sched = nullptr;  // tile scheduler pairs, one per volume launch of a step
+    static constexpr int kSchedPairs = 64;
     unsigned long long* d_flag = nullptr;
     cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [parity][1 or 2 steps]
     long long graph_launches[2][2] = {{0, 0}, {0, 0}};
@@ -266,7 +278,9 @@ struct sem_ctx {
 
 namespace sem {
 // kernels.cu
-void launch_volume(const VolParams& p, int N, cudaStream_t s);
+void launch_volume(VolLaunch L, cudaStream_t s);
+bool volume_pair_supported(int N0, int N1);
+void volume_pair_prepare(int N0, int N1);
 void launch_modal(const ModalParams& p, cudaStream_t s);
 void launch_iface(const IfaceParams& p, cudaStream_t s);
 void launch_fill_random(double* p, double* w, double* pn, long long NX, long long PX, long long rows,
@@ -282,5 +296,4 @@ void launch_nonfinite(const double* p, long long NX, long long PX, long long row
 int volume_smem_bytes(int N);
 int volume_tile_y();
 void volume_prepare(int N);
-unsigned volume_blocks(int N, long long NX, long long NY);
 }  // namespace sem
