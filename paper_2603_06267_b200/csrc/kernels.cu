@@ -26,6 +26,18 @@
 #ifndef SEM_MINB
 #define SEM_MINB 1
 #endif
+#ifndef SEM_L2HINT
+#define SEM_L2HINT 0
+#endif
+// launch bounds of the volume kernel; SEM_MAXREG caps registers explicitly (__maxnreg__)
+#ifdef SEM_MAXREG
+#define SEM_VOL_BOUNDS(TY) __maxnreg__(SEM_MAXREG)
+#else
+#define SEM_VOL_BOUNDS(TY) __launch_bounds__(32 * (TY + 1), SEM_MINB)
+#endif
+#ifndef SEM_CROWS
+#define SEM_CROWS 0
+#endif
 
 namespace sem {
 
@@ -63,6 +75,25 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
         ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
         : "memory");
 }
+// same with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap* map, int x, int y, int z,
+                                                 uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 
 // ------------------------------------------------------------------------------------------------
 // Volume + update kernel (persistent, one launch for both boxes of a step)
@@ -94,8 +125,26 @@ __device__ __forceinline__ void vol_issue(const VolParams& p, unsigned char* rin
     unsigned char* s = ring + slot * RG::SLOT;
     const uint32_t bar = bars + 8u * slot;
     mbar_expect_tx(bar, G::PBYTES + G::WBYTES);
+#if SEM_L2HINT
+    // p planes are re-read by the neighbouring tiles (halo): keep; w is read once: evict first
+    tma_load_3d_hint(smem_u32(s), &p.tmP, tx0 - G::NH, ty0 - N, z, bar, policy_evict_last());
+    tma_load_3d_hint(smem_u32(s + G::POFF), &p.tmW, tx0, ty0, z, bar, policy_evict_first());
+#else
     tma_load_3d(smem_u32(s), &p.tmP, tx0 - G::NH, ty0 - N, z, bar);
     tma_load_3d(smem_u32(s + G::POFF), &p.tmW, tx0, ty0, z, bar);
+#endif
+}
+
+// Output stores of the volume kernel (SEM_STORE: 0 streaming .cs, 1 default write-back policy)
+#ifndef SEM_STORE
+#define SEM_STORE 1
+#endif
+__device__ __forceinline__ void st_out(double* p, double v) {
+#if SEM_STORE == 0
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
 }
 
 // Per-thread state of the volume kernel (one tile).
@@ -141,26 +190,32 @@ __device__ constexpr gllc::Tables<N> kRef = gllc::make_tables<N>();
 constexpr int kFirst = 1, kLast = 2;
 
 // One plane: a = -(M^-1 K p)_i - C_ii/M_ii w_i + extras;  w <- w + dt a;  p <- p + dt w.
+// Returns the new (w, p) of this thread's node; the caller stores them.
 template <int N, int TY, int C, int F>
 __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>& t, const double* __restrict__ sP,
                                           const double* __restrict__ sW, const double (&zw)[2 * N + 1], int ez,
-                                          double* __restrict__ outP, double* __restrict__ outW) {
+                                          double& wn_out, double& pn_out) {
     using G = VolGeo<N, TY>;
     const BoxTables& T = p.tab;
 #ifdef SEM_MEMONLY   // diagnostic build: same data movement, no stencil arithmetic
     {
         const double wv = sW[t.wown];
-        const double pv = zw[N + C];
-        if (t.valid) {
-            __stcs(outW, wv);
-            __stcs(outP, fma(p.dt, wv, pv));
-        }
+        wn_out = wv;
+        pn_out = fma(p.dt, wv, zw[N + C]);
         return;
     }
 #endif
     // ---- x: right-element row with per-lane (scaled) coefficients; the left-element row of a shared
-    //      node uses the compile-time reference row L and is evaluated by lane-1, then shuffled
+    //      node (row L) is evaluated by lane-1, then shuffled.  Warp-uniform rows (x/y left rows, all
+    //      z rows) are read from the kernel-parameter constant bank as DFMA operands: no registers.
+#if SEM_CROWS
+    const double* Lx = T.G[0][row_L(N)];
+    const double* Ly = T.G[1][row_L(N)];
+#else
     const auto& RT = kRef<N>;
+    const double* Lx = RT.L;
+    const double* Ly = RT.L;
+#endif
     double v[N + 1];
 #pragma unroll
     for (int b = 0; b <= N; ++b) v[b] = sP[t.xb + b];
@@ -168,10 +223,10 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
 #pragma unroll
     for (int b = 0; b <= N; ++b) {
         xr = fma(t.cR[b], v[b], xr);
-        xl = fma(RT.L[b], v[b], xl);
+        xl = fma(Lx[b], v[b], xl);
     }
     const double xlr = __shfl_sync(0xffffffffu, xl, (threadIdx.x + 31) & 31);
-    // ---- y: per-warp row (registers, scaled); left row of a shared node: reference L, scaled
+    // ---- y: per-warp row (registers, scaled); left row of a shared node: row L
     double y0 = 0.0, y1 = 0.0;
 #pragma unroll
     for (int b = 0; b <= N; b += 2) y0 = fma(t.cyR[b], sP[t.yb + b * G::SW], y0);
@@ -181,11 +236,33 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
     if (t.yLs != 0.0) {
         double yl = 0.0;
 #pragma unroll
-        for (int b = 0; b <= N; ++b) yl = fma(RT.L[b], sP[t.yl + b * G::SW], yl);
+        for (int b = 0; b <= N; ++b) yl = fma(Ly[b], sP[t.yl + b * G::SW], yl);
         acc = fma(t.yLs, yl, acc);
     }
-    // ---- z: register window zw[k] = p(z0 - N + k), compile-time reference rows, scaled once
+    // ---- z: register window zw[k] = p(z0 - N + k), rows by compile-time plane class
     double z0 = 0.0, z1 = 0.0;
+#if SEM_CROWS
+    {
+        constexpr bool top = (C == N), bot = (C == 0 && (F & kFirst)), shared = (C == 0 && !(F & kFirst));
+        const double* Rz = T.G[2][top ? row_BN(N) : bot ? row_B0(N) : C];
+        if constexpr (shared) {
+            const double* Lz = T.G[2][row_L(N)];
+#pragma unroll
+            for (int b = 0; b <= N; ++b) z0 = fma(Rz[b], zw[N + b], z0);
+#pragma unroll
+            for (int b = 0; b <= N; ++b) z1 = fma(Lz[b], zw[b], z1);
+        } else {
+            // BN is the left-element row: it multiplies planes z0 - N .. z0 (window N-N+C .. N+C = 0..N
+            // at C = N); every other row multiplies the right element z0 .. z0 + N
+            constexpr int base = top ? 0 : N;
+#pragma unroll
+            for (int b = 0; b <= N; b += 2) z0 = fma(Rz[b], zw[base + b], z0);
+#pragma unroll
+            for (int b = 1; b <= N; b += 2) z1 = fma(Rz[b], zw[base + b], z1);
+        }
+    }
+    acc += z0 + z1;
+#else
     if constexpr (C == N) {   // top boundary plane: left element only, BN = 2 L
 #pragma unroll
         for (int b = 0; b <= N; b += 2) z0 = fma(2.0 * RT.L[b], zw[N + b], z0);
@@ -208,6 +285,7 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
         for (int b = 1; b <= N; b += 2) z1 = fma(RT.R[C][b], zw[N + b], z1);
     }
     acc = fma(p.sdir[2], z0 + z1, acc);
+#endif
     double a = -acc;
     const double wv = sW[t.wown];
     const double pv = zw[N + C];
@@ -248,35 +326,70 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
             a -= __ldg(p.sig + t.fc) * T.ksig[N];   // shared plane z = N of the first layer
     }
     a = fma(-damp, wv, a);
-    const double wn = fma(p.dt, a, wv);
-    const double pn = fma(p.dt, wn, pv);
-    if (t.valid) {
-        __stcs(outW, wn);
-        __stcs(outP, pn);
-    }
+    wn_out = fma(p.dt, a, wv);
+    pn_out = fma(p.dt, wn_out, pv);
 }
 
 // One element layer: planes z0 .. z0+N-1 (plus the top plane N nel_z on the last layer), unrolled by
 // compile-time recursion over the local plane index C so that every z row and window index is a
-// constant.  cur tracks the ring position of plane iz.
+// constant.  cur tracks the ring position of plane iz.  With SEM_PAIR, two planes are evaluated
+// together (independent dependency chains interleave: twice the ILP per consumer warp) before their
+// stores and slot releases.
+#ifndef SEM_PAIR
+#define SEM_PAIR 1
+#endif
 template <int N, int TY, class RG, int F, int C>
 __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
                                                uint32_t bars, int ez, const double (&zw)[2 * N + 1],
                                                double*& outP, double*& outW, RingPos& cur) {
-    if constexpr (C < N || (C == N && (F & kLast))) {
+    constexpr int NP = (F & kLast) ? N + 1 : N;   // planes of this layer
+    if constexpr (C < NP) {
         using G = VolGeo<N, TY>;
-        const double* sP = reinterpret_cast<const double*>(ring + cur.slot * RG::SLOT);
-        const double* sW = reinterpret_cast<const double*>(ring + cur.slot * RG::SLOT + G::POFF);
-        vol_plane<N, TY, C, F>(p, t, sP, sW, zw, ez, outP, outW);
         const long long PS = p.PX * p.NY;
-        outP += PS;
-        outW += PS;
-        // release the slot: one arrival per consumer warp on its "empty" barrier (no block-wide
-        // barrier: warps drift across planes and hide each other's latency; the producer warp refills)
-        __syncwarp();
-        if (threadIdx.x == 0) mbar_arrive(bars + 8u * (RG::D + cur.slot));
-        cur.template advance<RG::D>();
-        vol_layer_step<N, TY, RG, F, C + 1>(p, t, ring, bars, ez, zw, outP, outW, cur);
+        if constexpr (SEM_PAIR && C + 1 < NP) {
+            RingPos nxt = cur;
+            nxt.template advance<RG::D>();
+            const unsigned char* s0 = ring + cur.slot * RG::SLOT;
+            const unsigned char* s1 = ring + nxt.slot * RG::SLOT;
+            double w0, p0, w1, p1;
+            vol_plane<N, TY, C, F>(p, t, reinterpret_cast<const double*>(s0),
+                                   reinterpret_cast<const double*>(s0 + G::POFF), zw, ez, w0, p0);
+            vol_plane<N, TY, C + 1, F>(p, t, reinterpret_cast<const double*>(s1),
+                                       reinterpret_cast<const double*>(s1 + G::POFF), zw, ez, w1, p1);
+            if (t.valid) {
+                st_out(outW, w0);
+                st_out(outP, p0);
+                st_out(outW + PS, w1);
+                st_out(outP + PS, p1);
+            }
+            outP += 2 * PS;
+            outW += 2 * PS;
+            __syncwarp();
+            if (threadIdx.x == 0) {
+                mbar_arrive(bars + 8u * (RG::D + cur.slot));
+                mbar_arrive(bars + 8u * (RG::D + nxt.slot));
+            }
+            nxt.template advance<RG::D>();
+            cur = nxt;
+            vol_layer_step<N, TY, RG, F, C + 2>(p, t, ring, bars, ez, zw, outP, outW, cur);
+        } else {
+            const unsigned char* s0 = ring + cur.slot * RG::SLOT;
+            double w0, p0;
+            vol_plane<N, TY, C, F>(p, t, reinterpret_cast<const double*>(s0),
+                                   reinterpret_cast<const double*>(s0 + G::POFF), zw, ez, w0, p0);
+            if (t.valid) {
+                st_out(outW, w0);
+                st_out(outP, p0);
+            }
+            outP += PS;
+            outW += PS;
+            // release the slot: one arrival per consumer warp on its "empty" barrier (no block-wide
+            // barrier: warps drift across planes and hide each other's latency; the producer warp refills)
+            __syncwarp();
+            if (threadIdx.x == 0) mbar_arrive(bars + 8u * (RG::D + cur.slot));
+            cur.template advance<RG::D>();
+            vol_layer_step<N, TY, RG, F, C + 1>(p, t, ring, bars, ez, zw, outP, outW, cur);
+        }
     }
 }
 
@@ -385,11 +498,27 @@ __device__ __forceinline__ void vol_tile(const VolParams& p, unsigned char* ring
     }
 }
 
+// Tile order inside a box: strips of SEM_STRIP tiles along x, rows within a strip, strips in x order.
+// Tiles are handed out in this order, so the x and y neighbours of a tile (which re-read its halo
+// planes) run within a few tile-times of it and find those planes in L2.
+#ifndef SEM_STRIP
+#define SEM_STRIP 1000000
+#endif
+__device__ __forceinline__ void tile_xy(unsigned lt, unsigned ntx, unsigned nty, int& tx, int& ty) {
+    const unsigned W = SEM_STRIP;
+    const unsigned per = W * nty;
+    const unsigned s = lt / per, r = lt - s * per;
+    const unsigned w = (s + 1) * W <= ntx ? W : ntx - s * W;   // last strip may be narrower
+    tx = (int)(s * W + r % w);
+    ty = (int)(r / w);
+}
+
 // Launch-wide ring of a (N0, N1) pair (N1 = 0: one box).
 template <int N0, int N1, int TY>
 struct PairRing {
-    static constexpr int D = cmax(vol_depth(N0), N1 ? vol_depth(N1) : 0);
     static constexpr int SLOT = cmax(vol_slot_bytes(N0, TY), N1 ? vol_slot_bytes(N1, TY) : 0);
+    static constexpr int D = cmax(vol_depth_for_slot(N0, SLOT), N1 ? vol_depth_for_slot(N1, SLOT) : 0);
+    static_assert(D >= 2 * cmax(N0, N1) + 2, "ring too shallow for the z window");
     using RG = Ring<D, SLOT>;
 };
 
@@ -400,7 +529,7 @@ struct PairRing {
 // per-slot header, published by the mbarrier arrive).  The stream never stops at a tile boundary, so
 // the next tile's first planes are already in flight while the consumers finish the current one.
 template <int N0, int N1, int TY>
-__global__ void __launch_bounds__(32 * (TY + 1), SEM_MINB) vol_kernel(const __grid_constant__ VolLaunch L) {
+__global__ void SEM_VOL_BOUNDS(TY) vol_kernel(const __grid_constant__ VolLaunch L) {
     using RG = typename PairRing<N0, N1, TY>::RG;
     constexpr int D = RG::D;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -437,8 +566,10 @@ __global__ void __launch_bounds__(32 * (TY + 1), SEM_MINB) vol_kernel(const __gr
                 const unsigned lt = box ? tile : tile - n1;
                 const VolParams& p = L.box[box];
                 const int NZ = (int)p.NZ;
-                const int tx0 = (int)(lt % L.ntx[box]) * (box ? vol_txe(N1 ? N1 : 1) : vol_txe(N0));
-                const int ty0 = (int)(lt / L.ntx[box]) * TY;
+                int tx, ty;
+                tile_xy(lt, L.ntx[box], L.nty[box], tx, ty);
+                const int tx0 = tx * (box ? vol_txe(N1 ? N1 : 1) : vol_txe(N0));
+                const int ty0 = ty * TY;
                 for (int z = 0; z < NZ; ++z, ++g) {   // plane g reuses the slot of plane g - D
                     const int slot = (int)(g % D);
                     if (g >= (unsigned)D)
@@ -467,13 +598,17 @@ __global__ void __launch_bounds__(32 * (TY + 1), SEM_MINB) vol_kernel(const __gr
             if constexpr (N1 > 0) {
                 const VolParams& p = L.box[1];
                 const unsigned lt = (unsigned)tile;
-                vol_tile<N1, TY, RG>(p, ring, bars, (int)(lt % L.ntx[1]) * vol_txe(N1), (int)(lt / L.ntx[1]) * TY, g);
+                int tx, ty;
+                tile_xy(lt, L.ntx[1], L.nty[1], tx, ty);
+                vol_tile<N1, TY, RG>(p, ring, bars, tx * vol_txe(N1), ty * TY, g);
                 g += (unsigned)p.NZ;
             }
         } else {
             const VolParams& p = L.box[0];
             const unsigned lt = (unsigned)tile - n1;
-            vol_tile<N0, TY, RG>(p, ring, bars, (int)(lt % L.ntx[0]) * vol_txe(N0), (int)(lt / L.ntx[0]) * TY, g);
+            int tx, ty;
+            tile_xy(lt, L.ntx[0], L.nty[0], tx, ty);
+            vol_tile<N0, TY, RG>(p, ring, bars, tx * vol_txe(N0), ty * TY, g);
             g += (unsigned)p.NZ;
         }
     }
@@ -551,7 +686,8 @@ void fill_tiles(VolLaunch& L) {
         const VolParams& p = L.box[b];
         const int txe = vol_txe(p.N);
         L.ntx[b] = (unsigned)((p.NX + txe - 1) / txe);
-        L.ntiles[b] = L.ntx[b] * (unsigned)((p.NY + kTY - 1) / kTY);
+        L.nty[b] = (unsigned)((p.NY + kTY - 1) / kTY);
+        L.ntiles[b] = L.ntx[b] * L.nty[b];
     }
 }
 

@@ -14,7 +14,7 @@ constexpr int kMaxN = 8;          // supported GLL degrees 1..8
 constexpr int kRows = kMaxN + 3;  // row classes per direction: R[0..N-1], L, B0, BN
 constexpr int kMaxModes = 8;
 #ifndef SEM_KPREF
-#define SEM_KPREF 6
+#define SEM_KPREF 12
 #endif
 constexpr int kPref = SEM_KPREF;  // volume kernel: planes prefetched beyond the z-stencil window
 
@@ -27,7 +27,6 @@ __host__ __device__ constexpr int vol_txe(int N) { return (N * (31 / N)) % 2 ? N
 __host__ __device__ constexpr int vol_nh(int N) { return N + (N & 1); }
 __host__ __device__ constexpr int vol_pbox_w(int N) { return vol_txe(N) + 2 * vol_nh(N); }
 __host__ __device__ constexpr int vol_wbox_w(int N) { return vol_txe(N); }
-__host__ __device__ constexpr int vol_depth(int N) { return N + 2 + kPref; }
 // slot = [P tile | pad to 128 B | W tile | pad to 128 B]: TMA destinations must be 128 B aligned
 __host__ __device__ constexpr int vol_pbytes_aligned(int N, int TY) {
     return ((vol_pbox_w(N) * (TY + 2 * N) * 8 + 127) / 128) * 128;
@@ -35,9 +34,13 @@ __host__ __device__ constexpr int vol_pbytes_aligned(int N, int TY) {
 __host__ __device__ constexpr int vol_slot_bytes(int N, int TY) {
     return vol_pbytes_aligned(N, TY) + ((vol_wbox_w(N) * TY * 8 + 127) / 128) * 128;
 }
-__host__ __device__ constexpr int vol_smem_bytes(int N, int TY) {
-    return vol_depth(N) * vol_slot_bytes(N, TY) + 2 * vol_depth(N) * 8 + 128;   // ring + full/empty barriers
+// ring depth: the z window (N + 1 planes) + 1 + kPref planes of prefetch, capped by shared memory
+// (227 KB per CTA; per slot: the tiles, two mbarriers and a tile header)
+constexpr int kSmemMax = 227 * 1024;
+__host__ __device__ constexpr int vol_depth_for_slot(int N, int slot) {
+    return (N + 2 + kPref) * (slot + 20) + 128 <= kSmemMax ? N + 2 + kPref : (kSmemMax - 128) / (slot + 20);
 }
+__host__ __device__ constexpr int vol_depth(int N, int TY) { return vol_depth_for_slot(N, vol_slot_bytes(N, TY)); }
 
 // Row-class indices inside a direction table.
 //   R[a]  interior node with local index a (a = 0: shared, right element), base = i - a
@@ -99,6 +102,7 @@ struct VolLaunch {
     VolParams box[2];
     int nbox;                       // 1 or 2
     unsigned ntx[2];                // tiles along x per box (filled by launch_volume)
+    unsigned nty[2];                // tiles along y per box
     unsigned ntiles[2];             // tiles per box
     unsigned int* sched;            // [0] next tile, [1] finished CTAs; reset by the launch's last CTA
     long long* step;                // device step counter, bumped by the last CTA if bump_step
