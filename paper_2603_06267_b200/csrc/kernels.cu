@@ -831,111 +831,125 @@ void launch_modal(const ModalParams& p, cudaStream_t s) {
 // Interface (SIPG, Eq. 7) on the 2:1 face, fine-face GLL lattice as quadrature (reading R9)
 // ------------------------------------------------------------------------------------------------
 __global__ void iface_coarse_trace(const __grid_constant__ IfaceParams p) {
-    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (id >= p.NXc * p.NYc) return;
-    const long long jx = id % p.NXc, jy = id / p.NXc;
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= (int)(p.NXc * p.NYc)) return;
+    const int NXc = (int)p.NXc;
+    const int jx = id % NXc, jy = id / NXc;
     const long long S = p.PXc * p.NYc;
-    const double* col = p.Pc + jy * p.PXc + jx;
+    const double* col = p.Pc + (long long)jy * p.PXc + jx;
     double d = 0.0;
     for (int c = 0; c <= p.Nc; ++c) d = fma(p.dcB[c], col[c * S], d);
     p.trc[id] = col[0];
     p.drc[id] = d;
 }
 
-__device__ __forceinline__ void coarse_locate(long long i, int NfR, int nelc, int Nc, long long& base, int& q) {
-    long long e = i / NfR;
+// coarse element along one lattice direction of fine node i (the last node belongs to the last element)
+__device__ __forceinline__ void coarse_locate(int i, int NfR, int nelc, int Nc, int& base, int& q) {
+    int e = i / NfR;
     if (e > nelc - 1) e = nelc - 1;
-    q = (int)(i - e * NfR);
+    q = i - e * NfR;
     base = e * Nc;
 }
 
-__global__ void iface_fine(const __grid_constant__ IfaceParams p) {
-    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (id >= p.NXf * p.NYf) return;
-    const long long ix = id % p.NXf, iy = id / p.NXf;
+// Fine side of the SIPG flux at the fine-face GLL lattice (reading R9): jump J = p+ - p-(x_q) and
+// average flux A = 1/2 (c+^2 d_n p+ + c-^2 d_n p-) with p-, d_n p- interpolated from the coarse face
+// lattice (tensor product of the 1D tables I).  Writes tau = gamma J - A and sigma = -1/2 c+^2 J (the
+// fine side's layer terms); the coarse side's weighted terms are derived from them in iface_gather_y.
+template <int NC>
+__global__ void __launch_bounds__(256) iface_fine(const __grid_constant__ IfaceParams p) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    const int NXf = (int)p.NXf;
+    if (id >= NXf * (int)p.NYf) return;
+    const int ix = id % NXf, iy = id / NXf;
     const long long S = p.PXf * p.NYf;
-    const double* top = p.Pf + (p.NZf - 1) * S + iy * p.PXf + ix;
-    const int Nf = p.Nf, Nc = p.Nc, NfR = p.Nf * p.R, Nc1 = Nc + 1;
+    const double* top = p.Pf + (p.NZf - 1) * S + (long long)iy * p.PXf + ix;
+    const int Nf = p.Nf, NfR = p.Nf * p.R;
     // fine trace and normal derivative (n+ = +e_z)
-    const double pp = top[0];
+    const double pp = __ldg(top);
     double dpp = 0.0;
-    for (int c = 0; c <= Nf; ++c) dpp = fma(p.dfT[c], top[-(long long)(Nf - c) * S], dpp);
+    for (int c = 0; c <= Nf; ++c) dpp = fma(p.dfT[c], __ldg(top - (long long)(Nf - c) * S), dpp);
     // coarse trace / derivative interpolated to x_q
-    long long bx, by;
-    int qx, qy;
-    coarse_locate(ix, NfR, p.nelcx, Nc, bx, qx);
-    coarse_locate(iy, NfR, p.nelcy, Nc, by, qy);
+    int bx, by, qx, qy;
+    coarse_locate(ix, NfR, p.nelcx, NC, bx, qx);
+    coarse_locate(iy, NfR, p.nelcy, NC, by, qy);
+    const int NXc = (int)p.NXc;
+    double wx[NC + 1];
+#pragma unroll
+    for (int a = 0; a <= NC; ++a) wx[a] = __ldg(p.I + qx * (NC + 1) + a);
     double pm = 0.0, dpm = 0.0;
-    for (int b = 0; b <= Nc; ++b) {
-        const double wy = p.I[qy * Nc1 + b];
+#pragma unroll
+    for (int b = 0; b <= NC; ++b) {
+        const double wy = __ldg(p.I + qy * (NC + 1) + b);
+        const int row = (by + b) * NXc + bx;
         double rt = 0.0, rd = 0.0;
-        for (int a = 0; a <= Nc; ++a) {
-            const double wx = p.I[qx * Nc1 + a];
-            const long long cid = (by + b) * p.NXc + bx + a;
-            rt = fma(wx, p.trc[cid], rt);
-            rd = fma(wx, p.drc[cid], rd);
+#pragma unroll
+        for (int a = 0; a <= NC; ++a) {
+            rt = fma(wx[a], __ldg(p.trc + row + a), rt);
+            rd = fma(wx[a], __ldg(p.drc + row + a), rd);
         }
         pm = fma(wy, rt, pm);
         dpm = fma(wy, rd, dpm);
     }
     const double J = pp - pm;                              // [[p]].n+
     const double A = 0.5 * (p.cf2 * dpp + p.cc2 * dpm);     // {c^2 grad p}.n+
-    const double Wq = p.mxf[ix] * p.myf[iy];                // assembled fine-face weights
     p.tauf[id] = p.gamma * J - A;
     p.sigf[id] = -0.5 * p.cf2 * J;
-    p.g1[id] = Wq * (A - p.gamma * J);
-    p.g2[id] = Wq * (-0.5 * p.cc2 * J);
 }
 
 // transposed interpolation along one lattice direction: out(j) = sum_i psi_j(x_i) in(i)
-__device__ __forceinline__ void gather_range(long long j, int Nc, int NfR, long long nf, long long& lo, long long& hi) {
-    const long long e = j / Nc;
-    const int b = (int)(j - e * Nc);
+__device__ __forceinline__ void gather_range(int j, int Nc, int NfR, int nf, int& lo, int& hi) {
+    const int e = j / Nc;
+    const int b = j - e * Nc;
     lo = (b == 0 && e > 0) ? (e - 1) * NfR : e * NfR;
     hi = (e + 1) * NfR;
     if (hi > nf - 1) hi = nf - 1;
     if (lo > nf - 1) lo = nf - 1;
 }
 
-__device__ __forceinline__ double gather_weight(const IfaceParams& p, long long i, long long j, int NfR, int nelc) {
-    long long e = i / NfR;
+__device__ __forceinline__ double gather_weight(const IfaceParams& p, int i, int j, int NfR, int nelc) {
+    int e = i / NfR;
     if (e > nelc - 1) e = nelc - 1;
-    const int q = (int)(i - e * NfR);
-    const long long b = j - e * p.Nc;
+    const int q = i - e * NfR;
+    const int b = j - e * p.Nc;
     if (b < 0 || b > p.Nc) return 0.0;
-    return p.I[q * (p.Nc + 1) + b];
+    return __ldg(p.I + q * (p.Nc + 1) + b);
 }
 
-__global__ void iface_gather_y(const __grid_constant__ IfaceParams p) {
-    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (id >= p.NXf * p.NYc) return;
-    const long long ix = id % p.NXf, jy = id / p.NXf;
+// y pass of the coarse-side gather.  The weighted fine terms are g1 = W_q (A - gamma J) = -W_q tau and
+// g2 = W_q (-1/2 c-^2 J) = W_q (c-^2 / c+^2) sigma, W_q = m_x(ix) m_y(iy) the assembled fine-face weights.
+__global__ void __launch_bounds__(256) iface_gather_y(const __grid_constant__ IfaceParams p) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    const int NXf = (int)p.NXf;
+    if (id >= NXf * (int)p.NYc) return;
+    const int ix = id % NXf, jy = id / NXf;
     const int NfR = p.Nf * p.R;
-    long long lo, hi;
-    gather_range(jy, p.Nc, NfR, p.NYf, lo, hi);
+    int lo, hi;
+    gather_range(jy, p.Nc, NfR, (int)p.NYf, lo, hi);
     double s1 = 0.0, s2 = 0.0;
-    for (long long iy = lo; iy <= hi; ++iy) {
-        const double w = gather_weight(p, iy, jy, NfR, p.nelcy);
-        s1 = fma(w, p.g1[iy * p.NXf + ix], s1);
-        s2 = fma(w, p.g2[iy * p.NXf + ix], s2);
+    for (int iy = lo; iy <= hi; ++iy) {
+        const double w = gather_weight(p, iy, jy, NfR, p.nelcy) * __ldg(p.myf + iy);
+        s1 = fma(w, __ldg(p.tauf + iy * NXf + ix), s1);
+        s2 = fma(w, __ldg(p.sigf + iy * NXf + ix), s2);
     }
-    p.h1[id] = s1;
-    p.h2[id] = s2;
+    const double mx = __ldg(p.mxf + ix);
+    p.h1[id] = -mx * s1;
+    p.h2[id] = (p.cc2 / p.cf2) * mx * s2;
 }
 
-__global__ void iface_gather_x(const __grid_constant__ IfaceParams p) {
-    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (id >= p.NXc * p.NYc) return;
-    const long long jx = id % p.NXc, jy = id / p.NXc;
+__global__ void __launch_bounds__(256) iface_gather_x(const __grid_constant__ IfaceParams p) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    const int NXc = (int)p.NXc, NXf = (int)p.NXf;
+    if (id >= NXc * (int)p.NYc) return;
+    const int jx = id % NXc, jy = id / NXc;
     const int NfR = p.Nf * p.R;
-    long long lo, hi;
-    gather_range(jx, p.Nc, NfR, p.NXf, lo, hi);
+    int lo, hi;
+    gather_range(jx, p.Nc, NfR, NXf, lo, hi);
     if (p.skip_ix0 && lo == 0) lo = 1;   // the fine cut line is counted by the left slab only
     double s1 = 0.0, s2 = 0.0;
-    for (long long ix = lo; ix <= hi; ++ix) {
+    for (int ix = lo; ix <= hi; ++ix) {
         const double w = gather_weight(p, ix, jx, NfR, p.nelcx);
-        s1 = fma(w, p.h1[jy * p.NXf + ix], s1);
-        s2 = fma(w, p.h2[jy * p.NXf + ix], s2);
+        s1 = fma(w, __ldg(p.h1 + jy * NXf + ix), s1);
+        s2 = fma(w, __ldg(p.h2 + jy * NXf + ix), s2);
     }
     const double inv = 1.0 / (p.mxc[jx] * p.myc[jy]);
     p.tauc[id] = s1 * inv;
@@ -946,7 +960,18 @@ void launch_iface(const IfaceParams& p, cudaStream_t s) {
     const int T = 256;
     const long long nc = p.NXc * p.NYc, nf = p.NXf * p.NYf, nh = p.NXf * p.NYc;
     iface_coarse_trace<<<(unsigned)((nc + T - 1) / T), T, 0, s>>>(p);
-    iface_fine<<<(unsigned)((nf + T - 1) / T), T, 0, s>>>(p);
+    const unsigned gf = (unsigned)((nf + T - 1) / T);
+    switch (p.Nc) {
+        case 1: iface_fine<1><<<gf, T, 0, s>>>(p); break;
+        case 2: iface_fine<2><<<gf, T, 0, s>>>(p); break;
+        case 3: iface_fine<3><<<gf, T, 0, s>>>(p); break;
+        case 4: iface_fine<4><<<gf, T, 0, s>>>(p); break;
+        case 5: iface_fine<5><<<gf, T, 0, s>>>(p); break;
+        case 6: iface_fine<6><<<gf, T, 0, s>>>(p); break;
+        case 7: iface_fine<7><<<gf, T, 0, s>>>(p); break;
+        case 8: iface_fine<8><<<gf, T, 0, s>>>(p); break;
+        default: break;
+    }
     iface_gather_y<<<(unsigned)((nh + T - 1) / T), T, 0, s>>>(p);
     iface_gather_x<<<(unsigned)((nc + T - 1) / T), T, 0, s>>>(p);
 }

@@ -468,9 +468,9 @@ sem::CutParams cut_params(sem_ctx* ctx, sem::Part& pt, int side, int bi, int cur
 int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
     cudaStream_t s = ctx->stream;
     int nl = 0;
-    auto mark = [&](int which, bool begin) {
+    auto mark = [&](int which, bool begin, cudaStream_t on) {
         if (!prof) return;
-        static thread_local cudaEvent_t pend = nullptr;
+        static thread_local cudaEvent_t pend[3] = {nullptr, nullptr, nullptr};
         cudaEvent_t e;
         if (ctx->ev_pool.empty()) {
             cudaEventCreate(&e);
@@ -478,19 +478,32 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
             e = ctx->ev_pool.back();
             ctx->ev_pool.pop_back();
         }
-        cudaEventRecord(e, s);
-        if (begin) pend = e;
-        else ctx->ev_pending.push_back({which, {pend, e}});
+        cudaEventRecord(e, on);
+        if (begin) pend[which] = e;
+        else ctx->ev_pending.push_back({which, {pend[which], e}});
     };
-    mark(2, true);
+    // modal ROM (a2-a4) and SIPG interface (a8) only read p^{n+1}: with both present the modal kernel
+    // runs on the auxiliary stream, concurrently with the interface kernels (fork/join by events, also
+    // inside the captured graph)
+    bool any_pm = false;
+    for (auto& pt : ctx->parts) any_pm = any_pm || pt.pm.on;
+    const bool fork = any_pm && ctx->itf_on;
+    cudaStream_t ms = s;
+    if (fork) {
+        cudaEventRecord(ctx->ev_mfork, s);
+        cudaStreamWaitEvent(ctx->aux, ctx->ev_mfork, 0);
+        ms = ctx->aux;
+    }
+    mark(2, true, ms);
     for (auto& pt : ctx->parts)
         if (pt.pm.on) {
-            sem::launch_modal(modal_params(ctx, pt, cur), s);
+            sem::launch_modal(modal_params(ctx, pt, cur), ms);
             ++nl;
         }
-    mark(2, false);
+    mark(2, false, ms);
+    if (fork) cudaEventRecord(ctx->ev_mjoin, ctx->aux);
     if (ctx->itf_on) {
-        mark(1, true);
+        mark(1, true, s);
         for (auto& pt : ctx->parts) {
             sem::IfaceParams ip = pt.itf.prm;
             ip.Pf = pt.boxes[pt.itf.fine].P[cur];
@@ -498,8 +511,9 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
             sem::launch_iface(ip, s);
             nl += 4;
         }
-        mark(1, false);
+        mark(1, false, s);
     }
+    if (fork) cudaStreamWaitEvent(s, ctx->ev_mjoin, 0);
     const bool slabs = ctx->world > 1;
     if (slabs) {
         for (auto& pt : ctx->parts)
@@ -534,7 +548,7 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
             cudaEventRecord(ctx->ev_join, ctx->comm);
         }
     }
-    mark(0, true);
+    mark(0, true, s);
     {
         // persistent volume launches: both boxes of a slab in one launch when the degree pair is
         // instantiated (5/3 of configs 2-4), else one launch per box; each has its own scheduler pair
@@ -564,7 +578,7 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
             ++nl;
         }
     }
-    mark(0, false);
+    mark(0, false, s);
     if (slabs) {
         if (!ctx->emulate) cudaStreamWaitEvent(s, ctx->ev_join, 0);
         for (auto& pt : ctx->parts)
@@ -746,7 +760,10 @@ sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
     if (dalloc(ctx, &ctx->d_step, 1) || dalloc(ctx, &ctx->d_sched, 2 * sem_ctx::kSchedPairs) || dalloc(ctx, &ctx->d_flag, 1))
         return bail(SEM_E_OOM);
     if (cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_mfork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_mjoin, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess)
         return bail(SEM_E_CUDA);
     if (nccl_mode(ctx)) {
         NcclApi& api = nccl_api();
@@ -968,7 +985,7 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
         p.myc = C.my;
         const size_t nf = (size_t)F.NX * F.NY, nc = (size_t)C.NX * C.NY, nh = (size_t)F.NX * C.NY;
         if (dalloc(ctx, &p.trc, nc) || dalloc(ctx, &p.drc, nc) || dalloc(ctx, &p.tauf, nf) ||
-            dalloc(ctx, &p.sigf, nf) || dalloc(ctx, &p.g1, nf) || dalloc(ctx, &p.g2, nf) || dalloc(ctx, &p.h1, nh) ||
+            dalloc(ctx, &p.sigf, nf) || dalloc(ctx, &p.h1, nh) ||
             dalloc(ctx, &p.h2, nh) || dalloc(ctx, &p.tauc, nc) || dalloc(ctx, &p.sigc, nc))
             return SEM_E_OOM;
         // layer coefficients: a -= tau ktau[c] + sigma ksig[c]
@@ -1330,6 +1347,9 @@ void sem_destroy(sem_ctx* ctx) {
     }
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_mfork) cudaEventDestroy(ctx->ev_mfork);
+    if (ctx->ev_mjoin) cudaEventDestroy(ctx->ev_mjoin);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->comm) cudaStreamDestroy(ctx->comm);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);

@@ -152,7 +152,6 @@ struct IfaceParams {
     const double* __restrict__ myc;
     double* trc; double* drc;       // coarse trace / normal derivative [NXc*NYc]
     double* tauf; double* sigf;     // fine outputs [NXf*NYf]
-    double* g1; double* g2;         // fine weighted terms for the coarse gather
     double* h1; double* h2;         // [NYc][NXf] after the y gather
     double* tauc; double* sigc;     // coarse outputs [NXc*NYc]
     int skip_ix0;                   // slab with a left cut: the shared fine cut line belongs to the left slab
@@ -275,6 +274,8 @@ struct sem_ctx {
     double kt_ms[3] = {0, 0, 0};
     long long kt_n[3] = {0, 0, 0};
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_mfork = nullptr, ev_mjoin = nullptr;   // modal kernel on `aux`, beside the interface
+    cudaStream_t aux = nullptr;
     void* nccl = nullptr;        // ncclComm_t
     std::string err;
     std::vector<void*> allocs;
