@@ -843,49 +843,47 @@ __global__ void iface_coarse_trace(const __grid_constant__ IfaceParams p) {
     p.drc[id] = d;
 }
 
-// coarse element along one lattice direction of fine node i (the last node belongs to the last element)
-__device__ __forceinline__ void coarse_locate(int i, int NfR, int nelc, int Nc, int& base, int& q) {
-    int e = i / NfR;
-    if (e > nelc - 1) e = nelc - 1;
-    q = i - e * NfR;
-    base = e * Nc;
-}
 
 // Fine side of the SIPG flux at the fine-face GLL lattice (reading R9): jump J = p+ - p-(x_q) and
 // average flux A = 1/2 (c+^2 d_n p+ + c-^2 d_n p-) with p-, d_n p- interpolated from the coarse face
 // lattice (tensor product of the 1D tables I).  Writes tau = gamma J - A and sigma = -1/2 c+^2 J (the
 // fine side's layer terms); the coarse side's weighted terms are derived from them in iface_gather_y.
-template <int NC>
+// Template arguments NF, NC, R fix the degrees and the ratio at compile time (0: read from p).
+template <int NF, int NC, int R>
 __global__ void __launch_bounds__(256) iface_fine(const __grid_constant__ IfaceParams p) {
+    const int Nf = NF ? NF : p.Nf, Nc = NC ? NC : p.Nc, NfR = Nf * (R ? R : p.R);
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
     const int NXf = (int)p.NXf;
     if (id >= NXf * (int)p.NYf) return;
     const int ix = id % NXf, iy = id / NXf;
     const long long S = p.PXf * p.NYf;
     const double* top = p.Pf + (p.NZf - 1) * S + (long long)iy * p.PXf + ix;
-    const int Nf = p.Nf, NfR = p.Nf * p.R;
-    // fine trace and normal derivative (n+ = +e_z)
+    // coarse element and local fine index along x and y
+    int ex = ix / NfR, ey = iy / NfR;
+    if (ex > p.nelcx - 1) ex = p.nelcx - 1;
+    if (ey > p.nelcy - 1) ey = p.nelcy - 1;
+    const int qx = ix - ex * NfR, qy = iy - ey * NfR;
+    const int NXc = (int)p.NXc;
+    const int c0 = ey * Nc * NXc + ex * Nc;
+    // fine trace and normal derivative (n+ = +e_z): the top element layer of the fine box
     const double pp = __ldg(top);
     double dpp = 0.0;
-    for (int c = 0; c <= Nf; ++c) dpp = fma(p.dfT[c], __ldg(top - (long long)(Nf - c) * S), dpp);
-    // coarse trace / derivative interpolated to x_q
-    int bx, by, qx, qy;
-    coarse_locate(ix, NfR, p.nelcx, NC, bx, qx);
-    coarse_locate(iy, NfR, p.nelcy, NC, by, qy);
-    const int NXc = (int)p.NXc;
-    double wx[NC + 1];
 #pragma unroll
-    for (int a = 0; a <= NC; ++a) wx[a] = __ldg(p.I + qx * (NC + 1) + a);
+    for (int c = 0; c <= (NF ? NF : kMaxN); ++c)
+        if (NF || c <= Nf) dpp = fma(p.dfT[c], __ldg(top - (long long)(Nf - c) * S), dpp);
     double pm = 0.0, dpm = 0.0;
 #pragma unroll
-    for (int b = 0; b <= NC; ++b) {
-        const double wy = __ldg(p.I + qy * (NC + 1) + b);
-        const int row = (by + b) * NXc + bx;
+    for (int b = 0; b <= (NC ? NC : kMaxN); ++b) {
+        if (!NC && b > Nc) break;
+        const double wy = __ldg(p.I + qy * (Nc + 1) + b);
+        const int row = c0 + b * NXc;
         double rt = 0.0, rd = 0.0;
 #pragma unroll
-        for (int a = 0; a <= NC; ++a) {
-            rt = fma(wx[a], __ldg(p.trc + row + a), rt);
-            rd = fma(wx[a], __ldg(p.drc + row + a), rd);
+        for (int a = 0; a <= (NC ? NC : kMaxN); ++a) {
+            if (!NC && a > Nc) break;
+            const double wx = __ldg(p.I + qx * (Nc + 1) + a);
+            rt = fma(wx, __ldg(p.trc + row + a), rt);
+            rd = fma(wx, __ldg(p.drc + row + a), rd);
         }
         pm = fma(wy, rt, pm);
         dpm = fma(wy, rd, dpm);
@@ -896,84 +894,88 @@ __global__ void __launch_bounds__(256) iface_fine(const __grid_constant__ IfaceP
     p.sigf[id] = -0.5 * p.cf2 * J;
 }
 
-// transposed interpolation along one lattice direction: out(j) = sum_i psi_j(x_i) in(i)
-__device__ __forceinline__ void gather_range(int j, int Nc, int NfR, int nf, int& lo, int& hi) {
-    const int e = j / Nc;
-    const int b = j - e * Nc;
-    lo = (b == 0 && e > 0) ? (e - 1) * NfR : e * NfR;
-    hi = (e + 1) * NfR;
-    if (hi > nf - 1) hi = nf - 1;
-    if (lo > nf - 1) lo = nf - 1;
-}
-
-__device__ __forceinline__ double gather_weight(const IfaceParams& p, int i, int j, int NfR, int nelc) {
-    int e = i / NfR;
-    if (e > nelc - 1) e = nelc - 1;
-    const int q = i - e * NfR;
-    const int b = j - e * p.Nc;
-    if (b < 0 || b > p.Nc) return 0.0;
-    return __ldg(p.I + q * (p.Nc + 1) + b);
+// Transposed interpolation along one lattice direction: out(j) = sum_i psi_j(x_i) in(i), where fine
+// lattice index i lies in coarse element e = min(i / NfR, nelc - 1) at local index q = i - e NfR and
+// psi_j(x_i) = I[q][j - e Nc] if 0 <= j - e Nc <= Nc.  Coarse node j = e Nc + b touches the fine
+// nodes of element e (and of e - 1 if b = 0): at most 2 NfR + 1 of them, from lo = (e or e-1) NfR.
+template <int NF, int NC, int R>
+__device__ __forceinline__ void gather_1d(const IfaceParams& p, int j, int nelc, int nf, const double* __restrict__ in1,
+                                          const double* __restrict__ in2, int stride, const double* __restrict__ wi,
+                                          int skip0, double& s1, double& s2) {
+    const int Nc = NC ? NC : p.Nc, NfR = (NF ? NF : p.Nf) * (R ? R : p.R);
+    int e = j / Nc;
+    int b = j - e * Nc;
+    if (e > nelc - 1) {   // last coarse node: b = Nc of the last element
+        e = nelc - 1;
+        b = Nc;
+    }
+    s1 = 0.0;
+    s2 = 0.0;
+    // own element e: fine nodes e NfR + q, q = 0..NfR (q = NfR only for the last element)
+    const int qend = (e == nelc - 1) ? NfR : NfR - 1;
+#pragma unroll 4
+    for (int q = 0; q <= qend; ++q) {
+        const int i = e * NfR + q;
+        if (skip0 && i == 0) continue;
+        double w = __ldg(p.I + q * (Nc + 1) + b);
+        if (wi) w *= __ldg(wi + i);
+        s1 = fma(w, __ldg(in1 + i * stride), s1);
+        s2 = fma(w, __ldg(in2 + i * stride), s2);
+    }
+    if (b == 0 && e > 0) {   // left element e - 1 (its q = 0 node has weight I[0][Nc] = 0; q = NfR is in e)
+#pragma unroll 4
+        for (int q = 1; q < NfR; ++q) {
+            const int i = (e - 1) * NfR + q;
+            double w = __ldg(p.I + q * (Nc + 1) + Nc);
+            if (wi) w *= __ldg(wi + i);
+            s1 = fma(w, __ldg(in1 + i * stride), s1);
+            s2 = fma(w, __ldg(in2 + i * stride), s2);
+        }
+    }
 }
 
 // y pass of the coarse-side gather.  The weighted fine terms are g1 = W_q (A - gamma J) = -W_q tau and
 // g2 = W_q (-1/2 c-^2 J) = W_q (c-^2 / c+^2) sigma, W_q = m_x(ix) m_y(iy) the assembled fine-face weights.
+template <int NF, int NC, int R>
 __global__ void __launch_bounds__(256) iface_gather_y(const __grid_constant__ IfaceParams p) {
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
     const int NXf = (int)p.NXf;
     if (id >= NXf * (int)p.NYc) return;
     const int ix = id % NXf, jy = id / NXf;
-    const int NfR = p.Nf * p.R;
-    int lo, hi;
-    gather_range(jy, p.Nc, NfR, (int)p.NYf, lo, hi);
-    double s1 = 0.0, s2 = 0.0;
-    for (int iy = lo; iy <= hi; ++iy) {
-        const double w = gather_weight(p, iy, jy, NfR, p.nelcy) * __ldg(p.myf + iy);
-        s1 = fma(w, __ldg(p.tauf + iy * NXf + ix), s1);
-        s2 = fma(w, __ldg(p.sigf + iy * NXf + ix), s2);
-    }
+    double s1, s2;
+    gather_1d<NF, NC, R>(p, jy, p.nelcy, (int)p.NYf, p.tauf + ix, p.sigf + ix, NXf, p.myf, 0, s1, s2);
     const double mx = __ldg(p.mxf + ix);
     p.h1[id] = -mx * s1;
     p.h2[id] = (p.cc2 / p.cf2) * mx * s2;
 }
 
+template <int NF, int NC, int R>
 __global__ void __launch_bounds__(256) iface_gather_x(const __grid_constant__ IfaceParams p) {
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
     const int NXc = (int)p.NXc, NXf = (int)p.NXf;
     if (id >= NXc * (int)p.NYc) return;
     const int jx = id % NXc, jy = id / NXc;
-    const int NfR = p.Nf * p.R;
-    int lo, hi;
-    gather_range(jx, p.Nc, NfR, NXf, lo, hi);
-    if (p.skip_ix0 && lo == 0) lo = 1;   // the fine cut line is counted by the left slab only
-    double s1 = 0.0, s2 = 0.0;
-    for (int ix = lo; ix <= hi; ++ix) {
-        const double w = gather_weight(p, ix, jx, NfR, p.nelcx);
-        s1 = fma(w, __ldg(p.h1 + jy * NXf + ix), s1);
-        s2 = fma(w, __ldg(p.h2 + jy * NXf + ix), s2);
-    }
+    double s1, s2;
+    // the fine cut line ix = 0 of a slab with a left cut is counted by the left slab only
+    gather_1d<NF, NC, R>(p, jx, p.nelcx, NXf, p.h1 + jy * NXf, p.h2 + jy * NXf, 1, nullptr, p.skip_ix0, s1, s2);
     const double inv = 1.0 / (p.mxc[jx] * p.myc[jy]);
     p.tauc[id] = s1 * inv;
     p.sigc[id] = s2 * inv;
 }
 
-void launch_iface(const IfaceParams& p, cudaStream_t s) {
+template <int NF, int NC, int R>
+static void launch_iface_t(const IfaceParams& p, cudaStream_t s) {
     const int T = 256;
     const long long nc = p.NXc * p.NYc, nf = p.NXf * p.NYf, nh = p.NXf * p.NYc;
     iface_coarse_trace<<<(unsigned)((nc + T - 1) / T), T, 0, s>>>(p);
-    const unsigned gf = (unsigned)((nf + T - 1) / T);
-    switch (p.Nc) {
-        case 1: iface_fine<1><<<gf, T, 0, s>>>(p); break;
-        case 2: iface_fine<2><<<gf, T, 0, s>>>(p); break;
-        case 3: iface_fine<3><<<gf, T, 0, s>>>(p); break;
-        case 4: iface_fine<4><<<gf, T, 0, s>>>(p); break;
-        case 5: iface_fine<5><<<gf, T, 0, s>>>(p); break;
-        case 6: iface_fine<6><<<gf, T, 0, s>>>(p); break;
-        case 7: iface_fine<7><<<gf, T, 0, s>>>(p); break;
-        case 8: iface_fine<8><<<gf, T, 0, s>>>(p); break;
-        default: break;
-    }
-    iface_gather_y<<<(unsigned)((nh + T - 1) / T), T, 0, s>>>(p);
-    iface_gather_x<<<(unsigned)((nc + T - 1) / T), T, 0, s>>>(p);
+    iface_fine<NF, NC, R><<<(unsigned)((nf + T - 1) / T), T, 0, s>>>(p);
+    iface_gather_y<NF, NC, R><<<(unsigned)((nh + T - 1) / T), T, 0, s>>>(p);
+    iface_gather_x<NF, NC, R><<<(unsigned)((nc + T - 1) / T), T, 0, s>>>(p);
+}
+
+void launch_iface(const IfaceParams& p, cudaStream_t s) {
+    if (p.Nf == 5 && p.Nc == 3 && p.R == 2) launch_iface_t<5, 3, 2>(p, s);   // configs 2-4
+    else launch_iface_t<0, 0, 0>(p, s);
 }
 
 // ------------------------------------------------------------------------------------------------
