@@ -109,7 +109,7 @@ def cpu_baseline(steps, warmup=1, patch=4):
     nm.run(steps)
     dt = time.perf_counter() - t0
     val = sys_.ndof * steps / dt / 1e9
-    return {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "ms_per_step": dt / steps * 1e3,
             "sample": f"config-3 crop: {patch}x{patch} PMUTs ({rec['boxes'][0]['nel']} fine + "
                       f"{rec['boxes'][1]['nel']} coarse elements, {sys_.ndof} DOF), {steps} timed steps "
                       f"after {warmup} warm-up, {dt:.1f} s"}
@@ -120,7 +120,7 @@ def run_reference(args, rank, world):
         return
     cb = cpu_baseline(args.steps, args.warmup, patch=args.ref_patch)
     out = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
            "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"cfg{args.config} (bounded crop, oracle on host cores)"},
            "cpu_baseline": cb,

@@ -498,19 +498,21 @@ __device__ __forceinline__ void vol_tile(const VolParams& p, unsigned char* ring
     }
 }
 
-// Tile order inside a box: strips of SEM_STRIP tiles along x, rows within a strip, strips in x order.
-// Tiles are handed out in this order, so the x and y neighbours of a tile (which re-read its halo
-// planes) run within a few tile-times of it and find those planes in L2.
-#ifndef SEM_STRIP
-#define SEM_STRIP 1000000
+// Tile order inside a box: bands of SEM_BAND tile rows, column-major inside a band (tx slow, ty fast),
+// bands in y order.  Tiles are handed out in this order, so both the x and the y neighbours of a tile
+// (which re-read its halo rows of p) run within a few tile-times of it and find them in L2, while the
+// concurrently streamed region still spans long contiguous x rows (DRAM page locality).  SEM_BAND = 1
+// is plain row-major order.
+#ifndef SEM_BAND
+#define SEM_BAND 1
 #endif
 __device__ __forceinline__ void tile_xy(unsigned lt, unsigned ntx, unsigned nty, int& tx, int& ty) {
-    const unsigned W = SEM_STRIP;
-    const unsigned per = W * nty;
+    const unsigned B = SEM_BAND;
+    const unsigned per = B * ntx;
     const unsigned s = lt / per, r = lt - s * per;
-    const unsigned w = (s + 1) * W <= ntx ? W : ntx - s * W;   // last strip may be narrower
-    tx = (int)(s * W + r % w);
-    ty = (int)(r / w);
+    const unsigned h = (s + 1) * B <= nty ? B : nty - s * B;   // last band may be shorter
+    tx = (int)(r / h);
+    ty = (int)(s * B + r % h);
 }
 
 // Launch-wide ring of a (N0, N1) pair (N1 = 0: one box).
