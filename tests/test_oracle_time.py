@@ -204,6 +204,41 @@ def test_unloaded_pmut_hann_duhamel(zeta):
     assert lo < errs[0] / errs[1] < 5.5
 
 
+def test_rx_feedback_coupled_modes_closed_form():
+    """Open-circuit RX feedback (Eq. 3 second line): with kappa = 0, zeta = 0 and
+    phi = (1/C) sum_n eta q_n, the modes obey q'' = -A q with A = diag(w^2) - (eta^2/(M_m C)) 1 1^T,
+    so q(t) = V cos(sqrt(Lambda) t) V^-1 q0 (q'(0) = 0).  C is chosen so the feedback is ~30% of
+    w_1^2 (the config's C = 1e-10 F would shift w^2 by 3e-7 only); the scheme is second order."""
+    errs = []
+    for scale in (0.25, 0.125):
+        rec = _oscillator_record(scale)
+        pm = rec["pmut"]
+        pm["damping"] = np.zeros(3)
+        pm["rx"], pm["t_switch"] = True, 0.0
+        w = 2 * math.pi * pm["freq_hz"][0]
+        Mm, eta = pm["modal_mass"][0], pm["eta"][0]
+        pm["capacitance"] = eta * eta / (Mm * 0.3 * w[0] ** 2)
+        A = np.diag(w ** 2) - (eta * eta / (Mm * pm["capacitance"])) * np.ones((3, 3))
+        lam, V = np.linalg.eigh(A)
+        assert np.all(lam > 0)
+        q0 = np.array([1e-9, 0.5e-9, -0.3e-9])
+        nm = Newmark(System(rec))
+        nm.q[0] = q0
+        nm.qdd[0] = -A @ q0                  # consistent initial acceleration (reading R20)
+        err = 0.0
+        for _ in range(int(round(1e-6 / rec["dt"]))):
+            nm.step()
+            t = nm.n * rec["dt"]
+            ref = V @ (np.cos(np.sqrt(lam) * t) * (V.T @ q0))
+            err = max(err, np.max(np.abs(nm.q[0] - ref)) / 1e-9)
+        assert np.all(nm.p == 0)
+        # the received voltage is the feedback itself
+        assert abs(nm.v_rx()[0] - eta * nm.q[0].sum() / pm["capacitance"]) <= 1e-12 * abs(nm.v_rx()[0]) + 1e-30
+        errs.append(err)
+    assert errs[0] < 2e-2
+    assert 3.5 < errs[0] / errs[1] < 4.5                     # second order
+
+
 def test_drive_window():
     pm = config(1)["pmut"]
     tau = pm["delay_s"]

@@ -59,6 +59,24 @@ def test_random_state_operator_parity(name):
         sim.close()
 
 
+def test_tx_then_rx_switch():
+    """TX burst until t_bar, open-circuit RX feedback after it (Eq. 3):
+    cfg 0 with t_bar mid-run and a capacitance small enough for the feedback to matter."""
+    rec = config(0)
+    pm = rec["pmut"]
+    pm["rx"] = True
+    pm["amp_v"] = 5.0
+    pm["t_switch"] = 250.5 * rec["dt"]
+    w1 = 2 * np.pi * pm["freq_hz"][0, 0]
+    pm["capacitance"] = pm["eta"][0] ** 2 / (pm["modal_mass"][0] * 0.2 * w1 * w1)
+    nm = oracle_run(rec, 400)
+    sim = gpu_run(rec, 400)
+    r = compare(sim, nm)
+    assert np.abs(nm.q).max() > 1e-12
+    for k, v in r.items():
+        assert v < TOL, (k, v, r)
+
+
 def test_literal_coupling_flag():
     rec = config(0, coupling="literal")
     nm = oracle_run(rec, 300)
