@@ -19,8 +19,9 @@ What it computes, in the paper's order and notation (PAPER.md = P:L<line>):
 * ``newmark``    Algorithm 1 literally: three vectors per field,
                  predictor / solve / corrector, with the coupling-time-level flag
                  of DESIGN.md reading R2.
-* ``pointwise``  the same operators evaluated node-by-node, for sampled parity
-                 checks at full BASELINE sizes.
+* ``pml``        the perfectly matched layer of Eq. (1):
+                 damping profile, coefficients, element-local Phi, weak divergence,
+                 and the auxiliary update of readings R23-R25.
 
 Every function is pinned by ``tests/test_oracle_*.py`` against closed forms,
 invariants or brute force.  Functions marked

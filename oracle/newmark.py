@@ -58,6 +58,11 @@ class Newmark:
         self.pd = np.zeros(n)
         self.pdd = np.zeros(n)
         self.n = 0
+        # PML auxiliaries (Eq. 1 lines 2-3; readings R23-R25 in oracle/pml.py)
+        self.pml = None
+        if rec.get("pml") is not None:
+            from .pml import Pml
+            self.pml = Pml(system, rec["pml"])
         pm = system.pm
         if pm is not None:
             shape = pm["freq_hz"].shape
@@ -100,7 +105,13 @@ class Newmark:
             qd1 = qd1 + 0.5 * dt * qdd1
             f += s.pmut_force(qdd1)
         f += s.plane_wave_load(tn1)
-        pdd1 = (f - s.apply_K(p1) - s.C * pd1) / s.M
+        if self.pml is None:
+            pdd1 = (f - s.apply_K(p1) - s.C * pd1) / s.M
+        else:   # R25: PML terms at the predictor velocity, psi^{n+1} and Phi^{n+1}
+            rB, psi1 = self.pml.advance(p1, dt)
+            pm_ = self.pml
+            pdd1 = ((f - s.apply_K(p1) - s.C * pd1 - rB) / s.M
+                    - pm_.alpha * pd1 - pm_.beta * p1 - pm_.gamma * psi1)
         pd1 = pd1 + 0.5 * dt * pdd1
         self.p, self.pd, self.pdd = p1, pd1, pdd1
         if have_pmut:

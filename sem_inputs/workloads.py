@@ -242,6 +242,24 @@ def cavity_config(nel=(3, 3, 3), degree=4, extent=(1e-3, 1e-3, 1e-3), c=C_WATER,
     return _finish(rec)
 
 
+PML_R = 1e-4           # reflection coefficient of the PML profile (R in [1e-5, 1e-4])
+
+
+def pml_config(nel=(4, 4, 6), degree=4, extent=(0.4e-3, 0.4e-3, 0.6e-3), layers=(0, 0, 0, 0, 0, 1),
+               layer_el=2, R=PML_R, abc_on_pml=True, c=C_WATER, n_steps=100, cfl=0.3):
+    """One box with PML layers (oracle/pml.py readings R23-R25): ``layers`` flags
+    the faces (-x,+x,-y,+y,-z,+z) that carry a layer ``layer_el`` elements thick; those faces are
+    absorbing (the paper's Gamma_ABC behind the PML) if ``abc_on_pml``, the others rigid."""
+    h = [e / n for e, n in zip(extent, nel)]
+    thick = [float(layers[f]) * layer_el * h[f // 2] for f in range(6)]
+    bc = [BC_ABSORBING if (layers[f] and abc_on_pml) else BC_RIGID for f in range(6)]
+    boxes = [_box((0, 0, 0), extent, nel, degree, bc, c=c)]
+    rec = {"name": "pml", "boxes": boxes, "n_steps": n_steps, "seed": 0,
+           "pml": {"box": 0, "thickness": thick, "R": float(R)}}
+    rec["dt"] = cfl_dt(boxes, cfl)
+    return _finish(rec)
+
+
 def conforming_cut_config(nel_xy=3, nz_lo=2, nz_hi=2, degree=4, h=1e-4 / 3, alpha=PENALTY_ALPHA,
                           n_steps=100, cfl=0.3, ratio=1, degree_hi=None, bc_top=BC_RIGID):
     """Two boxes stacked in z with a DG interface between them.  ratio=1 and degree_hi=None gives
