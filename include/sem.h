@@ -145,6 +145,18 @@ sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, cons
 sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, double penalty_alpha,
                                   int quad_rule);
 
+/* Perfectly matched layer (Eq. 1 lines 1-3; coefficients P:L271-277; profile P:L280-289)
+ * inside box `box`: thickness[f] [m] for faces f = -x,+x,-y,+y,-z,+z (0 = no layer) is the slab of the
+ * box next to face f; z_d(d) = zt (d/l - sin(2 pi d/l)/(2 pi)), d = depth into the layer,
+ * zt = (c/l) log(1/R), 0 < R < 1 (the paper uses R in [1e-5, 1e-4]).  The faces keep their own
+ * boundary condition (the paper's Gamma_ABC behind the layer: tag them SEM_BC_ABSORBING).
+ * Discretisation (readings R23-R25): psi continuous nodal, Phi element-local, div Phi in weak
+ * form, psi/Phi at half steps (Crank-Nicolson on Z1), PML terms at the predictor velocity.
+ * Caller owns `thickness` (copied).  Single slab only (world 1, no emulation): SEM_E_PARTITION
+ * otherwise.  Errors: SEM_E_ARG (negative thickness, overlapping layers, R outside (0, 1)),
+ * SEM_E_STATE (already attached), SEM_E_OOM.  Resets the dynamic state like sem_pmut_attach. */
+sem_status sem_pml_attach(sem_ctx* ctx, int box, const double* thickness, double R);
+
 /* Incident plane wave entering through absorbing face `face` (only 5 = +z) of `box`
  * (reading R13): p_inc = amp s(t - k.(x - x_ref)/c), s(u) = exp(-(u-t0)^2/(2 sigma^2))
  * sin(2 pi f0 (u-t0)), imposed as total-field first-order ABC data
@@ -186,7 +198,8 @@ sem_status sem_fill_random_state(sem_ctx* ctx, int box, unsigned long long seed,
 sem_status sem_query(sem_ctx* ctx, long long* n_dof, long long* step, double* t);
 
 /* Per-kernel device time [ms] accumulated since the last reset while SEM_F_NO_GRAPH profiling
- * is enabled (sem_set_profiling).  which: 0 = volume (all boxes), 1 = interface, 2 = modal.
+ * is enabled (sem_set_profiling).  which: 0 = volume (all boxes), 1 = interface, 2 = modal,
+ * 3 = PML element kernel.
  * n_launches receives the number of launches timed. */
 sem_status sem_set_profiling(sem_ctx* ctx, int on);
 sem_status sem_kernel_time(sem_ctx* ctx, int which, double* ms, long long* n_launches);

@@ -1065,6 +1065,119 @@ void launch_cut_fixup(const CutParams& c, cudaStream_t s) {
     cut_fixup_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c);
 }
 
+// ------------------------------------------------------------------------------------------------
+// PML (Eq. 1; readings R23-R25): one block per PML element, one thread per
+// element GLL node.  psi^{n+3/2} = psi^{n+1/2} + dt p^{n+1}; element-local grad p^{n+1}, grad psi^{n+1};
+// Crank-Nicolson update of Phi; weak divergence sum_q w_q |J| Phi^{n+1}(q) . grad phi_i(x_q) and the
+// nodal terms alpha pdot + beta p + gamma psi accumulate (atomics) into the PML acceleration da.
+// ------------------------------------------------------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) pml_element_kernel(const __grid_constant__ PmlParams p) {
+    constexpr int n1 = N + 1, nl = n1 * n1 * n1;
+    __shared__ double sp[nl], ss[nl], sf[3][nl];
+    const int t = threadIdx.x;
+    const int a = t % n1, b = (t / n1) % n1, c = t / (n1 * n1);
+    const int k = blockIdx.x;
+    const int ex = p.elems[3 * k], ey = p.elems[3 * k + 1], ez = p.elems[3 * k + 2];
+    const int gx = N * ex + a, gy = N * ey + b, gz = N * ez + c;
+    const long long g = ((long long)gz * p.NY + gy) * p.PX + gx;
+    const double pv = p.P[g];
+    const double so = p.psi_old[g];
+    const double sn = fma(p.dt, pv, so);
+    p.psi_new[g] = sn;   // a node shared by several PML elements gets the same value from each
+    const double sm = 0.5 * (so + sn);
+    sp[t] = pv;
+    ss[t] = sm;
+    __syncthreads();
+    // element-local gradients at the own node (reference derivative rows, scaled by 2/h)
+    double gp[3] = {0.0, 0.0, 0.0}, gs[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j <= N; ++j) {
+        const int ix = j + n1 * (b + n1 * c), iy = a + n1 * (j + n1 * c), iz = a + n1 * (b + n1 * j);
+        gp[0] = fma(p.D[a][j], sp[ix], gp[0]);
+        gs[0] = fma(p.D[a][j], ss[ix], gs[0]);
+        gp[1] = fma(p.D[b][j], sp[iy], gp[1]);
+        gs[1] = fma(p.D[b][j], ss[iy], gs[1]);
+        gp[2] = fma(p.D[c][j], sp[iz], gp[2]);
+        gs[2] = fma(p.D[c][j], ss[iz], gs[2]);
+    }
+    const double z[3] = {p.zx[gx], p.zy[gy], p.zz[gz]};
+    const double alpha = z[0] + z[1] + z[2];
+    const double beta = z[0] * z[1] + z[1] * z[2] + z[2] * z[0];
+    const double gamma = z[0] * z[1] * z[2];
+    const double Z3[3] = {z[1] * z[2], z[2] * z[0], z[0] * z[1]};
+    double* ph = p.phi + (size_t)k * 3 * nl;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const double sc = 2.0 / p.h[d];
+        const double old = ph[d * nl + t];
+        const double rhs = p.c2 * ((alpha - 2.0 * z[d]) * sc * gp[d] + Z3[d] * sc * gs[d]);
+        const double nw = (fma(-0.5 * p.dt, z[d], 1.0) * old + p.dt * rhs) / fma(0.5 * p.dt, z[d], 1.0);
+        ph[d * nl + t] = nw;
+        sf[d][t] = 0.5 * (old + nw);
+    }
+    __syncthreads();
+    // weak divergence at the own node
+    double rx = 0.0, ry = 0.0, rz = 0.0;
+#pragma unroll
+    for (int j = 0; j <= N; ++j) {
+        rx = fma(p.w[j] * p.D[j][a], sf[0][j + n1 * (b + n1 * c)], rx);
+        ry = fma(p.w[j] * p.D[j][b], sf[1][a + n1 * (j + n1 * c)], ry);
+        rz = fma(p.w[j] * p.D[j][c], sf[2][a + n1 * (b + n1 * j)], rz);
+    }
+    const double J = 0.125 * p.h[0] * p.h[1] * p.h[2];
+    const double r = J * ((2.0 / p.h[0]) * p.w[b] * p.w[c] * rx + (2.0 / p.h[1]) * p.w[a] * p.w[c] * ry +
+                          (2.0 / p.h[2]) * p.w[a] * p.w[b] * rz);
+    double da = -r / (p.mx[gx] * p.my[gy] * p.mz[gz]);
+    // nodal terms once per node: by the element that owns it (lowest element index containing the node;
+    // a non-PML owner only occurs where all z vanish)
+    const bool own = (a < N || ex == p.nelx - 1) && (b < N || ey == p.nely - 1) && (c < N || ez == p.nelz - 1);
+    if (own) da -= alpha * p.W[g] + beta * pv + gamma * sm;
+    atomicAdd(p.da + g, da);
+}
+
+// After the volume kernel: w^{n+1} += dt da, p^{n+2} += dt^2 da (the update is linear in the
+// acceleration), and clear da for the next step.  Every node of every PML element is visited; the
+// atomic exchange hands each node's value to exactly one thread.
+template <int N>
+__global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) pml_fixup_kernel(const __grid_constant__ PmlParams p) {
+    constexpr int n1 = N + 1;
+    const int t = threadIdx.x;
+    const int a = t % n1, b = (t / n1) % n1, c = t / (n1 * n1);
+    const int k = blockIdx.x;
+    const int gx = N * p.elems[3 * k] + a, gy = N * p.elems[3 * k + 1] + b, gz = N * p.elems[3 * k + 2] + c;
+    const long long g = ((long long)gz * p.NY + gy) * p.PX + gx;
+    const unsigned long long bits = atomicExch(reinterpret_cast<unsigned long long*>(p.da + g), 0ull);
+    if (bits) {
+        const double v = __longlong_as_double((long long)bits);
+        const double dw = p.dt * v;
+        p.Wn[g] += dw;
+        p.Pn[g] = fma(p.dt, dw, p.Pn[g]);
+    }
+}
+
+void launch_pml_elements(const PmlParams& p, cudaStream_t s) {
+    if (p.n_el <= 0) return;
+    switch (p.N) {
+#define SEM_PML_CASE(n) case n: pml_element_kernel<n><<<p.n_el, (n + 1) * (n + 1) * (n + 1), 0, s>>>(p); break;
+        SEM_PML_CASE(1) SEM_PML_CASE(2) SEM_PML_CASE(3) SEM_PML_CASE(4)
+        SEM_PML_CASE(5) SEM_PML_CASE(6) SEM_PML_CASE(7) SEM_PML_CASE(8)
+#undef SEM_PML_CASE
+        default: break;
+    }
+}
+
+void launch_pml_fixup(const PmlParams& p, cudaStream_t s) {
+    if (p.n_el <= 0) return;
+    switch (p.N) {
+#define SEM_PML_CASE(n) case n: pml_fixup_kernel<n><<<p.n_el, (n + 1) * (n + 1) * (n + 1), 0, s>>>(p); break;
+        SEM_PML_CASE(1) SEM_PML_CASE(2) SEM_PML_CASE(3) SEM_PML_CASE(4)
+        SEM_PML_CASE(5) SEM_PML_CASE(6) SEM_PML_CASE(7) SEM_PML_CASE(8)
+#undef SEM_PML_CASE
+        default: break;
+    }
+}
+
 __global__ void set_state_kernel(const double* pprev, double* pcur, const double* w, long long NX, long long PX,
                                  long long rows, double dt) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;

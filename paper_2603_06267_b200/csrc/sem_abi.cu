@@ -464,13 +464,51 @@ sem::CutParams cut_params(sem_ctx* ctx, sem::Part& pt, int side, int bi, int cur
     return c;
 }
 
+sem::PmlParams pml_params(sem_ctx* ctx, sem::Part& pt, int cur) {
+    sem::PmlBox& m = pt.pml;
+    Box& b = pt.boxes[m.box];
+    sem::PmlParams p{};
+    p.N = b.N;
+    p.NX = b.NX;
+    p.NY = b.NY;
+    p.NZ = b.NZ;
+    p.PX = b.PX;
+    p.nelx = b.d.nel[0];
+    p.nely = b.d.nel[1];
+    p.nelz = b.d.nel[2];
+    p.elems = m.elems;
+    p.n_el = m.n_el;
+    p.P = b.P[cur];
+    p.W = b.W;
+    p.Pn = b.P[1 - cur];
+    p.Wn = b.W;
+    p.psi_old = m.psi[cur];
+    p.psi_new = m.psi[1 - cur];
+    p.phi = m.phi;
+    p.da = m.da;
+    p.zx = m.zx;
+    p.zy = m.zy;
+    p.zz = m.zz;
+    p.mx = b.mx;
+    p.my = b.my;
+    p.mz = m.mz;
+    for (int i = 0; i <= b.N; ++i) {
+        p.w[i] = m.w[i];
+        for (int j = 0; j <= b.N; ++j) p.D[i][j] = m.D[(size_t)i * (b.N + 1) + j];
+    }
+    for (int d = 0; d < 3; ++d) p.h[d] = b.h[d];
+    p.c2 = b.d.c * b.d.c;
+    p.dt = ctx->dt;
+    return p;
+}
+
 // enqueue one step with parity `cur` on ctx->stream; returns the number of kernel launches
 int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
     cudaStream_t s = ctx->stream;
     int nl = 0;
     auto mark = [&](int which, bool begin, cudaStream_t on) {
         if (!prof) return;
-        static thread_local cudaEvent_t pend[3] = {nullptr, nullptr, nullptr};
+        static thread_local cudaEvent_t pend[4] = {nullptr, nullptr, nullptr, nullptr};
         cudaEvent_t e;
         if (ctx->ev_pool.empty()) {
             cudaEventCreate(&e);
@@ -514,6 +552,18 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
         mark(1, false, s);
     }
     if (fork) cudaStreamWaitEvent(s, ctx->ev_mjoin, 0);
+    // PML auxiliaries and the PML acceleration (reads p^{n+1} and w^n: before the volume kernel)
+    bool any_pml = false;
+    for (auto& pt : ctx->parts) any_pml = any_pml || pt.pml.on;
+    if (any_pml) {
+        mark(3, true, s);
+        for (auto& pt : ctx->parts)
+            if (pt.pml.on) {
+                sem::launch_pml_elements(pml_params(ctx, pt, cur), s);
+                ++nl;
+            }
+        mark(3, false, s);
+    }
     const bool slabs = ctx->world > 1;
     if (slabs) {
         for (auto& pt : ctx->parts)
@@ -589,6 +639,11 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
                         ++nl;
                     }
     }
+    for (auto& pt : ctx->parts)
+        if (pt.pml.on) {
+            sem::launch_pml_fixup(pml_params(ctx, pt, cur), s);
+            ++nl;
+        }
     return nl;
 }
 
@@ -604,6 +659,15 @@ sem_status reset_dynamic(sem_ctx* ctx) {
         CU(cudaMemsetAsync(pt.pm.phi, 0, pt.pm.n_pmut * sizeof(double), ctx->stream));
         Box& b = pt.boxes[pt.pm.box];
         CU(cudaMemsetAsync(pt.pm.F, 0, b.NX * b.NY * sizeof(double), ctx->stream));
+    }
+    for (auto& pt : ctx->parts) {
+        sem::PmlBox& m = pt.pml;
+        if (!m.on) continue;
+        Box& b = pt.boxes[m.box];
+        const size_t nl = (size_t)(b.N + 1) * (b.N + 1) * (b.N + 1);
+        CU(cudaMemsetAsync(m.phi, 0, (size_t)m.n_el * 3 * nl * sizeof(double), ctx->stream));
+        for (int k = 0; k < 2; ++k) CU(cudaMemsetAsync(m.psi[k], 0, (size_t)b.nalloc() * sizeof(double), ctx->stream));
+        CU(cudaMemsetAsync(m.da, 0, (size_t)b.nalloc() * sizeof(double), ctx->stream));
     }
     ctx->step = 0;
     return SEM_OK;
@@ -1014,6 +1078,86 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
     return SEM_OK;
 }
 
+sem_status sem_pml_attach(sem_ctx* ctx, int box, const double* thickness, double R) {
+    sem_status st = check_ctx(ctx);
+    if (st) return st;
+    if (box < 0 || box >= (int)ctx->gdesc.size() || !thickness) return fail(ctx, SEM_E_ARG, "bad box / thickness");
+    if (!(R > 0.0 && R < 1.0)) return fail(ctx, SEM_E_ARG, "PML reflection coefficient must be in (0, 1)");
+    if (ctx->world > 1 || ctx->parts.size() != 1)
+        return fail(ctx, SEM_E_PARTITION, "the PML is implemented for a single slab (world 1) only");
+    sem::Part& pt = ctx->parts[0];
+    if (pt.pml.on) return fail(ctx, SEM_E_STATE, "PML already attached");
+    Box& b = pt.boxes[box];
+    const sem_box_desc& g = ctx->gdesc[box];
+    for (int f = 0; f < 6; ++f)
+        if (!(thickness[f] >= 0.0) || !std::isfinite(thickness[f])) return fail(ctx, SEM_E_ARG, "thickness must be >= 0");
+    for (int d = 0; d < 3; ++d)
+        if (thickness[2 * d] + thickness[2 * d + 1] > g.extent[d] * (1.0 + 1e-12))
+            return fail(ctx, SEM_E_ARG, "PML layers of opposite faces overlap");
+    const int N = b.N;
+    std::vector<double> x, w;
+    gll_rule(N, x, w);
+    sem::PmlBox& m = pt.pml;
+    m.box = box;
+    m.D = deriv_matrix(x);
+    m.w = w;
+    // 1D damping profiles z_d at the lattice nodes (reading R23)
+    const long long nn[3] = {b.NX, b.NY, b.NZ};
+    std::vector<double> zt[3];
+    std::vector<char> epml[3];
+    for (int d = 0; d < 3; ++d) {
+        const int nel = g.nel[d];
+        const double hd = g.extent[d] / nel;
+        zt[d].assign(nn[d], 0.0);
+        for (long long i = 0; i < nn[d]; ++i) {
+            long long e = i / N;
+            if (e > nel - 1) e = nel - 1;
+            const int a = (int)(i - e * N);
+            const double xc = g.origin[d] + hd * ((double)e + 0.5 * (x[a] + 1.0));
+            for (int side = 0; side < 2; ++side) {
+                const double ell = thickness[2 * d + side];
+                if (ell <= 0.0) continue;
+                const double lo = g.origin[d], hi = g.origin[d] + g.extent[d];
+                const double dist = side ? xc - (hi - ell) : (lo + ell) - xc;
+                if (dist <= 0.0) continue;
+                const double sfrac = std::min(dist / ell, 1.0);
+                const double ztl = g.c / ell * std::log(1.0 / R);
+                zt[d][i] += ztl * (sfrac - std::sin(2.0 * M_PI * sfrac) / (2.0 * M_PI));
+            }
+        }
+        epml[d].assign(nel, 0);
+        for (int e = 0; e < nel; ++e)
+            for (int a = 0; a <= N; ++a)
+                if (zt[d][(size_t)e * N + a] > 0.0) epml[d][e] = 1;
+    }
+    // PML elements: every element with a node where some z_d > 0
+    std::vector<int> el;
+    for (int ez = 0; ez < g.nel[2]; ++ez)
+        for (int ey = 0; ey < g.nel[1]; ++ey)
+            for (int ex = 0; ex < g.nel[0]; ++ex)
+                if (epml[0][ex] || epml[1][ey] || epml[2][ez]) {
+                    el.push_back(ex);
+                    el.push_back(ey);
+                    el.push_back(ez);
+                }
+    m.n_el = (int)(el.size() / 3);
+    const size_t nl = (size_t)(N + 1) * (N + 1) * (N + 1);
+    if (m.n_el > 0) {
+        if (upload(ctx, &m.elems, el) || upload(ctx, &m.zx, zt[0]) || upload(ctx, &m.zy, zt[1]) ||
+            upload(ctx, &m.zz, zt[2]) || upload(ctx, &m.mz, b.mzh))
+            return SEM_E_CUDA;
+        if (dalloc(ctx, &m.phi, (size_t)m.n_el * 3 * nl) || dalloc(ctx, &m.psi[0], (size_t)b.nalloc()) ||
+            dalloc(ctx, &m.psi[1], (size_t)b.nalloc()) || dalloc(ctx, &m.da, (size_t)b.nalloc()))
+            return SEM_E_OOM;
+        m.on = true;
+    }
+    drop_graphs(ctx);
+    st = reset_dynamic(ctx);
+    if (st) return st;
+    CU(cudaStreamSynchronize(ctx->stream));
+    return SEM_OK;
+}
+
 sem_status sem_plane_wave_source(sem_ctx* ctx, int box, int face, double amp, double f0, double sigma, double t0,
                                  const double dir[3]) {
     sem_status st = check_ctx(ctx);
@@ -1299,7 +1443,7 @@ sem_status sem_set_profiling(sem_ctx* ctx, int on) {
         ctx->ev_pool.push_back(pe.second.second);
     }
     ctx->ev_pending.clear();
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < 4; ++k) {
         ctx->kt_ms[k] = 0;
         ctx->kt_n[k] = 0;
     }
@@ -1310,7 +1454,7 @@ sem_status sem_set_profiling(sem_ctx* ctx, int on) {
 sem_status sem_kernel_time(sem_ctx* ctx, int which, double* ms, long long* nl) {
     sem_status st = check_ctx(ctx);
     if (st) return st;
-    if (which < 0 || which > 2) return fail(ctx, SEM_E_ARG, "which in 0..2");
+    if (which < 0 || which > 3) return fail(ctx, SEM_E_ARG, "which in 0..3");
     CU(cudaStreamSynchronize(ctx->stream));
     for (auto& pe : ctx->ev_pending) {
         float f = 0;

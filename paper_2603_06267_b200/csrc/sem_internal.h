@@ -157,6 +157,36 @@ struct IfaceParams {
     int skip_ix0;                   // slab with a left cut: the shared fine cut line belongs to the left slab
 };
 
+// PML auxiliaries of one box (readings R23-R25).  Phi is element-local
+// (3 components per element GLL node, PML elements only), psi a pitched nodal field (double
+// buffered: psi^{n+1/2} in, psi^{n+3/2} out), da the PML part of the acceleration at region nodes
+// (accumulated by pml_element_kernel, applied and cleared by pml_fixup_kernel).
+struct PmlParams {
+    int N;
+    long long NX, NY, NZ, PX;
+    int nelx, nely, nelz;
+    const int* __restrict__ elems;      // [n_el][3] element coordinates (ex, ey, ez)
+    int n_el;
+    const double* __restrict__ P;       // p^{n+1}
+    const double* __restrict__ W;       // w^n (the predictor velocity pdot^{n+1})
+    double* Pn;                         // p^{n+2} (fix-up)
+    double* Wn;                         // w^{n+1} (fix-up, same array as W)
+    const double* __restrict__ psi_old; // psi^{n+1/2}
+    double* psi_new;                    // psi^{n+3/2}
+    double* phi;                        // [n_el][3][(N+1)^3] Phi^{n+1/2} in, Phi^{n+3/2} out
+    double* da;                         // pitched [nalloc]: PML acceleration, accumulated with atomics
+    const double* __restrict__ zx;      // z_1 at the lattice x nodes [NX]
+    const double* __restrict__ zy;
+    const double* __restrict__ zz;
+    const double* __restrict__ mx;      // assembled 1D masses (h/2) w_asm [NX], [NY], [NZ]
+    const double* __restrict__ my;
+    const double* __restrict__ mz;
+    double D[kMaxN + 1][kMaxN + 1];     // GLL differentiation matrix D[i][j] = l_j'(x_i)
+    double w[kMaxN + 1];                // GLL weights
+    double h[3];                        // element edge lengths
+    double c2, dt;
+};
+
 // One side of one slab cut for one box (partial rows before, fix-up after the exchange).
 struct CutParams {
     int side;                       // 0: cut at ix = 0 (neighbour on the left), 1: at ix = NX-1
@@ -201,6 +231,18 @@ struct Box {
     long long nalloc() const { return PX * NY * NZ; }
 };
 
+struct PmlBox {
+    bool on = false;
+    int box = 0;
+    int n_el = 0;
+    int* elems = nullptr;
+    double* phi = nullptr;
+    double* psi[2] = {nullptr, nullptr};
+    double* da = nullptr;
+    double *zx = nullptr, *zy = nullptr, *zz = nullptr, *mz = nullptr;
+    std::vector<double> D, w;
+};
+
 struct Pmut {
     bool on = false;
     int box = 0, n_pmut = 0, n_modes = 0, lmax = 0;
@@ -235,6 +277,7 @@ struct Part {
     Pmut pm;
     std::vector<int> pm_global;   // global PMUT index of each local PMUT
     Iface itf;
+    PmlBox pml;
     bool cutL = false, cutR = false;
     double* send[2] = {nullptr, nullptr};   // [0] to the left neighbour, [1] to the right
     double* recv[2] = {nullptr, nullptr};
@@ -271,8 +314,8 @@ struct sem_ctx {
     bool profiling = false;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
-    double kt_ms[3] = {0, 0, 0};
-    long long kt_n[3] = {0, 0, 0};
+    double kt_ms[4] = {0, 0, 0, 0};   // kernel groups: 0 volume, 1 interface, 2 modal, 3 PML
+    long long kt_n[4] = {0, 0, 0, 0};
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_mfork = nullptr, ev_mjoin = nullptr;   // modal kernel on `aux`, beside the interface
     cudaStream_t aux = nullptr;
@@ -292,6 +335,8 @@ void launch_fill_random(double* p, double* w, double* pn, long long NX, long lon
                         long long gx0, long long NXg, unsigned long long seed, int box, double ps, double vs,
                         double dt, cudaStream_t s);
 void launch_cut_partial(const CutParams& c, cudaStream_t s);
+void launch_pml_elements(const PmlParams& p, cudaStream_t s);
+void launch_pml_fixup(const PmlParams& p, cudaStream_t s);
 void launch_cut_fixup(const CutParams& c, cudaStream_t s);
 void launch_set_state(const double* pprev, double* pcur, const double* w, long long NX, long long PX, long long rows,
                       double dt, cudaStream_t s);

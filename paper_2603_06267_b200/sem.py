@@ -65,6 +65,7 @@ def _load():
         "sem_dg_interface_build": [P, C.c_int, C.c_int, C.c_double, C.c_int],
         "sem_plane_wave_source": [P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                                   C.POINTER(C.c_double)],
+        "sem_pml_attach": [P, C.c_int, C.POINTER(C.c_double), C.c_double],
         "sem_step": [P, C.c_int],
         "sem_sync": [P],
         "sem_read_pressure": [P, C.c_int, C.POINTER(C.c_double), C.c_size_t],
@@ -89,7 +90,8 @@ def _load():
 
 
 LIB = _load()
-EXPORTED = ("sem_mesh_create", "sem_nccl_unique_id", "sem_slab_plan", "sem_pmut_attach", "sem_dg_interface_build", "sem_plane_wave_source",
+EXPORTED = ("sem_mesh_create", "sem_nccl_unique_id", "sem_slab_plan", "sem_pmut_attach", "sem_dg_interface_build",
+            "sem_plane_wave_source", "sem_pml_attach",
             "sem_step", "sem_sync", "sem_read_pressure", "sem_read_pressure_at", "sem_read_modal",
             "sem_write_state", "sem_fill_random_state", "sem_query", "sem_set_profiling", "sem_kernel_time",
             "sem_last_launch_count", "sem_last_error", "sem_destroy")
@@ -181,6 +183,11 @@ def sem_dg_interface_build(ctx, fine_box, coarse_box, penalty_alpha, quad_rule=0
 def sem_plane_wave_source(ctx, box, face, amp_pa, f0_hz, sigma_s, t0_s, direction):
     d = (C.c_double * 3)(*[float(v) for v in direction])
     _check(ctx, LIB.sem_plane_wave_source(ctx, box, face, amp_pa, f0_hz, sigma_s, t0_s, d))
+
+
+def sem_pml_attach(ctx, box, thickness, R):
+    t = (C.c_double * 6)(*[float(v) for v in thickness])
+    _check(ctx, LIB.sem_pml_attach(ctx, int(box), t, float(R)))
 
 
 def sem_step(ctx, n_steps):
@@ -279,6 +286,9 @@ class Simulation:
             if rec.get("interface") is not None:
                 it = rec["interface"]
                 sem_dg_interface_build(self.ctx, it["fine_box"], it["coarse_box"], it["alpha"], 0)
+            if rec.get("pml") is not None:
+                pl = rec["pml"]
+                sem_pml_attach(self.ctx, pl["box"], pl["thickness"], pl["R"])
             if rec.get("plane_wave") is not None:
                 pw = rec["plane_wave"]
                 sem_plane_wave_source(self.ctx, pw["box"], pw["face"], pw["amp_pa"], pw["f0_hz"], pw["sigma_s"],
