@@ -139,6 +139,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=20)
     ap.add_argument("--ref-patch", type=int, default=4)
+    ap.add_argument("--pml", type=int, default=0,
+                    help="PML layers of this many elements on the lateral and top faces of the last box "
+                         "(SURVEY 8(f) item 1; not part of BASELINE.json's configs)")
     args = ap.parse_args()
     assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_SHORT"), "timing rules: warmup >= 3"
 
@@ -162,6 +165,12 @@ def main():
     from sem_inputs import config
 
     rec = config(args.config)
+    if args.pml:
+        bl = rec["boxes"][-1]
+        hl = [e / n for e, n in zip(bl["extent"], bl["nel"])]
+        th = [args.pml * hl[f // 2] if f != 4 else 0.0 for f in range(6)]
+        bl["bc"] = [1 if th[f] > 0 else bl["bc"][f] for f in range(6)]     # ABC behind the layer
+        rec["pml"] = {"box": len(rec["boxes"]) - 1, "thickness": th, "R": 1e-4}
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     nccl_id = None
@@ -201,6 +210,7 @@ def main():
     vol_ms, vol_n = sem_kernel_time(sim.ctx, 0)
     ifc_ms, ifc_n = sem_kernel_time(sim.ctx, 1)
     mod_ms, mod_n = sem_kernel_time(sim.ctx, 2)
+    pml_ms, pml_n = sem_kernel_time(sim.ctx, 3)
     sem_set_profiling(sim.ctx, 0)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -273,6 +283,9 @@ def main():
         "clocks": clk,
         "e2e": e2e,
     }
+    if args.pml:
+        out["config"]["pml"] = {"elements_per_layer": args.pml, "box": rec["pml"]["box"], "R": rec["pml"]["R"],
+                                "faces": "lateral + top", "element_kernel_ms_per_step": pml_ms / max(pml_n, 1)}
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args.cpu_steps)
     if rank == 0:
