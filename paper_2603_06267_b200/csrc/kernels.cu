@@ -1101,7 +1101,11 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) pml_element_kerne
         gp[2] = fma(p.D[c][j], sp[iz], gp[2]);
         gs[2] = fma(p.D[c][j], ss[iz], gs[2]);
     }
-    const double z[3] = {p.zx[gx], p.zy[gy], p.zz[gz]};
+    const double* __restrict__ Tx = p.tx + 4 * gx;
+    const double* __restrict__ Ty = p.ty + 4 * gy;
+    const double* __restrict__ Tz = p.tz + 4 * gz;
+    const double z[3] = {Tx[0], Ty[0], Tz[0]};
+    const double cA[3] = {Tx[1], Ty[1], Tz[1]}, cB[3] = {Tx[2], Ty[2], Tz[2]};
     const double alpha = z[0] + z[1] + z[2];
     const double beta = z[0] * z[1] + z[1] * z[2] + z[2] * z[0];
     const double gamma = z[0] * z[1] * z[2];
@@ -1109,10 +1113,9 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) pml_element_kerne
     double* ph = p.phi + (size_t)k * 3 * nl;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        const double sc = 2.0 / p.h[d];
         const double old = ph[d * nl + t];
-        const double rhs = p.c2 * ((alpha - 2.0 * z[d]) * sc * gp[d] + Z3[d] * sc * gs[d]);
-        const double nw = (fma(-0.5 * p.dt, z[d], 1.0) * old + p.dt * rhs) / fma(0.5 * p.dt, z[d], 1.0);
+        const double rhs = p.c2 * p.s2h[d] * ((alpha - 2.0 * z[d]) * gp[d] + Z3[d] * gs[d]);
+        const double nw = fma(cA[d], old, cB[d] * rhs);   // Crank-Nicolson on Z1 = -z_d
         ph[d * nl + t] = nw;
         sf[d][t] = 0.5 * (old + nw);
     }
@@ -1125,10 +1128,9 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) pml_element_kerne
         ry = fma(p.w[j] * p.D[j][b], sf[1][a + n1 * (j + n1 * c)], ry);
         rz = fma(p.w[j] * p.D[j][c], sf[2][a + n1 * (b + n1 * j)], rz);
     }
-    const double J = 0.125 * p.h[0] * p.h[1] * p.h[2];
-    const double r = J * ((2.0 / p.h[0]) * p.w[b] * p.w[c] * rx + (2.0 / p.h[1]) * p.w[a] * p.w[c] * ry +
-                          (2.0 / p.h[2]) * p.w[a] * p.w[b] * rz);
-    double da = -r / (p.mx[gx] * p.my[gy] * p.mz[gz]);
+    const double r = p.jac * (p.s2h[0] * p.w[b] * p.w[c] * rx + p.s2h[1] * p.w[a] * p.w[c] * ry +
+                              p.s2h[2] * p.w[a] * p.w[b] * rz);
+    double da = -r * (Tx[3] * Ty[3] * Tz[3]);
     // nodal terms once per node: by the element that owns it (lowest element index containing the node;
     // a non-PML owner only occurs where all z vanish)
     const bool own = (a < N || ex == p.nelx - 1) && (b < N || ey == p.nely - 1) && (c < N || ez == p.nelz - 1);

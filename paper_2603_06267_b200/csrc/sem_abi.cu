@@ -486,17 +486,15 @@ sem::PmlParams pml_params(sem_ctx* ctx, sem::Part& pt, int cur) {
     p.psi_new = m.psi[1 - cur];
     p.phi = m.phi;
     p.da = m.da;
-    p.zx = m.zx;
-    p.zy = m.zy;
-    p.zz = m.zz;
-    p.mx = b.mx;
-    p.my = b.my;
-    p.mz = m.mz;
+    p.tx = m.tab[0];
+    p.ty = m.tab[1];
+    p.tz = m.tab[2];
     for (int i = 0; i <= b.N; ++i) {
         p.w[i] = m.w[i];
         for (int j = 0; j <= b.N; ++j) p.D[i][j] = m.D[(size_t)i * (b.N + 1) + j];
     }
-    for (int d = 0; d < 3; ++d) p.h[d] = b.h[d];
+    for (int d = 0; d < 3; ++d) p.s2h[d] = 2.0 / b.h[d];
+    p.jac = 0.125 * b.h[0] * b.h[1] * b.h[2];
     p.c2 = b.d.c * b.d.c;
     p.dt = ctx->dt;
     return p;
@@ -523,22 +521,40 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
     // modal ROM (a2-a4) and SIPG interface (a8) only read p^{n+1}: with both present the modal kernel
     // runs on the auxiliary stream, concurrently with the interface kernels (fork/join by events, also
     // inside the captured graph)
-    bool any_pm = false;
-    for (auto& pt : ctx->parts) any_pm = any_pm || pt.pm.on;
-    const bool fork = any_pm && ctx->itf_on;
+    // The modal ROM (a2-a4), the PML auxiliaries and the SIPG interface (a8) only read p^{n+1} (and
+    // w^n): with interface work present the first two run on the auxiliary stream, concurrently with
+    // the interface kernels (event fork/join, also inside the captured graph).
+    bool any_pm = false, any_pml = false;
+    for (auto& pt : ctx->parts) {
+        any_pm = any_pm || pt.pm.on;
+        any_pml = any_pml || pt.pml.on;
+    }
+    const bool fork = (any_pm || any_pml) && ctx->itf_on;
     cudaStream_t ms = s;
     if (fork) {
         cudaEventRecord(ctx->ev_mfork, s);
         cudaStreamWaitEvent(ctx->aux, ctx->ev_mfork, 0);
         ms = ctx->aux;
     }
-    mark(2, true, ms);
-    for (auto& pt : ctx->parts)
-        if (pt.pm.on) {
-            sem::launch_modal(modal_params(ctx, pt, cur), ms);
-            ++nl;
-        }
-    mark(2, false, ms);
+    if (any_pm) {
+        mark(2, true, ms);
+        for (auto& pt : ctx->parts)
+            if (pt.pm.on) {
+                sem::launch_modal(modal_params(ctx, pt, cur), ms);
+                ++nl;
+            }
+        mark(2, false, ms);
+    }
+    // PML auxiliaries and the PML acceleration (reads p^{n+1} and w^n: before the volume kernel)
+    if (any_pml) {
+        mark(3, true, ms);
+        for (auto& pt : ctx->parts)
+            if (pt.pml.on) {
+                sem::launch_pml_elements(pml_params(ctx, pt, cur), ms);
+                ++nl;
+            }
+        mark(3, false, ms);
+    }
     if (fork) cudaEventRecord(ctx->ev_mjoin, ctx->aux);
     if (ctx->itf_on) {
         mark(1, true, s);
@@ -552,18 +568,6 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
         mark(1, false, s);
     }
     if (fork) cudaStreamWaitEvent(s, ctx->ev_mjoin, 0);
-    // PML auxiliaries and the PML acceleration (reads p^{n+1} and w^n: before the volume kernel)
-    bool any_pml = false;
-    for (auto& pt : ctx->parts) any_pml = any_pml || pt.pml.on;
-    if (any_pml) {
-        mark(3, true, s);
-        for (auto& pt : ctx->parts)
-            if (pt.pml.on) {
-                sem::launch_pml_elements(pml_params(ctx, pt, cur), s);
-                ++nl;
-            }
-        mark(3, false, s);
-    }
     const bool slabs = ctx->world > 1;
     if (slabs) {
         for (auto& pt : ctx->parts)
@@ -1143,9 +1147,20 @@ sem_status sem_pml_attach(sem_ctx* ctx, int box, const double* thickness, double
     m.n_el = (int)(el.size() / 3);
     const size_t nl = (size_t)(N + 1) * (N + 1) * (N + 1);
     if (m.n_el > 0) {
-        if (upload(ctx, &m.elems, el) || upload(ctx, &m.zx, zt[0]) || upload(ctx, &m.zy, zt[1]) ||
-            upload(ctx, &m.zz, zt[2]) || upload(ctx, &m.mz, b.mzh))
-            return SEM_E_CUDA;
+        // per-axis node tables: z, CN factors, inverse assembled 1D mass (PmlParams::tx)
+        const std::vector<double>* m1[3] = {&b.mxh, &b.myh, &b.mzh};
+        for (int d = 0; d < 3; ++d) {
+            std::vector<double> t4((size_t)nn[d] * 4);
+            for (long long i = 0; i < nn[d]; ++i) {
+                const double zz = zt[d][i], den = 1.0 + 0.5 * ctx->dt * zz;
+                t4[4 * i] = zz;
+                t4[4 * i + 1] = (1.0 - 0.5 * ctx->dt * zz) / den;
+                t4[4 * i + 2] = ctx->dt / den;
+                t4[4 * i + 3] = 1.0 / (*m1[d])[i];
+            }
+            if (upload(ctx, &m.tab[d], t4)) return SEM_E_CUDA;
+        }
+        if (upload(ctx, &m.elems, el)) return SEM_E_CUDA;
         if (dalloc(ctx, &m.phi, (size_t)m.n_el * 3 * nl) || dalloc(ctx, &m.psi[0], (size_t)b.nalloc()) ||
             dalloc(ctx, &m.psi[1], (size_t)b.nalloc()) || dalloc(ctx, &m.da, (size_t)b.nalloc()))
             return SEM_E_OOM;

@@ -175,15 +175,15 @@ struct PmlParams {
     double* psi_new;                    // psi^{n+3/2}
     double* phi;                        // [n_el][3][(N+1)^3] Phi^{n+1/2} in, Phi^{n+3/2} out
     double* da;                         // pitched [nalloc]: PML acceleration, accumulated with atomics
-    const double* __restrict__ zx;      // z_1 at the lattice x nodes [NX]
-    const double* __restrict__ zy;
-    const double* __restrict__ zz;
-    const double* __restrict__ mx;      // assembled 1D masses (h/2) w_asm [NX], [NY], [NZ]
-    const double* __restrict__ my;
-    const double* __restrict__ mz;
+    // per-axis node tables [n_d][4]: z_d, (1 - dt z_d/2)/(1 + dt z_d/2), dt/(1 + dt z_d/2), 1/m_d with
+    // m_d the assembled 1D lumped mass (h/2) w_asm (no division in the kernel)
+    const double* __restrict__ tx;
+    const double* __restrict__ ty;
+    const double* __restrict__ tz;
     double D[kMaxN + 1][kMaxN + 1];     // GLL differentiation matrix D[i][j] = l_j'(x_i)
     double w[kMaxN + 1];                // GLL weights
-    double h[3];                        // element edge lengths
+    double s2h[3];                      // 2 / h_d
+    double jac;                         // |J| = h_x h_y h_z / 8
     double c2, dt;
 };
 
@@ -239,7 +239,7 @@ struct PmlBox {
     double* phi = nullptr;
     double* psi[2] = {nullptr, nullptr};
     double* da = nullptr;
-    double *zx = nullptr, *zy = nullptr, *zz = nullptr, *mz = nullptr;
+    double* tab[3] = {nullptr, nullptr, nullptr};   // per-axis node tables (PmlParams::tx)
     std::vector<double> D, w;
 };
 
