@@ -299,3 +299,47 @@ def random_state(rec, seed=1234, scale_v=None):
         v = rng.standard_normal(n) * (1.0 / rec["dt"] * 1e-3 if scale_v is None else scale_v)
         out.append((p, v))
     return out
+
+
+def interface_faces(nfx=4, nfy=3, R=2, hf=25e-6, z0=0.0, jitter=0.0, seed=0):
+    """Face sets of a 2:1 (R:1) non-conforming interface for the face-matching algorithm (Algorithm 3):
+    fine elements nfx x nfy of edge hf below the plane z = z0 (their +z faces, local face 5) and coarse
+    elements (nfx/R) x (nfy/R) of edge R hf above it (their -z faces, local face 4).  Interior vertices
+    of the plane are moved in-plane by U(-jitter, jitter) * edge (seeded), so the maps are trilinear
+    (non-affine) while both face sets still tile the same planar region.  Returns (fine, coarse):
+    lists of (verts (8, 3) in the order v = i + 2 j + 4 k, local face)."""
+    rng = np.random.default_rng(seed)
+    ncx, ncy = nfx // R, nfy // R
+
+    def plane_lattice(nx, ny, h):
+        X, Y = np.meshgrid(np.arange(nx + 1) * h, np.arange(ny + 1) * h, indexing="ij")
+        J = rng.uniform(-jitter, jitter, size=(2, nx + 1, ny + 1)) * h
+        J[:, 0, :] = J[:, -1, :] = 0.0
+        J[:, :, 0] = J[:, :, -1] = 0.0
+        return X + J[0], Y + J[1]
+
+    fx, fy = plane_lattice(nfx, nfy, hf)
+    cx, cy = plane_lattice(ncx, ncy, R * hf)
+    fine, coarse = [], []
+    for j in range(nfy):
+        for i in range(nfx):
+            v = np.zeros((8, 3))
+            for k in range(8):
+                a, b, c = k & 1, (k >> 1) & 1, k >> 2
+                if c == 1:      # top = interface plane (jittered)
+                    v[k] = [fx[i + a, j + b], fy[i + a, j + b], z0]
+                else:
+                    v[k] = [(i + a) * hf, (j + b) * hf, z0 - hf]
+            fine.append((v, 5))
+    for j in range(ncy):
+        for i in range(ncx):
+            v = np.zeros((8, 3))
+            for k in range(8):
+                a, b, c = k & 1, (k >> 1) & 1, k >> 2
+                if c == 0:      # bottom = interface plane (jittered)
+                    v[k] = [cx[i + a, j + b], cy[i + a, j + b], z0]
+                else:
+                    v[k] = [(i + a) * R * hf, (j + b) * R * hf, z0 + R * hf]
+            coarse.append((v, 4))
+    return fine, coarse
+
