@@ -157,6 +157,26 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
  * SEM_E_STATE (already attached), SEM_E_OOM.  Resets the dynamic state like sem_pmut_attach. */
 sem_status sem_pml_attach(sem_ctx* ctx, int box, const double* thickness, double R);
 
+/* Algorithm 3 (face matching on the non-conforming interface) on GPU `device`: for every
+ * quadrature node x_q = X_{K+}(xhat_q+) of every fine face (the face's GLL nodes of `degree`, reading R9;
+ * node q = a + (degree+1) b, a along the face's first tangential axis) find the coarse face dK- that
+ * contains it: opposite normals |n+ + n-| < normal_tol (centre normals), one-vertex radius filter
+ * |V_{K-} - x_q| < max(diam dK-, diam dK+) + eps, Newton-Raphson xhat_q- = X_{K-}^{-1}(x_q), accept if
+ * xhat_q- in [-1,1]^3 (1e-9 tolerance); the lowest coarse index wins (reading R26).  A uniform grid of
+ * the coarse faces' first vertices (cell = the largest filter radius) supplies the candidates.
+ * Face sets (host, caller-owned, copied): verts [n][8][3] of the trilinear elements (vertex v = i + 2j
+ * + 4k at reference corner (2i-1, 2j-1, 2k-1)), face [n] local face 0..5 (-x,+x,-y,+y,-z,+z).
+ * Outputs (host, caller-owned): owner [n_fine (degree+1)^2] coarse face index or -1, xi_minus [..][3];
+ * elapsed_ms (optional) = device time of the matching kernels.  Self-contained (no sem_ctx).
+ * Errors: SEM_E_ARG, SEM_E_CUDA, SEM_E_OOM; SEM_E_UNMATCHED if some node has no owner (outputs filled). */
+typedef struct {
+    int n;
+    const double* verts;
+    const int* face;
+} sem_face_set;
+sem_status sem_face_match(int device, const sem_face_set* fine, const sem_face_set* coarse, int degree,
+                          double normal_tol, long long* owner, double* xi_minus, double* elapsed_ms);
+
 /* Incident plane wave entering through absorbing face `face` (only 5 = +z) of `box`
  * (reading R13): p_inc = amp s(t - k.(x - x_ref)/c), s(u) = exp(-(u-t0)^2/(2 sigma^2))
  * sin(2 pi f0 (u-t0)), imposed as total-field first-order ABC data

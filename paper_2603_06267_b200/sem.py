@@ -41,6 +41,10 @@ class MeshDesc(C.Structure):
                 ("nccl_unique_id", C.c_void_p), ("flags", C.c_int)]
 
 
+class FaceSet(C.Structure):
+    _fields_ = [("n", C.c_int), ("verts", C.POINTER(C.c_double)), ("face", C.POINTER(C.c_int))]
+
+
 class PmutDesc(C.Structure):
     _fields_ = [("box", C.c_int), ("face", C.c_int), ("n_pmut", C.c_int), ("n_modes", C.c_int),
                 ("center", C.POINTER(C.c_double)), ("side", C.c_double), ("mode_mn", C.POINTER(C.c_int)),
@@ -66,6 +70,8 @@ def _load():
         "sem_plane_wave_source": [P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                                   C.POINTER(C.c_double)],
         "sem_pml_attach": [P, C.c_int, C.POINTER(C.c_double), C.c_double],
+        "sem_face_match": [C.c_int, C.POINTER(FaceSet), C.POINTER(FaceSet), C.c_int, C.c_double,
+                           C.POINTER(C.c_longlong), C.POINTER(C.c_double), C.POINTER(C.c_double)],
         "sem_step": [P, C.c_int],
         "sem_sync": [P],
         "sem_read_pressure": [P, C.c_int, C.POINTER(C.c_double), C.c_size_t],
@@ -91,7 +97,7 @@ def _load():
 
 LIB = _load()
 EXPORTED = ("sem_mesh_create", "sem_nccl_unique_id", "sem_slab_plan", "sem_pmut_attach", "sem_dg_interface_build",
-            "sem_plane_wave_source", "sem_pml_attach",
+            "sem_plane_wave_source", "sem_pml_attach", "sem_face_match",
             "sem_step", "sem_sync", "sem_read_pressure", "sem_read_pressure_at", "sem_read_modal",
             "sem_write_state", "sem_fill_random_state", "sem_query", "sem_set_profiling", "sem_kernel_time",
             "sem_last_launch_count", "sem_last_error", "sem_destroy")
@@ -188,6 +194,26 @@ def sem_plane_wave_source(ctx, box, face, amp_pa, f0_hz, sigma_s, t0_s, directio
 def sem_pml_attach(ctx, box, thickness, R):
     t = (C.c_double * 6)(*[float(v) for v in thickness])
     _check(ctx, LIB.sem_pml_attach(ctx, int(box), t, float(R)))
+
+
+def sem_face_match(fine, coarse, degree, normal_tol=1e-6, device=0):
+    """Algorithm 3 on the GPU.  fine / coarse: lists of (verts (8,3), local face).  Returns
+    (owner [n_fine, (degree+1)^2] int64, xi [n_fine, (degree+1)^2, 3], device ms)."""
+    def faceset(fs):
+        v = np.ascontiguousarray(np.stack([f[0] for f in fs]) if fs else np.zeros((0, 8, 3)), np.float64)
+        fc = np.ascontiguousarray([int(f[1]) for f in fs], np.int32)
+        return FaceSet(len(fs), _dptr(v), fc.ctypes.data_as(C.POINTER(C.c_int))), (v, fc)
+    fset, keep_f = faceset(fine)
+    cset, keep_c = faceset(coarse)
+    nq = (degree + 1) ** 2
+    owner = np.empty((len(fine), nq), np.int64)
+    xi = np.empty((len(fine), nq, 3), np.float64)
+    ms = C.c_double(0.0)
+    st = LIB.sem_face_match(int(device), C.byref(fset), C.byref(cset), int(degree), float(normal_tol),
+                            owner.ctypes.data_as(C.POINTER(C.c_longlong)), _dptr(xi), C.byref(ms))
+    if st not in (0, -7):
+        raise SemError(st, "sem_face_match failed")
+    return owner, xi, ms.value
 
 
 def sem_step(ctx, n_steps):
