@@ -82,6 +82,10 @@ class Box:
         self.ndof = self.nn[0] * self.nn[1] * self.nn[2]
         self.nelem = self.nel[0] * self.nel[1] * self.nel[2]
         self.h = self.extent / np.asarray(self.nel, dtype=np.float64)
+        v = desc.get("vertices")
+        self.vlat = None if v is None else np.asarray(v, dtype=np.float64).reshape(-1, 3)
+        if self.vlat is not None and len(self.vlat) != (self.nel[0] + 1) * (self.nel[1] + 1) * (self.nel[2] + 1):
+            raise ValueError("vertex lattice size mismatch")
 
     # --- lattice / numbering -------------------------------------------------
     def gid(self, gx, gy, gz):
@@ -110,8 +114,14 @@ class Box:
                         self.N * ez[:, None] + loc[None, :, 2]).astype(np.int64)
 
     def vertices(self, e):
-        """The 8 physical vertices of element e (order v = i + 2j + 4k)."""
+        """The 8 physical vertices of element e (order v = i + 2j + 4k).  A box with a "vertices"
+        lattice [(nel_x+1)(nel_y+1)(nel_z+1), 3] (x fastest) is a logically structured, geometrically
+        trilinear (curved) mesh; otherwise the vertices are the affine lattice."""
         ex, ey, ez = self.elem_coords(e)
+        if self.vlat is not None:
+            nx, ny = self.nel[0] + 1, self.nel[1] + 1
+            idx = [(ex + i) + nx * ((ey + j) + ny * (ez + k)) for k in (0, 1) for j in (0, 1) for i in (0, 1)]
+            return self.vlat[idx]
         lo = self.origin + self.h * np.array([ex, ey, ez], dtype=np.float64)
         return lo[None, :] + (REF_VERTS + 1.0) / 2.0 * self.h[None, :]
 

@@ -343,3 +343,28 @@ def interface_faces(nfx=4, nfy=3, R=2, hf=25e-6, z0=0.0, jitter=0.0, seed=0):
             coarse.append((v, 4))
     return fine, coarse
 
+
+def curved_config(nel=(3, 3, 3), degree=4, extent=(3e-4, 3e-4, 3e-4), amp=0.12, bc_top=BC_RIGID, c=C_WATER,
+                  n_steps=100, cfl=0.25, seed=None):
+    """One logically structured box whose vertex lattice is displaced by the smooth bulge
+    u(x) = amp h (sin(pi x/Lx) sin(pi y/Ly) sin(pi z/Lz)) (1, 0.7, -0.5) (boundary vertices fixed, so
+    the box faces stay planar) -- trilinear, non-affine elements.  With ``seed``
+    the interior vertices get an extra U(-amp/2, amp/2) h jitter.  Faces rigid except the top (bc_top)."""
+    L = np.asarray(extent, dtype=np.float64)
+    h = L / np.asarray(nel)
+    gx, gy, gz = [np.arange(n + 1) * hh for n, hh in zip(nel, h)]
+    Z, Y, X = np.meshgrid(gz, gy, gx, indexing="ij")
+    pts = np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1)
+    bump = np.sin(np.pi * pts[:, 0] / L[0]) * np.sin(np.pi * pts[:, 1] / L[1]) * np.sin(np.pi * pts[:, 2] / L[2])
+    hmin = float(h.min())
+    pts = pts + amp * hmin * bump[:, None] * np.array([1.0, 0.7, -0.5])[None, :]
+    if seed is not None:
+        interior = np.all((pts > 1e-12 * L) & (pts < L * (1 - 1e-12)), axis=1)
+        jit = np.random.default_rng(seed).uniform(-0.5 * amp, 0.5 * amp, size=pts.shape) * hmin
+        pts[interior] += jit[interior]
+    boxes = [_box((0, 0, 0), extent, nel, degree, [BC_RIGID] * 5 + [bc_top], c=c)]
+    boxes[0]["vertices"] = pts
+    rec = {"name": "curved", "boxes": boxes, "n_steps": n_steps, "seed": 0}
+    rec["dt"] = cfl_dt(boxes, cfl)
+    return _finish(rec)
+
