@@ -145,6 +145,18 @@ sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, cons
 sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, double penalty_alpha,
                                   int quad_rule);
 
+/* Curved box (trilinear maps X_K of P:L415-416): replace the affine geometry of
+ * `box` by the vertex lattice verts[n_verts][3], n_verts = (nel_x+1)(nel_y+1)(nel_z+1), x fastest
+ * (element (ex,ey,ez) vertex v = i + 2j + 4k is lattice vertex (ex+i, ey+j, ez+k)); connectivity stays
+ * the box's lattice.  The box then uses the element-scatter path: K p element by element with the
+ * metric terms w_q c^2 |J| J^-1 J^-T recomputed from the 8 vertices at every GLL point (nothing
+ * stored per quadrature point), FP64 atomics into an assembled residual, and a nodal kick-drift with
+ * the assembled lumped mass and ABC diagonal (computed here on the host).  Call right after
+ * sem_mesh_create: curved boxes carry no PMUT / interface / PML / plane wave (SEM_E_STATE), world 1
+ * only (SEM_E_PARTITION).  Caller owns `verts` (copied).  Errors: SEM_E_ARG (size, non-positive
+ * Jacobian at a GLL point), SEM_E_STATE, SEM_E_OOM. */
+sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size_t n_verts);
+
 /* Perfectly matched layer (Eq. 1 lines 1-3; coefficients P:L271-277; profile P:L280-289)
  * inside box `box`: thickness[f] [m] for faces f = -x,+x,-y,+y,-z,+z (0 = no layer) is the slab of the
  * box next to face f; z_d(d) = zt (d/l - sin(2 pi d/l)/(2 pi)), d = depth into the layer,

@@ -1180,6 +1180,108 @@ void launch_pml_fixup(const PmlParams& p, cudaStream_t s) {
     }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Curved boxes (trilinear vertex lattice): one block per element, one thread per
+// element GLL node.  grad_hat p by the differentiation matrix, flux = w_q c^2 |J| J^-1 J^-T grad_hat p
+// with J recomputed from the element's 8 vertices (cofactor form: |J| J^-1 J^-T = adj adj^T / det),
+// r_i = sum_q grad_hat phi_i(q) . flux(q) (D^T), scatter-add; then a nodal kick-drift.
+// ------------------------------------------------------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) curved_residual_kernel(const __grid_constant__ CurvedParams p) {
+    constexpr int n1 = N + 1, nl = n1 * n1 * n1;
+    __shared__ double sp[nl], sf[3][nl], sv[24];
+    const int t = threadIdx.x;
+    const int a = t % n1, b = (t / n1) % n1, c = t / (n1 * n1);
+    const int e = blockIdx.x;
+    const int ex = e % p.nelx, ey = (e / p.nelx) % p.nely, ez = e / (p.nelx * p.nely);
+    if (t < 24) {
+        const int v = t / 3, i = t % 3;
+        const int vx = ex + (v & 1), vy = ey + ((v >> 1) & 1), vz = ez + (v >> 2);
+        sv[t] = p.vlat[3 * ((size_t)vx + (size_t)(p.nelx + 1) * ((size_t)vy + (size_t)(p.nely + 1) * vz)) + i];
+    }
+    const int gx = N * ex + a, gy = N * ey + b, gz = N * ez + c;
+    const long long g = ((long long)gz * p.NY + gy) * p.PX + gx;
+    sp[t] = p.P[g];
+    __syncthreads();
+    double gh[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j <= N; ++j) {
+        gh[0] = fma(p.D[a][j], sp[j + n1 * (b + n1 * c)], gh[0]);
+        gh[1] = fma(p.D[b][j], sp[a + n1 * (j + n1 * c)], gh[1]);
+        gh[2] = fma(p.D[c][j], sp[a + n1 * (b + n1 * j)], gh[2]);
+    }
+    // Jacobian of the trilinear map at (x_a, x_b, x_c): J[i][j] = sum_v X_v,i dN_v/dxi_j
+    const double xi[3] = {p.x[a], p.x[b], p.x[c]};
+    double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+        const double s0 = (v & 1) ? 1.0 : -1.0, s1 = (v & 2) ? 1.0 : -1.0, s2 = (v & 4) ? 1.0 : -1.0;
+        const double f0 = 1.0 + s0 * xi[0], f1 = 1.0 + s1 * xi[1], f2 = 1.0 + s2 * xi[2];
+        const double dN[3] = {0.125 * s0 * f1 * f2, 0.125 * s1 * f0 * f2, 0.125 * s2 * f0 * f1};
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) J[i][j] = fma(dN[j], sv[3 * v + i], J[i][j]);
+    }
+    // adj = det J^-1 (rows: cofactors); |J| J^-1 J^-T = adj adj^T / det
+    double A[3][3];
+    A[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    A[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+    A[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+    A[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    A[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+    A[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+    A[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    A[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+    A[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double det = J[0][0] * A[0][0] + J[0][1] * A[1][0] + J[0][2] * A[2][0];
+    const double sc = p.w[a] * p.w[b] * p.w[c] * p.c2 / det;
+    // flux = sc * A A^T gh  (A = adj J, rows i: A[i][:] = d xi_i / d x * det)
+    double u[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) u[i] = A[0][i] * gh[0] + A[1][i] * gh[1] + A[2][i] * gh[2];   // A^T gh
+#pragma unroll
+    for (int i = 0; i < 3; ++i) sf[i][t] = sc * (A[i][0] * u[0] + A[i][1] * u[1] + A[i][2] * u[2]);
+    __syncthreads();
+    double r = 0.0;
+#pragma unroll
+    for (int j = 0; j <= N; ++j) {
+        r = fma(p.D[j][a], sf[0][j + n1 * (b + n1 * c)], r);
+        r = fma(p.D[j][b], sf[1][a + n1 * (j + n1 * c)], r);
+        r = fma(p.D[j][c], sf[2][a + n1 * (b + n1 * j)], r);
+    }
+    atomicAdd(p.res + g, r);
+}
+
+__global__ void curved_update_kernel(const __grid_constant__ CurvedParams p) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.NX * p.NY * p.NZ) return;
+    const long long g = (i / p.NX) * p.PX + i % p.NX;
+    const double wv = p.W[g];
+    const double a = -p.minv[g] * p.res[g] - p.cdamp[g] * wv;
+    p.res[g] = 0.0;
+    const double wn = fma(p.dt, a, wv);
+    p.W[g] = wn;
+    p.Pn[g] = fma(p.dt, wn, p.P[g]);
+}
+
+void launch_curved(const CurvedParams& p, cudaStream_t s) {
+    const int nel = p.nelx * p.nely * p.nelz;
+    switch (p.N) {
+#define SEM_CV_CASE(n) case n: curved_residual_kernel<n><<<nel, (n + 1) * (n + 1) * (n + 1), 0, s>>>(p); break;
+        SEM_CV_CASE(1) SEM_CV_CASE(2) SEM_CV_CASE(3) SEM_CV_CASE(4)
+        SEM_CV_CASE(5) SEM_CV_CASE(6) SEM_CV_CASE(7) SEM_CV_CASE(8)
+#undef SEM_CV_CASE
+        default: break;
+    }
+    const long long n = p.NX * p.NY * p.NZ;
+    curved_update_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p);
+}
+
+__global__ void step_bump_kernel(long long* step) { *step += 1; }
+
+void launch_step_bump(long long* step, cudaStream_t s) { step_bump_kernel<<<1, 1, 0, s>>>(step); }
+
 __global__ void set_state_kernel(const double* pprev, double* pcur, const double* w, long long NX, long long PX,
                                  long long rows, double dt) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;

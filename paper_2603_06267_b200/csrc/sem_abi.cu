@@ -464,6 +464,36 @@ sem::CutParams cut_params(sem_ctx* ctx, sem::Part& pt, int side, int bi, int cur
     return c;
 }
 
+sem::CurvedParams curved_params(sem_ctx* ctx, Box& b, int cur) {
+    sem::CurvedParams p{};
+    p.N = b.N;
+    p.NX = b.NX;
+    p.NY = b.NY;
+    p.NZ = b.NZ;
+    p.PX = b.PX;
+    p.nelx = b.d.nel[0];
+    p.nely = b.d.nel[1];
+    p.nelz = b.d.nel[2];
+    p.vlat = b.vlat;
+    p.P = b.P[cur];
+    p.res = b.res;
+    p.W = b.W;
+    p.Pn = b.P[1 - cur];
+    p.minv = b.minv;
+    p.cdamp = b.cdamp;
+    std::vector<double> x, w;
+    gll_rule(b.N, x, w);
+    const std::vector<double> D = deriv_matrix(x);
+    for (int i = 0; i <= b.N; ++i) {
+        p.x[i] = x[i];
+        p.w[i] = w[i];
+        for (int j = 0; j <= b.N; ++j) p.D[i][j] = D[(size_t)i * (b.N + 1) + j];
+    }
+    p.c2 = b.d.c * b.d.c;
+    p.dt = ctx->dt;
+    return p;
+}
+
 sem::PmlParams pml_params(sem_ctx* ctx, sem::Part& pt, int cur) {
     sem::PmlBox& m = pt.pml;
     Box& b = pt.boxes[m.box];
@@ -609,7 +639,8 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
         std::vector<sem::VolLaunch> ls;
         for (auto& pt : ctx->parts) {
             const int nb = (int)pt.boxes.size();
-            if (nb == 2 && sem::volume_pair_supported(pt.boxes[0].N, pt.boxes[1].N)) {
+            if (nb == 2 && sem::volume_pair_supported(pt.boxes[0].N, pt.boxes[1].N) && !pt.boxes[0].curved &&
+                !pt.boxes[1].curved) {
                 sem::VolLaunch L{};
                 L.nbox = 2;
                 L.box[0] = vol_params(ctx, pt, 0, cur);
@@ -617,6 +648,7 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
                 ls.push_back(L);
             } else {
                 for (int bi = 0; bi < nb; ++bi) {
+                    if (pt.boxes[bi].curved) continue;   // element-scatter path below
                     sem::VolLaunch L{};
                     L.nbox = 1;
                     L.box[0] = vol_params(ctx, pt, bi, cur);
@@ -629,6 +661,17 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
             ls[i].step = ctx->d_step;
             ls[i].bump_step = i + 1 == ls.size() ? 1 : 0;
             sem::launch_volume(ls[i], s);
+            ++nl;
+        }
+        // curved boxes: element-by-element residual + nodal update (no structured volume launch)
+        for (auto& pt : ctx->parts)
+            for (auto& bx : pt.boxes)
+                if (bx.curved) {
+                    sem::launch_curved(curved_params(ctx, bx, cur), s);
+                    nl += 2;
+                }
+        if (ls.empty()) {
+            sem::launch_step_bump(ctx->d_step, s);
             ++nl;
         }
     }
@@ -860,6 +903,8 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
     if (ctx->n_pmut) return fail(ctx, SEM_E_STATE, "PMUT array already attached");
     if (pd->box < 0 || pd->box >= (int)ctx->gdesc.size()) return fail(ctx, SEM_E_ARG, "bad box");
     if (pd->face != 4) return fail(ctx, SEM_E_ARG, "PMUTs supported on the -z face only");
+    for (auto& pt : ctx->parts)
+        if (pt.boxes[pd->box].curved) return fail(ctx, SEM_E_STATE, "PMUTs on a curved box are not supported");
     if (pd->n_pmut < 1 || pd->n_modes < 1 || pd->n_modes > sem::kMaxModes)
         return fail(ctx, SEM_E_ARG, "n_pmut >= 1 and 1 <= n_modes <= 8 required");
     if (!(pd->side > 0) || !pd->center || !pd->mode_mn || !pd->freq_hz || !pd->modal_mass || !pd->damping_ratio ||
@@ -983,6 +1028,9 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
     const int nb = (int)ctx->gdesc.size();
     if (fine_box < 0 || coarse_box < 0 || fine_box >= nb || coarse_box >= nb || fine_box == coarse_box)
         return fail(ctx, SEM_E_ARG, "bad box indices");
+    for (auto& pt : ctx->parts)
+        if (pt.boxes[fine_box].curved || pt.boxes[coarse_box].curved)
+            return fail(ctx, SEM_E_STATE, "the interface of a curved box is not supported");
     if (!(alpha > 0)) return fail(ctx, SEM_E_ARG, "penalty alpha must be > 0");
     const sem_box_desc& gF = ctx->gdesc[fine_box];
     const sem_box_desc& gC = ctx->gdesc[coarse_box];
@@ -1082,6 +1130,80 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
     return SEM_OK;
 }
 
+sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size_t n_verts) {
+    sem_status st = check_ctx(ctx);
+    if (st) return st;
+    if (box < 0 || box >= (int)ctx->gdesc.size() || !verts) return fail(ctx, SEM_E_ARG, "bad box / vertices");
+    if (ctx->world > 1 || ctx->parts.size() != 1)
+        return fail(ctx, SEM_E_PARTITION, "curved boxes are implemented for a single slab (world 1) only");
+    sem::Part& pt = ctx->parts[0];
+    Box& b = pt.boxes[box];
+    const sem_box_desc& g = ctx->gdesc[box];
+    if (b.curved) return fail(ctx, SEM_E_STATE, "vertices already set");
+    if ((pt.pm.on && pt.pm.box == box) || b.iface_side != 0 || (pt.pml.on && pt.pml.box == box) ||
+        (ctx->pw.on && ctx->pw.box == box))
+        return fail(ctx, SEM_E_STATE, "curved boxes carry no PMUT / interface / PML / plane wave (set vertices first)");
+    const int nx = g.nel[0] + 1, ny = g.nel[1] + 1, nz = g.nel[2] + 1;
+    if (n_verts != (size_t)nx * ny * nz) return fail(ctx, SEM_E_ARG, "n_verts must be (nel_x+1)(nel_y+1)(nel_z+1)");
+    const int N = b.N, n1 = N + 1;
+    std::vector<double> x, w;
+    gll_rule(N, x, w);
+    // assembled lumped mass (sum_e w_q |det J|) and ABC diagonal (sum_F c w_s w_t |J_s|), Eq. 8
+    std::vector<double> M((size_t)b.nalloc(), 0.0), Cd((size_t)b.nalloc(), 0.0);
+    auto vtx = [&](int vx, int vy, int vz, int i) { return verts[3 * ((size_t)vx + (size_t)nx * ((size_t)vy + (size_t)ny * vz)) + i]; };
+    for (int ez = 0; ez < g.nel[2]; ++ez)
+        for (int ey = 0; ey < g.nel[1]; ++ey)
+            for (int ex = 0; ex < g.nel[0]; ++ex)
+                for (int c = 0; c <= N; ++c)
+                    for (int bb = 0; bb <= N; ++bb)
+                        for (int a = 0; a <= N; ++a) {
+                            const double xi[3] = {x[a], x[bb], x[c]};
+                            double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+                            for (int v = 0; v < 8; ++v) {
+                                const double s0 = (v & 1) ? 1.0 : -1.0, s1 = (v & 2) ? 1.0 : -1.0, s2 = (v & 4) ? 1.0 : -1.0;
+                                const double f0 = 1.0 + s0 * xi[0], f1 = 1.0 + s1 * xi[1], f2 = 1.0 + s2 * xi[2];
+                                const double dN[3] = {0.125 * s0 * f1 * f2, 0.125 * s1 * f0 * f2, 0.125 * s2 * f0 * f1};
+                                for (int i = 0; i < 3; ++i)
+                                    for (int j = 0; j < 3; ++j)
+                                        J[i][j] += dN[j] * vtx(ex + (v & 1), ey + ((v >> 1) & 1), ez + (v >> 2), i);
+                            }
+                            const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                                               J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                                               J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+                            if (!(det > 0.0)) return fail(ctx, SEM_E_ARG, "non-positive Jacobian at a GLL point");
+                            const long long gx = (long long)N * ex + a, gy = (long long)N * ey + bb, gz = (long long)N * ez + c;
+                            const size_t gi = (size_t)((gz * b.NY + gy) * b.PX + gx);
+                            M[gi] += w[a] * w[bb] * w[c] * det;
+                            // faces of the box (absorbing): surface element |dX/ds x dX/dt| at the node
+                            const int loc[3] = {a, bb, c};
+                            const int el[3] = {ex, ey, ez};
+                            for (int f = 0; f < 6; ++f) {
+                                if (g.bc[f] != SEM_BC_ABSORBING) continue;
+                                const int d = f / 2, side = f % 2;
+                                if (loc[d] != (side ? N : 0) || el[d] != (side ? g.nel[d] - 1 : 0)) continue;
+                                const int t0 = d == 0 ? 1 : 0, t1 = d == 2 ? 1 : 2;
+                                const double cx = J[1][t0] * J[2][t1] - J[2][t0] * J[1][t1];
+                                const double cy = J[2][t0] * J[0][t1] - J[0][t0] * J[2][t1];
+                                const double cz = J[0][t0] * J[1][t1] - J[1][t0] * J[0][t1];
+                                Cd[gi] += g.c * w[loc[t0]] * w[loc[t1]] * std::sqrt(cx * cx + cy * cy + cz * cz);
+                            }
+                        }
+    for (size_t i = 0; i < M.size(); ++i) {
+        if (M[i] > 0.0) {
+            Cd[i] /= M[i];
+            M[i] = 1.0 / M[i];
+        }
+    }
+    std::vector<double> V(verts, verts + 3 * n_verts);
+    if (upload(ctx, &b.vlat, V) || upload(ctx, &b.minv, M) || upload(ctx, &b.cdamp, Cd)) return SEM_E_CUDA;
+    if (dalloc(ctx, &b.res, (size_t)b.nalloc())) return SEM_E_OOM;
+    CU(cudaMemset(b.res, 0, (size_t)b.nalloc() * sizeof(double)));
+    b.curved = true;
+    drop_graphs(ctx);
+    CU(cudaStreamSynchronize(ctx->stream));
+    return SEM_OK;
+}
+
 sem_status sem_pml_attach(sem_ctx* ctx, int box, const double* thickness, double R) {
     sem_status st = check_ctx(ctx);
     if (st) return st;
@@ -1091,6 +1213,7 @@ sem_status sem_pml_attach(sem_ctx* ctx, int box, const double* thickness, double
         return fail(ctx, SEM_E_PARTITION, "the PML is implemented for a single slab (world 1) only");
     sem::Part& pt = ctx->parts[0];
     if (pt.pml.on) return fail(ctx, SEM_E_STATE, "PML already attached");
+    if (pt.boxes[box].curved) return fail(ctx, SEM_E_STATE, "PML on a curved box is not supported");
     Box& b = pt.boxes[box];
     const sem_box_desc& g = ctx->gdesc[box];
     for (int f = 0; f < 6; ++f)
@@ -1181,6 +1304,8 @@ sem_status sem_plane_wave_source(sem_ctx* ctx, int box, int face, double amp, do
         return fail(ctx, SEM_E_ARG, "plane wave: +z face of an existing box only");
     const sem_box_desc& g = ctx->gdesc[box];
     if (g.bc[5] != SEM_BC_ABSORBING) return fail(ctx, SEM_E_ARG, "plane wave needs an absorbing face");
+    for (auto& pt : ctx->parts)
+        if (pt.boxes[box].curved) return fail(ctx, SEM_E_STATE, "a plane wave on a curved box is not supported");
     const double nk = std::sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
     if (!(nk > 0) || !(sigma > 0)) return fail(ctx, SEM_E_ARG, "bad plane-wave parameters");
     sem::PlaneWave& pw = ctx->pw;

@@ -187,6 +187,24 @@ struct PmlParams {
     double c2, dt;
 };
 
+// Curved box: element-by-element K p with the geometric factors recomputed from
+// the 8 vertices at every GLL point (no stored metric terms), scatter-add, then a nodal update.
+struct CurvedParams {
+    int N;
+    long long NX, NY, NZ, PX;
+    int nelx, nely, nelz;
+    const double* __restrict__ vlat;
+    const double* __restrict__ P;    // p^{n+1}
+    double* res;
+    double* W;                       // w^n in, w^{n+1} out
+    double* Pn;                      // p^{n+2}
+    const double* __restrict__ minv;
+    const double* __restrict__ cdamp;
+    double D[kMaxN + 1][kMaxN + 1];  // D[i][j] = l_j'(x_i)
+    double x[kMaxN + 1], w[kMaxN + 1];
+    double c2, dt;
+};
+
 // One side of one slab cut for one box (partial rows before, fix-up after the exchange).
 struct CutParams {
     int side;                       // 0: cut at ix = 0 (neighbour on the left), 1: at ix = NX-1
@@ -227,6 +245,12 @@ struct Box {
     int iface_side = 0;
     double* tau = nullptr;  // interface outputs on this box's face lattice
     double* sig = nullptr;
+    // curved (trilinear vertex-lattice) box: element-scatter path (curved_residual/update kernels)
+    bool curved = false;
+    double* vlat = nullptr;   // vertex lattice [(nelx+1)(nely+1)(nelz+1)][3]
+    double* minv = nullptr;   // pitched: inverse assembled lumped mass
+    double* cdamp = nullptr;  // pitched: C_ii / M_ii on absorbing faces, 0 elsewhere
+    double* res = nullptr;    // pitched: assembled K p residual (atomics), cleared by the update
     long long ndof() const { return NX * NY * NZ; }
     long long nalloc() const { return PX * NY * NZ; }
 };
@@ -336,6 +360,8 @@ void launch_fill_random(double* p, double* w, double* pn, long long NX, long lon
                         double dt, cudaStream_t s);
 void launch_cut_partial(const CutParams& c, cudaStream_t s);
 void launch_pml_elements(const PmlParams& p, cudaStream_t s);
+void launch_curved(const CurvedParams& p, cudaStream_t s);
+void launch_step_bump(long long* step, cudaStream_t s);
 void launch_pml_fixup(const PmlParams& p, cudaStream_t s);
 void launch_cut_fixup(const CutParams& c, cudaStream_t s);
 void launch_set_state(const double* pprev, double* pcur, const double* w, long long NX, long long PX, long long rows,

@@ -70,6 +70,7 @@ def _load():
         "sem_plane_wave_source": [P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                                   C.POINTER(C.c_double)],
         "sem_pml_attach": [P, C.c_int, C.POINTER(C.c_double), C.c_double],
+        "sem_box_set_vertices": [P, C.c_int, C.POINTER(C.c_double), C.c_size_t],
         "sem_face_match": [C.c_int, C.POINTER(FaceSet), C.POINTER(FaceSet), C.c_int, C.c_double,
                            C.POINTER(C.c_longlong), C.POINTER(C.c_double), C.POINTER(C.c_double)],
         "sem_step": [P, C.c_int],
@@ -97,7 +98,7 @@ def _load():
 
 LIB = _load()
 EXPORTED = ("sem_mesh_create", "sem_nccl_unique_id", "sem_slab_plan", "sem_pmut_attach", "sem_dg_interface_build",
-            "sem_plane_wave_source", "sem_pml_attach", "sem_face_match",
+            "sem_plane_wave_source", "sem_pml_attach", "sem_face_match", "sem_box_set_vertices",
             "sem_step", "sem_sync", "sem_read_pressure", "sem_read_pressure_at", "sem_read_modal",
             "sem_write_state", "sem_fill_random_state", "sem_query", "sem_set_profiling", "sem_kernel_time",
             "sem_last_launch_count", "sem_last_error", "sem_destroy")
@@ -189,6 +190,11 @@ def sem_dg_interface_build(ctx, fine_box, coarse_box, penalty_alpha, quad_rule=0
 def sem_plane_wave_source(ctx, box, face, amp_pa, f0_hz, sigma_s, t0_s, direction):
     d = (C.c_double * 3)(*[float(v) for v in direction])
     _check(ctx, LIB.sem_plane_wave_source(ctx, box, face, amp_pa, f0_hz, sigma_s, t0_s, d))
+
+
+def sem_box_set_vertices(ctx, box, verts):
+    v = np.ascontiguousarray(verts, np.float64).reshape(-1, 3)
+    _check(ctx, LIB.sem_box_set_vertices(ctx, int(box), _dptr(v), v.shape[0]))
 
 
 def sem_pml_attach(ctx, box, thickness, R):
@@ -307,6 +313,9 @@ class Simulation:
         self.nn = [tuple(b["degree"] * n + 1 for n in b["nel"]) for b in rec["boxes"]]
         self.ndof = [a * b * c for a, b, c in self.nn]
         try:
+            for bi, b in enumerate(rec["boxes"]):
+                if b.get("vertices") is not None:
+                    sem_box_set_vertices(self.ctx, bi, b["vertices"])
             if rec.get("pmut") is not None:
                 sem_pmut_attach(self.ctx, rec["pmut"])
             if rec.get("interface") is not None:
