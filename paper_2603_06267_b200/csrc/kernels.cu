@@ -1254,9 +1254,9 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) curved_residual_k
 }
 
 __global__ void curved_update_kernel(const __grid_constant__ CurvedParams p) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= p.NX * p.NY * p.NZ) return;
-    const long long g = (i / p.NX) * p.PX + i % p.NX;
+    const long long ix = (long long)blockIdx.x * blockDim.x + threadIdx.x;   // 2D grid: x, lattice row
+    if (ix >= p.NX) return;
+    const long long g = (long long)blockIdx.y * p.PX + ix;
     const double wv = p.W[g];
     const double a = -p.minv[g] * p.res[g] - p.cdamp[g] * wv;
     p.res[g] = 0.0;
@@ -1274,8 +1274,7 @@ void launch_curved(const CurvedParams& p, cudaStream_t s) {
 #undef SEM_CV_CASE
         default: break;
     }
-    const long long n = p.NX * p.NY * p.NZ;
-    curved_update_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p);
+    curved_update_kernel<<<dim3((unsigned)((p.NX + 127) / 128), (unsigned)(p.NY * p.NZ)), 128, 0, s>>>(p);
 }
 
 __global__ void step_bump_kernel(long long* step) { *step += 1; }
