@@ -14,7 +14,7 @@ constexpr int kMaxN = 8;          // supported GLL degrees 1..8
 constexpr int kRows = kMaxN + 3;  // row classes per direction: R[0..N-1], L, B0, BN
 constexpr int kMaxModes = 8;
 #ifndef SEM_KPREF
-#define SEM_KPREF 12
+#define SEM_KPREF 16
 #endif
 constexpr int kPref = SEM_KPREF;  // volume kernel: planes prefetched beyond the z-stencil window
 
