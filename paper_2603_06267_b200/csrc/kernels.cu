@@ -427,7 +427,9 @@ __device__ __forceinline__ void vol_tile(const VolParams& p, unsigned char* ring
     const BoxTables& T = p.tab;
     VolThread<N> t;
     const long long ix = tx0 + lane, iy = ty0 + ly;
-    const bool node_lane = lane < G::TXE;
+    // node lanes: TXE per tile; the last tile in x takes one more node when that ends the box
+    const int txe_t = (NX - tx0 <= G::TXE + 1) ? (int)(NX - tx0) : G::TXE;
+    const bool node_lane = lane < txe_t;
     t.valid = node_lane && ix < NX && iy < NY;
     const int a = lane % N;
     int rxR = -1;
@@ -439,7 +441,9 @@ __device__ __forceinline__ void vol_tile(const VolParams& p, unsigned char* ring
         else if (ix < NX - 1) rxR = a;
         if (a == 0 && ix > 0) t.fL = (ix == NX - 1 && !p.cutR) ? 2.0 : 1.0;
     }
-    t.xb = (ly + N) * G::SW + (node_lane ? lane - a + G::NH : G::NH - N);
+    // the extra last node (lane TXE, a = 0, no right element: its x row is zero) reads its left element
+    // so that every shared-memory read stays inside the row
+    t.xb = (ly + N) * G::SW + (!node_lane ? G::NH - N : (lane == G::TXE ? lane - N + G::NH : lane - a + G::NH));
     const int ay = (int)(iy % N);
     int ryR = -1;
     t.yLs = 0.0;
@@ -687,7 +691,7 @@ void fill_tiles(VolLaunch& L) {
     for (int b = 0; b < L.nbox; ++b) {
         const VolParams& p = L.box[b];
         const int txe = vol_txe(p.N);
-        L.ntx[b] = (unsigned)((p.NX + txe - 1) / txe);
+        L.ntx[b] = (unsigned)((p.NX - 1 + txe - 1) / txe);   // the last tile may take TXE + 1 nodes
         L.nty[b] = (unsigned)((p.NY + kTY - 1) / kTY);
         L.ntiles[b] = L.ntx[b] * L.nty[b];
     }

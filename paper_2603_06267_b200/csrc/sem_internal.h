@@ -26,7 +26,9 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int vol_txe(int N) { return (N * (31 / N)) % 2 ? N * (31 / N) - N : N * (31 / N); }
 __host__ __device__ constexpr int vol_nh(int N) { return N + (N & 1); }
 __host__ __device__ constexpr int vol_pbox_w(int N) { return vol_txe(N) + 2 * vol_nh(N); }
-__host__ __device__ constexpr int vol_wbox_w(int N) { return vol_txe(N); }
+// W tile: TXE + 1 nodes (the last x tile of a box also takes the box's last node, so NX = k TXE + 1
+// needs k tiles, not k + 1), rounded up to an even count (TMA boxes are 16-byte multiples)
+__host__ __device__ constexpr int vol_wbox_w(int N) { return ((vol_txe(N) + 2) / 2) * 2; }
 // slot = [P tile | pad to 128 B | W tile | pad to 128 B]: TMA destinations must be 128 B aligned
 __host__ __device__ constexpr int vol_pbytes_aligned(int N, int TY) {
     return ((vol_pbox_w(N) * (TY + 2 * N) * 8 + 127) / 128) * 128;
