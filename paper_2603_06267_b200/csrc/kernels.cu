@@ -661,7 +661,9 @@ struct VolInst {
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         }
         const unsigned ntot = L.ntiles[0] + (N1 ? L.ntiles[1] : 0u);
-        unsigned grid = (unsigned)(nsm * ctas_per_sm());
+        // SMs left free for a concurrent NCCL exchange (its kernel could not co-reside with a volume CTA)
+        const int nsm_use = nsm - L.reserve_sms > 1 ? nsm - L.reserve_sms : 1;
+        unsigned grid = (unsigned)(nsm_use * ctas_per_sm());
         if (grid > ntot) grid = ntot;
         vol_kernel<N0, N1, kTY><<<grid, dim3(32, kTY + 1), smem(), s>>>(L);
     }
@@ -1028,7 +1030,9 @@ void launch_fill_random(double* pprev, double* w, double* pcur, long long NX, lo
 // exchange.  A shared cut node's x row is R0 (right slab) + L (left slab); each
 // slab evaluates its own part inside vol_kernel and sends it to the neighbour, which adds it here.
 // ------------------------------------------------------------------------------------------------
-__global__ void cut_partial_kernel(const CutParams c) {
+// One launch per phase for all (side, box) pairs of a slab: blockIdx.y selects the CutParams.
+__global__ void cut_partial_kernel(const __grid_constant__ CutBatch B) {
+    const CutParams& c = B.c[blockIdx.y];
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long n = c.NY * c.NZ;
     if (i < n) {
@@ -1045,7 +1049,8 @@ __global__ void cut_partial_kernel(const CutParams c) {
     }
 }
 
-__global__ void cut_fixup_kernel(const CutParams c) {
+__global__ void cut_fixup_kernel(const __grid_constant__ CutBatch B) {
+    const CutParams& c = B.c[blockIdx.y];
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long n = c.NY * c.NZ;
     if (i >= n) return;
@@ -1059,14 +1064,21 @@ __global__ void cut_fixup_kernel(const CutParams c) {
     c.Pn[d] = fma(c.dt, dw, c.Pn[d]);
 }
 
-void launch_cut_partial(const CutParams& c, cudaStream_t s) {
-    const long long n = c.NY * c.NZ + c.NYt;
-    cut_partial_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c);
+static unsigned cut_blocks(const CutBatch& B, bool partial) {
+    long long m = 0;
+    for (int k = 0; k < B.n; ++k) {
+        const long long n = B.c[k].NY * B.c[k].NZ + (partial ? B.c[k].NYt : 0);
+        if (n > m) m = n;
+    }
+    return (unsigned)((m + 255) / 256);
 }
 
-void launch_cut_fixup(const CutParams& c, cudaStream_t s) {
-    const long long n = c.NY * c.NZ;
-    cut_fixup_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c);
+void launch_cut_partial(const CutBatch& B, cudaStream_t s) {
+    if (B.n > 0) cut_partial_kernel<<<dim3(cut_blocks(B, true), B.n), 256, 0, s>>>(B);
+}
+
+void launch_cut_fixup(const CutBatch& B, cudaStream_t s) {
+    if (B.n > 0) cut_fixup_kernel<<<dim3(cut_blocks(B, false), B.n), 256, 0, s>>>(B);
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -494,6 +494,14 @@ sem::CurvedParams curved_params(sem_ctx* ctx, Box& b, int cur) {
     return p;
 }
 
+sem::CutBatch cut_batch(sem_ctx* ctx, sem::Part& pt, int cur) {
+    sem::CutBatch B{};
+    for (int side = 0; side < 2; ++side)
+        if (side == 0 ? pt.cutL : pt.cutR)
+            for (int bi = 0; bi < (int)pt.boxes.size() && B.n < 4; ++bi) B.c[B.n++] = cut_params(ctx, pt, side, bi, cur);
+    return B;
+}
+
 sem::PmlParams pml_params(sem_ctx* ctx, sem::Part& pt, int cur) {
     sem::PmlBox& m = pt.pml;
     Box& b = pt.boxes[m.box];
@@ -600,13 +608,11 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
     if (fork) cudaStreamWaitEvent(s, ctx->ev_mjoin, 0);
     const bool slabs = ctx->world > 1;
     if (slabs) {
-        for (auto& pt : ctx->parts)
-            for (int side = 0; side < 2; ++side)
-                if (side == 0 ? pt.cutL : pt.cutR)
-                    for (int bi = 0; bi < (int)pt.boxes.size(); ++bi) {
-                        sem::launch_cut_partial(cut_params(ctx, pt, side, bi, cur), s);
-                        ++nl;
-                    }
+        for (auto& pt : ctx->parts) {
+            sem::CutBatch B = cut_batch(ctx, pt, cur);
+            sem::launch_cut_partial(B, s);
+            nl += B.n ? 1 : 0;
+        }
         if (ctx->emulate) {   // device copies between the slabs of this context
             for (size_t r = 0; r < ctx->parts.size(); ++r) {
                 sem::Part& pt = ctx->parts[r];
@@ -660,6 +666,9 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
             ls[i].sched = ctx->d_sched + 2 * (i % sem_ctx::kSchedPairs);
             ls[i].step = ctx->d_step;
             ls[i].bump_step = i + 1 == ls.size() ? 1 : 0;
+            // NCCL's send/recv kernel cannot co-reside with a volume CTA (smem, registers): keep a few SMs
+            // free so the cut-plane exchange overlaps the volume launch instead of waiting for its end
+            ls[i].reserve_sms = nccl_mode(ctx) ? 4 : 0;
             sem::launch_volume(ls[i], s);
             ++nl;
         }
@@ -678,13 +687,11 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
     mark(0, false, s);
     if (slabs) {
         if (!ctx->emulate) cudaStreamWaitEvent(s, ctx->ev_join, 0);
-        for (auto& pt : ctx->parts)
-            for (int side = 0; side < 2; ++side)
-                if (side == 0 ? pt.cutL : pt.cutR)
-                    for (int bi = 0; bi < (int)pt.boxes.size(); ++bi) {
-                        sem::launch_cut_fixup(cut_params(ctx, pt, side, bi, cur), s);
-                        ++nl;
-                    }
+        for (auto& pt : ctx->parts) {
+            sem::CutBatch B = cut_batch(ctx, pt, cur);
+            sem::launch_cut_fixup(B, s);
+            nl += B.n ? 1 : 0;
+        }
     }
     for (auto& pt : ctx->parts)
         if (pt.pml.on) {

@@ -109,6 +109,7 @@ struct VolLaunch {
     unsigned int* sched;            // [0] next tile, [1] finished CTAs; reset by the launch's last CTA
     long long* step;                // device step counter, bumped by the last CTA if bump_step
     int bump_step;                  // 1 for the last volume launch of a step
+    int reserve_sms;                // SMs kept free (NCCL exchange running beside the launch)
 };
 
 struct ModalParams {
@@ -224,6 +225,12 @@ struct CutParams {
     double ktau[kMaxN + 1], ksig[kMaxN + 1];
     double* out;                    // send buffer: [NY*NZ plane][NYt tau][NYt sigma]
     const double* in;               // receive buffer, same layout
+};
+
+// all cut (side, box) pairs of one slab, handled by one launch per phase
+struct CutBatch {
+    CutParams c[4];
+    int n;
 };
 
 struct Box {
@@ -360,12 +367,12 @@ void launch_iface(const IfaceParams& p, cudaStream_t s);
 void launch_fill_random(double* p, double* w, double* pn, long long NX, long long PX, long long rows,
                         long long gx0, long long NXg, unsigned long long seed, int box, double ps, double vs,
                         double dt, cudaStream_t s);
-void launch_cut_partial(const CutParams& c, cudaStream_t s);
+void launch_cut_partial(const CutBatch& B, cudaStream_t s);
 void launch_pml_elements(const PmlParams& p, cudaStream_t s);
 void launch_curved(const CurvedParams& p, cudaStream_t s);
 void launch_step_bump(long long* step, cudaStream_t s);
 void launch_pml_fixup(const PmlParams& p, cudaStream_t s);
-void launch_cut_fixup(const CutParams& c, cudaStream_t s);
+void launch_cut_fixup(const CutBatch& B, cudaStream_t s);
 void launch_set_state(const double* pprev, double* pcur, const double* w, long long NX, long long PX, long long rows,
                       double dt, cudaStream_t s);
 void launch_gather(const double* src, const long long* idx, long long n, double* out, cudaStream_t s);
