@@ -434,12 +434,10 @@ __device__ __forceinline__ void vol_tile(const VolParams& p, unsigned char* ring
     const int a = lane % N;
     int rxR = -1;
     t.fL = 0.0;
-    if (t.valid) {
-        // box faces: B0 = 2 R0 / BN = 2 L; slab cuts (multi-GPU): the shared node keeps its interior
-        // rows R0 (right side) / L (left side) and the other side's part is added by cut_fixup_kernel
-        if (ix == 0) rxR = p.cutL ? 0 : row_B0(N);
+    if (t.valid) {   // box faces: B0 = 2 R0 / BN = 2 L
+        if (ix == 0) rxR = row_B0(N);
         else if (ix < NX - 1) rxR = a;
-        if (a == 0 && ix > 0) t.fL = (ix == NX - 1 && !p.cutR) ? 2.0 : 1.0;
+        if (a == 0 && ix > 0) t.fL = (ix == NX - 1) ? 2.0 : 1.0;
     }
     // the extra last node (lane TXE, a = 0, no right element: its x row is zero) reads its left element
     // so that every shared-memory read stays inside the row
@@ -448,9 +446,12 @@ __device__ __forceinline__ void vol_tile(const VolParams& p, unsigned char* ring
     int ryR = -1;
     t.yLs = 0.0;
     if (iy < NY) {
-        if (iy == 0) ryR = row_B0(N);
+        // box faces: B0 = 2 R0 / BN = 2 L; slab cuts (multi-GPU, y-slabs): the shared node keeps its
+        // interior rows R0 (upper side) / L (lower side) and the other side's part is added by
+        // cut_fixup_kernel after the exchange
+        if (iy == 0) ryR = p.cutL ? 0 : row_B0(N);
         else if (iy < NY - 1) ryR = ay;
-        if (ay == 0 && iy > 0) t.yLs = (iy == NY - 1) ? 2.0 * p.sdir[1] : p.sdir[1];
+        if (ay == 0 && iy > 0) t.yLs = (iy == NY - 1 && !p.cutR) ? 2.0 * p.sdir[1] : p.sdir[1];
     }
     t.fL *= p.sdir[0];
 #pragma unroll
@@ -951,7 +952,8 @@ __global__ void __launch_bounds__(256) iface_gather_y(const __grid_constant__ If
     if (id >= NXf * (int)p.NYc) return;
     const int ix = id % NXf, jy = id / NXf;
     double s1, s2;
-    gather_1d<NF, NC, R>(p, jy, p.nelcy, (int)p.NYf, p.tauf + ix, p.sigf + ix, NXf, p.myf, 0, s1, s2);
+    // the fine cut line iy = 0 of a slab with a lower cut is counted by the lower slab only
+    gather_1d<NF, NC, R>(p, jy, p.nelcy, (int)p.NYf, p.tauf + ix, p.sigf + ix, NXf, p.myf, p.skip_iy0, s1, s2);
     const double mx = __ldg(p.mxf + ix);
     p.h1[id] = -mx * s1;
     p.h2[id] = (p.cc2 / p.cf2) * mx * s2;
@@ -964,8 +966,7 @@ __global__ void __launch_bounds__(256) iface_gather_x(const __grid_constant__ If
     if (id >= NXc * (int)p.NYc) return;
     const int jx = id % NXc, jy = id / NXc;
     double s1, s2;
-    // the fine cut line ix = 0 of a slab with a left cut is counted by the left slab only
-    gather_1d<NF, NC, R>(p, jx, p.nelcx, NXf, p.h1 + jy * NXf, p.h2 + jy * NXf, 1, nullptr, p.skip_ix0, s1, s2);
+    gather_1d<NF, NC, R>(p, jx, p.nelcx, NXf, p.h1 + jy * NXf, p.h2 + jy * NXf, 1, nullptr, 0, s1, s2);
     const double inv = 1.0 / (p.mxc[jx] * p.myc[jy]);
     p.tauc[id] = s1 * inv;
     p.sigc[id] = s2 * inv;
@@ -1003,13 +1004,13 @@ __device__ __forceinline__ double cb_uniform(unsigned long long seed, int box, i
     return 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
 }
 
-__global__ void fill_random_kernel(double* pprev, double* w, double* pcur, long long NX, long long PX, long long rows,
-                                   long long gx0, long long NXg, unsigned long long seed, int box, double ps,
-                                   double vs, double dt) {
+__global__ void fill_random_kernel(double* pprev, double* w, double* pcur, long long NX, long long PX, long long NY,
+                                   long long NZ, long long gy0, long long NYg, unsigned long long seed, int box,
+                                   double ps, double vs, double dt) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= NX * rows) return;
-    const long long ix = i % NX, r = i / NX, d = r * PX + ix;
-    const long long gid = (ix + gx0) + NXg * r;   // global lexicographic id (slab-independent field)
+    if (i >= NX * NY * NZ) return;
+    const long long ix = i % NX, r = i / NX, iy = r % NY, iz = r / NY, d = r * PX + ix;
+    const long long gid = ix + NX * ((iy + gy0) + NYg * iz);   // global lexicographic id (slab-independent field)
     const double p0 = ps * cb_uniform(seed, box, 0, gid);
     const double v0 = vs * cb_uniform(seed, box, 1, gid);
     pprev[d] = p0;
@@ -1017,48 +1018,50 @@ __global__ void fill_random_kernel(double* pprev, double* w, double* pcur, long 
     pcur[d] = p0 + dt * v0;     // p^1 = p^0 + dt p'^0 (+ dt^2/2 p''^0 = 0)
 }
 
-void launch_fill_random(double* pprev, double* w, double* pcur, long long NX, long long PX, long long rows,
-                        long long gx0, long long NXg, unsigned long long seed, int box, double ps, double vs, double dt,
+void launch_fill_random(double* pprev, double* w, double* pcur, long long NX, long long PX, long long NY, long long NZ,
+                        long long gy0, long long NYg, unsigned long long seed, int box, double ps, double vs, double dt,
                         cudaStream_t s) {
-    const long long n = NX * rows;
-    fill_random_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pprev, w, pcur, NX, PX, rows, gx0, NXg, seed, box,
-                                                                   ps, vs, dt);
+    const long long n = NX * NY * NZ;
+    fill_random_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pprev, w, pcur, NX, PX, NY, NZ, gy0, NYg, seed,
+                                                                   box, ps, vs, dt);
 }
 
 // ------------------------------------------------------------------------------------------------
-// Slab decomposition along x (multi-GPU): partial rows at the cut planes and the fix-up after the
+// Slab decomposition along y (multi-GPU): partial rows at the cut planes and the fix-up after the
 // exchange.  A shared cut node's x row is R0 (right slab) + L (left slab); each
 // slab evaluates its own part inside vol_kernel and sends it to the neighbour, which adds it here.
 // ------------------------------------------------------------------------------------------------
-// One launch per phase for all (side, box) pairs of a slab: blockIdx.y selects the CutParams.
+// One launch per phase for all (side, box) pairs of a slab: blockIdx.y selects the CutParams.  The cut
+// plane iy = const is, per z-plane, a contiguous lattice row: one thread per (ix, iz), coalesced.
 __global__ void cut_partial_kernel(const __grid_constant__ CutBatch B) {
     const CutParams& c = B.c[blockIdx.y];
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long n = c.NY * c.NZ;
+    const long long n = c.NX * c.NZ;
     if (i < n) {
-        const long long iy = i % c.NY, iz = i / c.NY;
-        const double* col = c.P + (iz * c.NY + iy) * c.PX + (c.side ? c.NX - 1 - c.N : 0);
+        const long long ix = i % c.NX, iz = i / c.NX;
+        const long long y0 = c.side ? c.NY - 1 - c.N : 0;
+        const double* col = c.P + (iz * c.NY + y0) * c.PX + ix;
         double s = 0.0;
-        for (int b = 0; b <= c.N; ++b) s = fma(c.row[b], col[b], s);
+        for (int b = 0; b <= c.N; ++b) s = fma(c.row[b], col[(long long)b * c.PX], s);
         c.out[i] = s;
-    } else if (i < n + c.NYt) {   // coarse SIPG partial sums at the cut column
-        const long long jy = i - n;
-        const long long jx = c.side ? c.NXt - 1 : 0;
-        c.out[n + jy] = c.tau[jy * c.NXt + jx];
-        c.out[n + c.NYt + jy] = c.sig[jy * c.NXt + jx];
+    } else if (i < n + c.NXt) {   // coarse SIPG partial sums at the cut row of the face lattice
+        const long long jx = i - n;
+        const long long jy = c.side ? c.NYt - 1 : 0;
+        c.out[n + jx] = c.tau[jy * c.NXt + jx];
+        c.out[n + c.NXt + jx] = c.sig[jy * c.NXt + jx];
     }
 }
 
 __global__ void cut_fixup_kernel(const __grid_constant__ CutBatch B) {
     const CutParams& c = B.c[blockIdx.y];
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long n = c.NY * c.NZ;
+    const long long n = c.NX * c.NZ;
     if (i >= n) return;
-    const long long iy = i % c.NY, iz = i / c.NY;
+    const long long ix = i % c.NX, iz = i / c.NX;
     double da = -c.in[i];
-    if (c.NYt > 0 && iz <= c.N)   // coarse-side SIPG layer terms of the neighbour's fine points
-        da -= c.in[n + iy] * c.ktau[iz] + c.in[n + c.NYt + iy] * c.ksig[iz];
-    const long long d = (iz * c.NY + iy) * c.PX + (c.side ? c.NX - 1 : 0);
+    if (c.NXt > 0 && iz <= c.N)   // coarse-side SIPG layer terms of the neighbour's fine points
+        da -= c.in[n + ix] * c.ktau[iz] + c.in[n + c.NXt + ix] * c.ksig[iz];
+    const long long d = (iz * c.NY + (c.side ? c.NY - 1 : 0)) * c.PX + ix;
     const double dw = c.dt * da;
     c.W[d] += dw;
     c.Pn[d] = fma(c.dt, dw, c.Pn[d]);
@@ -1067,7 +1070,7 @@ __global__ void cut_fixup_kernel(const __grid_constant__ CutBatch B) {
 static unsigned cut_blocks(const CutBatch& B, bool partial) {
     long long m = 0;
     for (int k = 0; k < B.n; ++k) {
-        const long long n = B.c[k].NY * B.c[k].NZ + (partial ? B.c[k].NYt : 0);
+        const long long n = B.c[k].NX * B.c[k].NZ + (partial ? B.c[k].NXt : 0);
         if (n > m) m = n;
     }
     return (unsigned)((m + 255) / 256);

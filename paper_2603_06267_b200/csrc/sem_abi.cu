@@ -289,35 +289,37 @@ NcclApi& nccl_api() {
 bool nccl_mode(const sem_ctx* ctx) { return ctx->world > 1 && !ctx->emulate; }
 
 // ---- partition rules (shared by sem_mesh_create / sem_pmut_attach / sem_dg_interface_build and the
-//      host-only sem_slab_plan): G equal x-slabs of every box, cuts at the same x for all boxes
+//      host-only sem_slab_plan): G equal y-slabs of every box, cuts at the same y for all boxes.
+//      y (not x): a cut plane iy = const is, per z-plane, one contiguous lattice row, so the cut-plane
+//      partial rows and fix-ups are coalesced (an x cut touches one node per row).
 const char* slabs_divisible(const sem_box_desc* boxes, int n, int G) {
     for (int i = 0; i < n; ++i)
-        if (boxes[i].nel[0] % G) return "nel_x of every box must be divisible by the number of slabs";
+        if (boxes[i].nel[1] % G) return "nel_y of every box must be divisible by the number of slabs";
     return nullptr;
 }
 
-// slab owning a membrane spanning [x0, x0 + a] on box g; -1 if a cut crosses or touches it (membranes
+// slab owning a membrane spanning [y0, y0 + a] on box g; -1 if a cut crosses or touches it (membranes
 // are never split across GPUs: the paper's membrane-preserving partition)
-int membrane_slab(const sem_box_desc& g, int G, double x0, double a) {
-    const double hx = g.extent[0] / g.nel[0];
+int membrane_slab(const sem_box_desc& g, int G, double y0, double a) {
+    const double hy = g.extent[1] / g.nel[1];
     int slab = 0;
     for (int r = 1; r < G; ++r) {
-        const double cut = g.origin[0] + hx * (double)(g.nel[0] / G) * r;
-        if (x0 <= cut + 1e-9 * hx && x0 + a >= cut - 1e-9 * hx) return -1;
-        if (x0 > cut) slab = r;
+        const double cut = g.origin[1] + hy * (double)(g.nel[1] / G) * r;
+        if (y0 <= cut + 1e-9 * hy && y0 + a >= cut - 1e-9 * hy) return -1;
+        if (y0 > cut) slab = r;
     }
     return slab;
 }
 
 // cuts must fall on coarse-element boundaries so every 2:1 interface face pair is slab-local
 bool interface_aligned(const sem_box_desc& F, const sem_box_desc& C, int G) {
-    const int R = F.nel[0] / C.nel[0];
-    return R >= 1 && (F.nel[0] / G) % R == 0;
+    const int R = F.nel[1] / C.nel[1];
+    return R >= 1 && (F.nel[1] / G) % R == 0;
 }
 
-// Slab `slab` of global box g: elements [ex0, ex0 + nel_loc) along x.  1D tables (coordinates, face
-// masses) are taken from the global lattice, so a cut node keeps its interior (two-sided) mass.
-Box make_slab(const sem_box_desc& g, long long ex0, long long nel_loc, bool cutL, bool cutR) {
+// Slab of global box g: elements [ey0, ey0 + nel_loc) along y.  1D tables (coordinates, face masses)
+// are taken from the global lattice, so a cut node keeps its interior (two-sided) mass.
+Box make_slab(const sem_box_desc& g, long long ey0, long long nel_loc, bool cutL, bool cutR) {
     Box gb;
     gb.d = g;
     gb.N = g.degree;
@@ -327,19 +329,19 @@ Box make_slab(const sem_box_desc& g, long long ex0, long long nel_loc, bool cutL
     for (int k = 0; k < 3; ++k) gb.h[k] = g.extent[k] / g.nel[k];
     build_tables(gb);
     Box b = gb;
-    b.d.origin[0] = g.origin[0] + gb.h[0] * (double)ex0;
-    b.d.extent[0] = gb.h[0] * (double)nel_loc;
-    b.d.nel[0] = (int)nel_loc;
-    if (cutL) b.d.bc[0] = SEM_BC_RIGID;
-    if (cutR) b.d.bc[1] = SEM_BC_RIGID;
-    b.NX = (long long)b.N * nel_loc + 1;
+    b.d.origin[1] = g.origin[1] + gb.h[1] * (double)ey0;
+    b.d.extent[1] = gb.h[1] * (double)nel_loc;
+    b.d.nel[1] = (int)nel_loc;
+    if (cutL) b.d.bc[2] = SEM_BC_RIGID;
+    if (cutR) b.d.bc[3] = SEM_BC_RIGID;
+    b.NY = (long long)b.N * nel_loc + 1;
     b.PX = (b.NX + 7) / 8 * 8;
-    b.gx0 = (long long)b.N * ex0;
-    b.NXg = gb.NX;
+    b.gy0 = (long long)b.N * ey0;
+    b.NYg = gb.NY;
     b.cutL = cutL;
     b.cutR = cutR;
-    b.xh.assign(gb.xh.begin() + b.gx0, gb.xh.begin() + b.gx0 + b.NX);
-    b.mxh.assign(gb.mxh.begin() + b.gx0, gb.mxh.begin() + b.gx0 + b.NX);
+    b.yh.assign(gb.yh.begin() + b.gy0, gb.yh.begin() + b.gy0 + b.NY);
+    b.myh.assign(gb.myh.begin() + b.gy0, gb.myh.begin() + b.gy0 + b.NY);
     return b;
 }
 
@@ -433,7 +435,7 @@ sem::ModalParams modal_params(sem_ctx* ctx, sem::Part& pt, int cur) {
     return p;
 }
 
-// partial rows (side 0: this slab's first plane, R0 row; side 1: last plane, L row) of box bi
+// partial rows (side 0: this slab's first y plane, R0 row; side 1: last y plane, L row) of box bi
 sem::CutParams cut_params(sem_ctx* ctx, sem::Part& pt, int side, int bi, int cur) {
     Box& b = pt.boxes[bi];
     sem::CutParams c{};
@@ -447,9 +449,9 @@ sem::CutParams cut_params(sem_ctx* ctx, sem::Part& pt, int side, int bi, int cur
     c.Pn = b.P[1 - cur];
     c.W = b.W;
     const int row = side == 0 ? 0 : sem::row_L(b.N);
-    for (int k = 0; k <= b.N; ++k) c.row[k] = b.tab.G[0][row][k];
+    for (int k = 0; k <= b.N; ++k) c.row[k] = b.tab.G[1][row][k];   // y rows (scaled by c^2 (2/h_y)^2)
     c.dt = ctx->dt;
-    if (b.iface_side < 0) {   // coarse box of the interface: SIPG partials travel with it
+    if (b.iface_side < 0) {   // coarse box of the interface: SIPG partials (one face-lattice row) travel with it
         c.NXt = b.NX;
         c.NYt = b.NY;
         c.tau = b.tau;
@@ -743,13 +745,37 @@ sem_status check_ctx(sem_ctx* ctx) {
     return SEM_OK;
 }
 
-// owner slab of global lattice column gx of box bi (a shared cut column belongs to the left slab)
-int owner_part(sem_ctx* ctx, int bi, long long gx) {
+// owner slab of global lattice row gy of box bi (a shared cut row belongs to the lower slab)
+int owner_part(sem_ctx* ctx, int bi, long long gy) {
     for (size_t r = 0; r < ctx->parts.size(); ++r) {
         const Box& b = ctx->parts[r].boxes[bi];
-        if (gx >= b.gx0 && gx < b.gx0 + b.NX) return (int)r;
+        if (gy >= b.gy0 && gy < b.gy0 + b.NY) return (int)r;
     }
     return -1;
+}
+
+// One y-slab (rows y_skip .. NY-1 of every z-plane) between the pitched device layout and the
+// lexicographic host layout of the global box (x fastest), as one 3D copy.
+cudaError_t copy_slab(double* host, double* dev, const Box& b, long long NYg, long long gy0, long long y_skip,
+                      bool to_host, cudaStream_t s) {
+    cudaMemcpy3DParms m = {};
+    const cudaPitchedPtr hp = make_cudaPitchedPtr(host, (size_t)b.NX * 8, (size_t)b.NX * 8, (size_t)NYg);
+    const cudaPitchedPtr dp = make_cudaPitchedPtr(dev, (size_t)b.PX * 8, (size_t)b.NX * 8, (size_t)b.NY);
+    m.extent = make_cudaExtent((size_t)b.NX * 8, (size_t)(b.NY - y_skip), (size_t)b.NZ);
+    if (to_host) {
+        m.srcPtr = dp;
+        m.srcPos = make_cudaPos(0, (size_t)y_skip, 0);
+        m.dstPtr = hp;
+        m.dstPos = make_cudaPos(0, (size_t)(gy0 + y_skip), 0);
+        m.kind = cudaMemcpyDeviceToHost;
+    } else {
+        m.srcPtr = hp;
+        m.srcPos = make_cudaPos(0, (size_t)(gy0 + y_skip), 0);
+        m.dstPtr = dp;
+        m.dstPos = make_cudaPos(0, (size_t)y_skip, 0);
+        m.kind = cudaMemcpyHostToDevice;
+    }
+    return cudaMemcpy3DAsync(&m, s);
 }
 
 sem_status setup_part_buffers(sem_ctx* ctx, sem::Part& pt) {
@@ -770,12 +796,12 @@ sem_status setup_part_buffers(sem_ctx* ctx, sem::Part& pt) {
             !make_map(&b.tmW, b.W, b, sem::vol_wbox_w(b.N), TY))
             return fail(ctx, SEM_E_CUDA, "cuTensorMapEncodeTiled failed");
     }
-    // exchange buffers: per box one NY x NZ plane (+ 2 NY for the coarse SIPG column, sized always)
+    // exchange buffers: per box one NX x NZ cut plane (+ 2 NX for the coarse SIPG row, sized always)
     pt.xoff.clear();
     long long off = 0;
     for (auto& b : pt.boxes) {
         pt.xoff.push_back(off);
-        off += b.NY * b.NZ + 2 * b.NY;
+        off += b.NX * b.NZ + 2 * b.NX;
     }
     pt.xcount = off;
     for (int s = 0; s < 2; ++s) {
@@ -810,11 +836,11 @@ sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, cons
     if (pm) {
         if (pm->box < 0 || pm->box >= n_boxes || !pm->center) return SEM_E_ARG;
         for (int k = 0; k < pm->n_pmut; ++k)
-            if (membrane_slab(boxes[pm->box], world, pm->center[2 * k] - 0.5 * pm->side, pm->side) < 0)
+            if (membrane_slab(boxes[pm->box], world, pm->center[2 * k + 1] - 0.5 * pm->side, pm->side) < 0)
                 return SEM_E_PARTITION;
     }
     if (slab_x0)
-        for (int r = 0; r <= world; ++r) slab_x0[r] = (long long)(boxes[0].nel[0] / world) * r;
+        for (int r = 0; r <= world; ++r) slab_x0[r] = (long long)(boxes[0].nel[1] / world) * r;
     return SEM_OK;
 }
 
@@ -853,7 +879,7 @@ sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
         ctx->gNY.push_back((long long)g.degree * g.nel[1] + 1);
         ctx->gNZ.push_back((long long)g.degree * g.nel[2] + 1);
     }
-    // slab decomposition along x: equal element counts per slab, the same slab boundaries for all
+    // slab decomposition along y: equal element counts per slab, the same slab boundaries for all
     // boxes (box b's element count must be a multiple of the world size)
     const int G = ctx->world;
     if (const char* why = slabs_divisible(ctx->gdesc.data(), (int)ctx->gdesc.size(), G)) {
@@ -868,7 +894,7 @@ sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
         pt.cutL = r > 0;
         pt.cutR = r < G - 1;
         for (auto& g : ctx->gdesc) {
-            const long long nloc = g.nel[0] / G;
+            const long long nloc = g.nel[1] / G;
             pt.boxes.push_back(make_slab(g, nloc * r, nloc, pt.cutL, pt.cutR));
         }
         ctx->parts.push_back(pt);
@@ -933,7 +959,7 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
         if (x0 < g.origin[0] - 1e-12 * a || y0 < g.origin[1] - 1e-12 * a ||
             x0 + a > g.origin[0] + g.extent[0] + 1e-12 * a || y0 + a > g.origin[1] + g.extent[1] + 1e-12 * a)
             return fail(ctx, SEM_E_ARG, "membrane off the face");
-        const int slab = membrane_slab(g, G, x0, a);
+        const int slab = membrane_slab(g, G, y0, a);
         if (slab < 0) return fail(ctx, SEM_E_PARTITION, "a slab cut crosses a membrane");
         ctx->pm_lists[slab].push_back(k);
     }
@@ -1096,7 +1122,7 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
         p.gamma = gamma;
         p.cf2 = gF.c * gF.c;
         p.cc2 = gC.c * gC.c;
-        p.skip_ix0 = F.cutL ? 1 : 0;
+        p.skip_iy0 = F.cutL ? 1 : 0;
         for (int c = 0; c <= Nf; ++c) p.dfT[c] = (2.0 / hF[2]) * Df[Nf * (Nf + 1) + c];
         for (int c = 0; c <= Nc; ++c) p.dcB[c] = (2.0 / hC[2]) * Dc[0 * (Nc + 1) + c];
         double* dI = nullptr;
@@ -1404,12 +1430,12 @@ sem_status sem_read_pressure(sem_ctx* ctx, int box, double* host, size_t n) {
     const long long NXg = ctx->gNX[box], rows = ctx->gNY[box] * ctx->gNZ[box];
     const bool receiver = !nccl_mode(ctx) || ctx->rank == 0;
     if (receiver && (!host || n != (size_t)(NXg * rows))) return fail(ctx, SEM_E_ARG, "n must equal the box node count");
+    const long long NYg = ctx->gNY[box];
     if (!nccl_mode(ctx)) {
         for (auto& pt : ctx->parts) {
             Box& b = pt.boxes[box];
-            const long long skip = b.cutL ? 1 : 0;   // the shared cut column is reported by the left slab
-            CU(cudaMemcpy2DAsync(host + b.gx0 + skip, NXg * 8, b.P[1 - ctx->cur] + skip, b.PX * 8,
-                                 (b.NX - skip) * 8, rows, cudaMemcpyDeviceToHost, ctx->stream));
+            const long long skip = b.cutL ? 1 : 0;   // the shared cut row is reported by the lower slab
+            CU(copy_slab(host, b.P[1 - ctx->cur], b, NYg, b.gy0, skip, true, ctx->stream));
         }
         CU(cudaStreamSynchronize(ctx->stream));
         return SEM_OK;
@@ -1422,15 +1448,13 @@ sem_status sem_read_pressure(sem_ctx* ctx, int box, double* host, size_t n) {
         CU(cudaStreamSynchronize(ctx->stream));
         return SEM_OK;
     }
-    CU(cudaMemcpy2DAsync(host, NXg * 8, mine.P[1 - ctx->cur], mine.PX * 8, mine.NX * 8, rows, cudaMemcpyDeviceToHost,
-                         ctx->stream));
+    CU(copy_slab(host, mine.P[1 - ctx->cur], mine, NYg, mine.gy0, 0, true, ctx->stream));
     double* tmp = nullptr;
     CU(cudaMallocAsync(&tmp, (size_t)mine.nalloc() * 8, ctx->stream));
     for (int r = 1; r < ctx->world; ++r) {
-        const long long gx0 = mine.NX - 1 + (long long)(mine.NX - 1) * (r - 1);   // equal slabs
+        const long long gy0 = (mine.NY - 1) * (long long)r;   // equal slabs
         NC(api.recv(tmp, (size_t)mine.nalloc(), kNcclDouble, r, ctx->nccl, ctx->stream));
-        CU(cudaMemcpy2DAsync(host + gx0 + 1, NXg * 8, tmp + 1, mine.PX * 8, (mine.NX - 1) * 8, rows,
-                             cudaMemcpyDeviceToHost, ctx->stream));
+        CU(copy_slab(host, tmp, mine, NYg, gy0, 1, true, ctx->stream));
     }
     CU(cudaFreeAsync(tmp, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
@@ -1443,14 +1467,14 @@ sem_status sem_read_pressure_at(sem_ctx* ctx, int box, const long long* ids, siz
     if (box < 0 || box >= (int)ctx->gdesc.size() || (n && (!ids || !out))) return fail(ctx, SEM_E_ARG, "bad args");
     if (nccl_mode(ctx)) return fail(ctx, SEM_E_STATE, "sampled readout is single-process only (world 1 or emulated)");
     if (n == 0) return SEM_OK;
-    const long long NXg = ctx->gNX[box], total = NXg * ctx->gNY[box] * ctx->gNZ[box];
+    const long long NXg = ctx->gNX[box], NYg = ctx->gNY[box], total = NXg * NYg * ctx->gNZ[box];
     std::vector<std::vector<long long>> idx(ctx->parts.size()), pos(ctx->parts.size());
     for (size_t i = 0; i < n; ++i) {
         if (ids[i] < 0 || ids[i] >= total) return fail(ctx, SEM_E_ARG, "node id out of range");
-        const long long gx = ids[i] % NXg, row = ids[i] / NXg;
-        const int r = owner_part(ctx, box, gx);
+        const long long gx = ids[i] % NXg, row = ids[i] / NXg, gy = row % NYg, gz = row / NYg;
+        const int r = owner_part(ctx, box, gy);
         const Box& b = ctx->parts[r].boxes[box];
-        idx[r].push_back(row * b.PX + (gx - b.gx0));
+        idx[r].push_back((gz * b.NY + (gy - b.gy0)) * b.PX + gx);
         pos[r].push_back((long long)i);
     }
     std::vector<double> tmp(n);
@@ -1545,9 +1569,9 @@ sem_status sem_write_state(sem_ctx* ctx, int box, const double* p, const double*
     for (auto& pt : ctx->parts) {
         Box& b = pt.boxes[box];
         double* pprev = b.P[1 - ctx->cur];
-        CU(cudaMemcpy2DAsync(pprev, b.PX * 8, p + b.gx0, NXg * 8, b.NX * 8, rows, cudaMemcpyHostToDevice, ctx->stream));
-        CU(cudaMemcpy2DAsync(b.W, b.PX * 8, pdot + b.gx0, NXg * 8, b.NX * 8, rows, cudaMemcpyHostToDevice, ctx->stream));
-        sem::launch_set_state(pprev, b.P[ctx->cur], b.W, b.NX, b.PX, rows, ctx->dt, ctx->stream);
+        CU(copy_slab(const_cast<double*>(p), pprev, b, ctx->gNY[box], b.gy0, 0, false, ctx->stream));
+        CU(copy_slab(const_cast<double*>(pdot), b.W, b, ctx->gNY[box], b.gy0, 0, false, ctx->stream));
+        sem::launch_set_state(pprev, b.P[ctx->cur], b.W, b.NX, b.PX, b.NY * b.NZ, ctx->dt, ctx->stream);
     }
     st = reset_dynamic(ctx);
     if (st) return st;
@@ -1561,7 +1585,7 @@ sem_status sem_fill_random_state(sem_ctx* ctx, int box, unsigned long long seed,
     if (box < 0 || box >= (int)ctx->gdesc.size()) return fail(ctx, SEM_E_ARG, "bad box");
     for (auto& pt : ctx->parts) {
         Box& b = pt.boxes[box];
-        sem::launch_fill_random(b.P[1 - ctx->cur], b.W, b.P[ctx->cur], b.NX, b.PX, b.NY * b.NZ, b.gx0, b.NXg, seed, box,
+        sem::launch_fill_random(b.P[1 - ctx->cur], b.W, b.P[ctx->cur], b.NX, b.PX, b.NY, b.NZ, b.gy0, b.NYg, seed, box,
                                 ps, vs, ctx->dt, ctx->stream);
     }
     st = reset_dynamic(ctx);

@@ -82,7 +82,7 @@ struct VolParams {
     const double* __restrict__ F;
     double kF;
     // slab cuts (multi-GPU): this slab's -x / +x face is an internal cut, not a box face
-    int cutL, cutR;
+    int cutL, cutR;                 // this slab's -y / +y face is an internal cut (y-slabs)
     // DG interface layer: side = +1 (this box's +z face is Gamma_I, fine side),
     // -1 (its -z face, coarse side), 0 none; tau / sigma on the face lattice [NX*NY]
     int iface_side;
@@ -157,7 +157,7 @@ struct IfaceParams {
     double* tauf; double* sigf;     // fine outputs [NXf*NYf]
     double* h1; double* h2;         // [NYc][NXf] after the y gather
     double* tauc; double* sigc;     // coarse outputs [NXc*NYc]
-    int skip_ix0;                   // slab with a left cut: the shared fine cut line belongs to the left slab
+    int skip_iy0;                   // slab with a lower cut: the shared fine cut line belongs to the lower slab
 };
 
 // PML auxiliaries of one box (readings R23-R25).  Phi is element-local
@@ -210,20 +210,20 @@ struct CurvedParams {
 
 // One side of one slab cut for one box (partial rows before, fix-up after the exchange).
 struct CutParams {
-    int side;                       // 0: cut at ix = 0 (neighbour on the left), 1: at ix = NX-1
+    int side;                       // 0: cut at iy = 0 (neighbour below in y), 1: at iy = NY-1
     int N;
     long long NX, NY, NZ, PX;
     const double* P;                // p^{n+1} (partial)
     double* Pn;                     // p^{n+2}, w^{n+1} (fix-up)
     double* W;
-    double row[kMaxN + 1];          // R0 (side 0) or L (side 1), scaled by c^2 (2/h_x)^2
+    double row[kMaxN + 1];          // R0 (side 0) or L (side 1), scaled by c^2 (2/h_y)^2
     double dt;
     // coarse box of an interface: SIPG partials at the cut column (NYt > 0)
     long long NXt, NYt;
     const double* tau;
     const double* sig;
     double ktau[kMaxN + 1], ksig[kMaxN + 1];
-    double* out;                    // send buffer: [NY*NZ plane][NYt tau][NYt sigma]
+    double* out;                    // send buffer: [NX*NZ plane][NXt tau][NXt sigma]
     const double* in;               // receive buffer, same layout
 };
 
@@ -248,9 +248,9 @@ struct Box {
     double* my = nullptr;
     BoxTables tab{};
     std::vector<double> xh, yh, mxh, myh, mzh;  // host copies (global-lattice values for slab nodes)
-    long long gx0 = 0;      // global lattice x index of local ix = 0 (slab decomposition)
-    long long NXg = 0;      // global lattice NX of the box
-    bool cutL = false, cutR = false;  // -x / +x face of this slab is an internal cut
+    long long gy0 = 0;      // global lattice y index of local iy = 0 (slab decomposition)
+    long long NYg = 0;      // global lattice NY of the box
+    bool cutL = false, cutR = false;  // -y / +y face of this slab is an internal cut
     int iface_side = 0;
     double* tau = nullptr;  // interface outputs on this box's face lattice
     double* sig = nullptr;
@@ -364,8 +364,8 @@ bool volume_pair_supported(int N0, int N1);
 void volume_pair_prepare(int N0, int N1);
 void launch_modal(const ModalParams& p, cudaStream_t s);
 void launch_iface(const IfaceParams& p, cudaStream_t s);
-void launch_fill_random(double* p, double* w, double* pn, long long NX, long long PX, long long rows,
-                        long long gx0, long long NXg, unsigned long long seed, int box, double ps, double vs,
+void launch_fill_random(double* p, double* w, double* pn, long long NX, long long PX, long long NY, long long NZ,
+                        long long gy0, long long NYg, unsigned long long seed, int box, double ps, double vs,
                         double dt, cudaStream_t s);
 void launch_cut_partial(const CutBatch& B, cudaStream_t s);
 void launch_pml_elements(const PmlParams& p, cudaStream_t s);

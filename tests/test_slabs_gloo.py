@@ -1,7 +1,7 @@
-"""Multi-rank host logic on CPU (world size 2, gloo): the x-slab decomposition that libsem's NCCL path
+"""Multi-rank host logic on CPU (world size 2, gloo): the y-slab decomposition that libsem's NCCL path
 implements, checked without a GPU.
 
-* `sem_slab_plan` (host-only C-ABI entry) applies the partition rules: equal x-slabs, cuts in the
+* `sem_slab_plan` (host-only C-ABI entry) applies the partition rules: equal y-slabs, cuts in the
   membrane gaps, cuts on coarse-element boundaries of the 2:1 interface.
 * Two gloo ranks each build the oracle operator of their own slab with natural (rigid) cut faces,
   exchange ONE cut plane of partial results (K p and the lumped mass) and add the neighbour's part:
@@ -30,7 +30,7 @@ def test_slab_plan_rules():
         rec = config(i)
         for g in (1, 2, 4, 8):
             x0 = _plan(rec, g)
-            nel = rec["boxes"][0]["nel"][0]
+            nel = rec["boxes"][0]["nel"][1]
             assert x0 == [nel // g * r for r in range(g + 1)]
     assert _plan(config(1), 2) == [0, 12, 24]
     for rec, g in ((config(1), 4), (config(1), 8), (config(0), 2), (small_config("cfg2s"), 3),
@@ -66,7 +66,7 @@ def _worker(rank, world, port, name):
         gM = gs.split(gs.M)
         gG = gs.pmut_project(gp) if gs.pm is not None else None
         # this rank's slab with natural cut faces
-        win = (x0[rank], x0[rank + 1], 0, rec["boxes"][0]["nel"][1])
+        win = (0, rec["boxes"][0]["nel"][0], x0[rank], x0[rank + 1])
         crop, info = crop_record(rec, win, margin_fine=0)
         ss = System(crop)
         sp = np.concatenate([cb_uniform(seed, b, 0, info["maps"][b]) for b in range(nb)])
@@ -75,18 +75,19 @@ def _worker(rank, world, port, name):
         for b in range(nb):
             N = crop["boxes"][b]["degree"]
             nx = N * crop["boxes"][b]["nel"][0] + 1
+            ny = N * crop["boxes"][b]["nel"][1] + 1
             lat = np.arange(len(info["maps"][b]))
-            gx = lat % nx
-            # the cut column shared with the neighbour: last column (rank 0) / first column (rank 1)
-            cut_col = nx - 1 if rank == 0 else 0
-            mine = torch.from_numpy(np.stack([sK[b][gx == cut_col], sM[b][gx == cut_col]]))
+            gy = (lat // nx) % ny
+            # the cut row shared with the neighbour: last row (rank 0) / first row (rank 1)
+            cut_row = ny - 1 if rank == 0 else 0
+            mine = torch.from_numpy(np.stack([sK[b][gy == cut_row], sM[b][gy == cut_row]]))
             other = [torch.zeros_like(mine) for _ in range(world)]
             dist.all_gather(other, mine)                      # the one-plane exchange
             nbr = other[1 - rank].numpy()
             K_tot = sK[b].copy()
             M_tot = sM[b].copy()
-            K_tot[gx == cut_col] += nbr[0]
-            M_tot[gx == cut_col] += nbr[1]
+            K_tot[gy == cut_row] += nbr[0]
+            M_tot[gy == cut_row] += nbr[1]
             ref_K = gK[b][info["maps"][b]]
             ref_M = gM[b][info["maps"][b]]
             scale = np.abs(ref_K).max()

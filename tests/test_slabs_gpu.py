@@ -1,4 +1,4 @@
-"""x-slab decomposition (the multi-GPU path) verified on one GPU: SEM_F_EMULATE_SLABS keeps every
+"""y-slab decomposition (the multi-GPU path) verified on one GPU: SEM_F_EMULATE_SLABS keeps every
 slab of a world-size-W decomposition in one context and replaces the per-step NCCL exchange by a
 device copy, so the cut-plane partial rows, the coarse SIPG partial sums, the fix-up kernel, the
 membrane-preserving PMUT assignment and the slab readouts all run exactly as on W GPUs.
@@ -43,8 +43,8 @@ def test_small_configs_slabs(name, world):
 
 @pytest.mark.parametrize("world", [2, 3, 4, 6])
 def test_random_state_cavity_slabs(world):
-    rec = cavity_config(nel=(12, 3, 2), degree=5, extent=(12 * 2e-5, 6e-5, 4e-5))
-    rec["boxes"][0]["bc"] = [1, 1, 0, 1, 1, 0]
+    rec = cavity_config(nel=(3, 12, 2), degree=5, extent=(6e-5, 12 * 2e-5, 4e-5))
+    rec["boxes"][0]["bc"] = [0, 1, 1, 1, 1, 0]
     st = random_state(rec, seed=world)
     nm = oracle_run(rec, 25, state=st)
     sim = _sim(rec, world, state=st, steps=25)
@@ -65,15 +65,15 @@ def test_random_state_interface_slabs(world):
 def test_partition_errors():
     from paper_2603_06267_b200 import SemError
     with pytest.raises(SemError, match="PARTITION"):
-        _sim(config(0), 2)                     # the cut at 300 um crosses the membrane
+        _sim(config(0), 2)                     # the cut at y = 300 um crosses the membrane
     with pytest.raises(SemError, match="PARTITION"):
         _sim(small_config("cfg2s"), 5)         # 12 elements are not divisible by 5
     with pytest.raises(SemError, match="PARTITION"):
-        _sim(small_config("cfg2s"), 3)         # cuts at 100, 200 um cross membranes
+        _sim(small_config("cfg2s"), 3)         # cuts at y = 100, 200 um cross membranes
 
 
 def test_fullsize_cfg3_eight_slabs_crops():
-    """Config 3 at full size split into 8 slabs (cuts every 48 fine elements = 1.2 mm, in membrane
+    """Config 3 at full size split into 8 y-slabs (cuts every 48 fine elements = 1.2 mm, in membrane
     gaps), sampled against the oracle on crops that straddle a cut."""
     from oracle.newmark import Newmark
     from oracle.operators import System
@@ -86,7 +86,7 @@ def test_fullsize_cfg3_eight_slabs_crops():
         sim.fill_random_state(b, seed, ps, vs)
     rng = np.random.default_rng(3)
     crops = []
-    for win in [(36, 54, 0, 18), (180, 198, 186, 204)]:      # straddle the cuts at 48 and 192
+    for win in [(0, 18, 36, 54), (186, 204, 180, 198)]:      # straddle the y cuts at 48 and 192
         crop, info = crop_record(rec, win)
         picks = []
         for b, bx in enumerate(crop["boxes"]):

@@ -14,7 +14,7 @@ from sem_inputs import config  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 rec = config(3)
-out = {"what": "cfg3 x-slab decomposition emulated on one GPU", "steps": steps}
+out = {"what": "cfg3 y-slab decomposition emulated on one GPU", "steps": steps}
 base = None
 for G in (1, 2, 4, 8):
     flags = SEM_F_EMULATE_SLABS if G > 1 else 0
