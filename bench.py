@@ -176,7 +176,7 @@ def main():
     nccl_id = None
     flags = 0
     if world > 1:
-        # x-slab decomposition: libsem's own NCCL communicator for the per-step
+        # y-slab decomposition: libsem's own NCCL communicator for the per-step
         # cut-plane exchange; the id is created on rank 0 and broadcast through torch.distributed
         idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
@@ -186,7 +186,7 @@ def main():
         flags |= SEM_F_NO_GRAPH
     sim = Simulation(rec, device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_unique_id=nccl_id,
                      flags=flags)
-    ndof_total = sum(sim.ndof)      # global node count (every rank holds one x-slab of it)
+    ndof_total = sum(sim.ndof)      # global node count (every rank holds one y-slab of it)
 
     # ---- device-resident timed region ----------------------------------------------------------
     sim.step(args.warmup)
@@ -279,7 +279,7 @@ def main():
                    "n_pmut": len(rec["pmut"]["centers"]) if rec.get("pmut") else 0,
                    "n_modes": len(rec["pmut"]["mode_mn"]) if rec.get("pmut") else 0,
                    "dt": rec["dt"], "l2": "state 24 B/DOF resident = %.1f GB > 126 MB L2; no flush needed"
-                   % (24 * ndof_total / 1e9), "parallelism": f"x-slabs x{world}"},
+                   % (24 * ndof_total / 1e9), "parallelism": f"y-slabs x{world}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "vol_kernel (both boxes, per step)",
                      "bytes_per_step_algorithmic": BYTES_PER_DOF * ndof_total,

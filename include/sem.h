@@ -57,7 +57,7 @@ enum {
     SEM_F_COUPLING_LITERAL = 1 << 0, /* g(p^n, phi^n) exactly as printed (unstable at cfg masses)  */
     SEM_F_NAN_CHECK = 1 << 1,        /* check p for NaN/Inf after every sem_step call              */
     SEM_F_NO_GRAPH = 1 << 2,         /* launch kernels directly instead of a captured CUDA graph   */
-    SEM_F_EMULATE_SLABS = 1 << 3     /* world > 1 in ONE context on one device: every x-slab of the
+    SEM_F_EMULATE_SLABS = 1 << 3     /* world > 1 in ONE context on one device: every y-slab of the
                                         decomposition lives here and the per-step exchange is a
                                         device copy instead of NCCL (verifies the slab path on 1 GPU) */
 };
@@ -79,8 +79,8 @@ typedef struct {
     double dt;                   /* time step [s], caller-computed (reading R8)          */
     int device;                  /* CUDA device ordinal                                  */
     void* stream;                /* cudaStream_t to enqueue on; NULL -> library stream   */
-    int rank, world;             /* x-slab decomposition: rank's slab = elements
-                                    [r nel_x/world, (r+1) nel_x/world) of every box (nel_x must be
+    int rank, world;             /* y-slab decomposition: rank's slab = elements
+                                    [r nel_y/world, (r+1) nel_y/world) of every box (nel_y must be
                                     divisible by world; cuts must miss the membranes and align with
                                     the coarse elements of an interface -> SEM_E_PARTITION)       */
     const void* nccl_unique_id;  /* ncclUniqueId (128 bytes) when world > 1, else NULL  */
@@ -88,11 +88,11 @@ typedef struct {
 } sem_mesh_desc;
 
 /* Create the context: validates boxes, builds the 1D GLL tables and allocates p (two time
- * levels), w = p' + dt/2 p'' (one level) per box (this rank's x-slab), zero-initialised
+ * levels), w = p' + dt/2 p'' (one level) per box (this rank's y-slab), zero-initialised
  * (P:L609-610).  With world > 1 (and no SEM_F_EMULATE_SLABS) every rank calls it with the same
  * global boxes and the ncclUniqueId from sem_nccl_unique_id on rank 0; each step then exchanges
- * one cut plane per box with each x-neighbour.
- * Errors: SEM_E_ARG (bad descriptor), SEM_E_PARTITION (nel_x not divisible by world),
+ * one cut plane per box with each y-neighbour.
+ * Errors: SEM_E_ARG (bad descriptor), SEM_E_PARTITION (nel_y not divisible by world),
  * SEM_E_NCCL, SEM_E_CUDA / SEM_E_OOM.  *out is NULL on error. */
 sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out);
 
@@ -129,9 +129,9 @@ typedef struct {
 } sem_pmut_desc;
 sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pm);
 
-/* Host-only (no device touched): the x-slab plan of `world` slabs for these global boxes and (optional)
- * PMUT array.  slab_x0[world+1] receives the box-0 element index where each slab starts.
- * SEM_E_PARTITION if nel_x is not divisible by world, a cut crosses a membrane, or a cut is not
+/* Host-only (no device touched): the y-slab plan of `world` slabs for these global boxes and (optional)
+ * PMUT array.  slab_x0[world+1] receives the box-0 element y index where each slab starts.
+ * SEM_E_PARTITION if nel_y is not divisible by world, a cut crosses a membrane, or a cut is not
  * aligned with the coarse elements of a 2:1 interface (box 0 +z / box 1 -z tagged INTERFACE). */
 sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, const sem_pmut_desc* pm,
                          long long* slab_x0);

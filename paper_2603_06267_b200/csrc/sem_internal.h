@@ -303,7 +303,7 @@ struct PlaneWave {
 }  // namespace sem
 
 namespace sem {
-// One x-slab of the decomposition (one rank; all slabs live in one context under emulation).
+// One y-slab of the decomposition (one rank; all slabs live in one context under emulation).
 struct Part {
     int slab = 0;
     std::vector<Box> boxes;

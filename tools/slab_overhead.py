@@ -1,4 +1,4 @@
-"""Cost of the x-slab decomposition measured on one GPU (SEM_F_EMULATE_SLABS: all G slabs in one
+"""Cost of the y-slab decomposition measured on one GPU (SEM_F_EMULATE_SLABS: all G slabs in one
 context, exchange by device copies): ms/step of cfg 3 for G = 1, 2, 4, 8 slabs processed back to
 back.  The G-slab time divided by G approximates one rank's compute per step at G GPUs (the NCCL
 exchange of ~3 MB per neighbour runs on a second stream beside the volume kernel)."""
