@@ -26,18 +26,7 @@
 #ifndef SEM_MINB
 #define SEM_MINB 1
 #endif
-#ifndef SEM_L2HINT
-#define SEM_L2HINT 0
-#endif
-// launch bounds of the volume kernel; SEM_MAXREG caps registers explicitly (__maxnreg__)
-#ifdef SEM_MAXREG
-#define SEM_VOL_BOUNDS(TY) __maxnreg__(SEM_MAXREG)
-#else
 #define SEM_VOL_BOUNDS(TY) __launch_bounds__(32 * (TY + 1), SEM_MINB)
-#endif
-#ifndef SEM_CROWS
-#define SEM_CROWS 0
-#endif
 
 namespace sem {
 
@@ -75,26 +64,6 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
         ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
         : "memory");
 }
-// same with an L2 eviction-priority policy (createpolicy)
-__device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap* map, int x, int y, int z,
-                                                 uint32_t bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%2, %3, %4}], [%5], %6;"
-        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar), "l"(pol)
-        : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
 // ------------------------------------------------------------------------------------------------
 // Volume + update kernel (persistent, one launch for both boxes of a step)
 // ------------------------------------------------------------------------------------------------
@@ -125,27 +94,12 @@ __device__ __forceinline__ void vol_issue(const VolParams& p, unsigned char* rin
     unsigned char* s = ring + slot * RG::SLOT;
     const uint32_t bar = bars + 8u * slot;
     mbar_expect_tx(bar, G::PBYTES + G::WBYTES);
-#if SEM_L2HINT
-    // p planes are re-read by the neighbouring tiles (halo): keep; w is read once: evict first
-    tma_load_3d_hint(smem_u32(s), &p.tmP, tx0 - G::NH, ty0 - N, z, bar, policy_evict_last());
-    tma_load_3d_hint(smem_u32(s + G::POFF), &p.tmW, tx0, ty0, z, bar, policy_evict_first());
-#else
     tma_load_3d(smem_u32(s), &p.tmP, tx0 - G::NH, ty0 - N, z, bar);
     tma_load_3d(smem_u32(s + G::POFF), &p.tmW, tx0, ty0, z, bar);
-#endif
 }
 
-// Output stores of the volume kernel (SEM_STORE: 0 streaming .cs, 1 default write-back policy)
-#ifndef SEM_STORE
-#define SEM_STORE 1
-#endif
-__device__ __forceinline__ void st_out(double* p, double v) {
-#if SEM_STORE == 0
-    __stcs(p, v);
-#else
-    *p = v;
-#endif
-}
+// Output stores of the volume kernel: default write-back policy (measured faster than streaming .cs)
+__device__ __forceinline__ void st_out(double* p, double v) { *p = v; }
 
 // Per-thread state of the volume kernel (one tile).
 template <int N>
@@ -206,16 +160,8 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
     }
 #endif
     // ---- x: right-element row with per-lane (scaled) coefficients; the left-element row of a shared
-    //      node (row L) is evaluated by lane-1, then shuffled.  Warp-uniform rows (x/y left rows, all
-    //      z rows) are read from the kernel-parameter constant bank as DFMA operands: no registers.
-#if SEM_CROWS
-    const double* Lx = T.G[0][row_L(N)];
-    const double* Ly = T.G[1][row_L(N)];
-#else
+    //      node (the compile-time reference row L) is evaluated by lane-1, then shuffled
     const auto& RT = kRef<N>;
-    const double* Lx = RT.L;
-    const double* Ly = RT.L;
-#endif
     double v[N + 1];
 #pragma unroll
     for (int b = 0; b <= N; ++b) v[b] = sP[t.xb + b];
@@ -223,7 +169,7 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
 #pragma unroll
     for (int b = 0; b <= N; ++b) {
         xr = fma(t.cR[b], v[b], xr);
-        xl = fma(Lx[b], v[b], xl);
+        xl = fma(RT.L[b], v[b], xl);
     }
     const double xlr = __shfl_sync(0xffffffffu, xl, (threadIdx.x + 31) & 31);
     // ---- y: per-warp row (registers, scaled); left row of a shared node: row L
@@ -236,33 +182,11 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
     if (t.yLs != 0.0) {
         double yl = 0.0;
 #pragma unroll
-        for (int b = 0; b <= N; ++b) yl = fma(Ly[b], sP[t.yl + b * G::SW], yl);
+        for (int b = 0; b <= N; ++b) yl = fma(RT.L[b], sP[t.yl + b * G::SW], yl);
         acc = fma(t.yLs, yl, acc);
     }
     // ---- z: register window zw[k] = p(z0 - N + k), rows by compile-time plane class
     double z0 = 0.0, z1 = 0.0;
-#if SEM_CROWS
-    {
-        constexpr bool top = (C == N), bot = (C == 0 && (F & kFirst)), shared = (C == 0 && !(F & kFirst));
-        const double* Rz = T.G[2][top ? row_BN(N) : bot ? row_B0(N) : C];
-        if constexpr (shared) {
-            const double* Lz = T.G[2][row_L(N)];
-#pragma unroll
-            for (int b = 0; b <= N; ++b) z0 = fma(Rz[b], zw[N + b], z0);
-#pragma unroll
-            for (int b = 0; b <= N; ++b) z1 = fma(Lz[b], zw[b], z1);
-        } else {
-            // BN is the left-element row: it multiplies planes z0 - N .. z0 (window N-N+C .. N+C = 0..N
-            // at C = N); every other row multiplies the right element z0 .. z0 + N
-            constexpr int base = top ? 0 : N;
-#pragma unroll
-            for (int b = 0; b <= N; b += 2) z0 = fma(Rz[b], zw[base + b], z0);
-#pragma unroll
-            for (int b = 1; b <= N; b += 2) z1 = fma(Rz[b], zw[base + b], z1);
-        }
-    }
-    acc += z0 + z1;
-#else
     if constexpr (C == N) {   // top boundary plane: left element only, BN = 2 L
 #pragma unroll
         for (int b = 0; b <= N; b += 2) z0 = fma(2.0 * RT.L[b], zw[N + b], z0);
@@ -285,7 +209,6 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
         for (int b = 1; b <= N; b += 2) z1 = fma(RT.R[C][b], zw[N + b], z1);
     }
     acc = fma(p.sdir[2], z0 + z1, acc);
-#endif
     double a = -acc;
     const double wv = sW[t.wown];
     const double pv = zw[N + C];
@@ -503,21 +426,13 @@ __device__ __forceinline__ void vol_tile(const VolParams& p, unsigned char* ring
     }
 }
 
-// Tile order inside a box: bands of SEM_BAND tile rows, column-major inside a band (tx slow, ty fast),
-// bands in y order.  Tiles are handed out in this order, so both the x and the y neighbours of a tile
-// (which re-read its halo rows of p) run within a few tile-times of it and find them in L2, while the
-// concurrently streamed region still spans long contiguous x rows (DRAM page locality).  SEM_BAND = 1
-// is plain row-major order.
-#ifndef SEM_BAND
-#define SEM_BAND 1
-#endif
-__device__ __forceinline__ void tile_xy(unsigned lt, unsigned ntx, unsigned nty, int& tx, int& ty) {
-    const unsigned B = SEM_BAND;
-    const unsigned per = B * ntx;
-    const unsigned s = lt / per, r = lt - s * per;
-    const unsigned h = (s + 1) * B <= nty ? B : nty - s * B;   // last band may be shorter
-    tx = (int)(r / h);
-    ty = (int)(s * B + r % h);
+// Tile order inside a box: row-major (tx fastest).  Tiles are handed out in this order, so a tile's x
+// neighbours (which re-read its halo columns of p) run at the same time, and the concurrently streamed
+// region spans long contiguous x rows (DRAM page locality).  (Strip and band orders that keep the y
+// neighbours closer were measured slower: profiles/README.md.)
+__device__ __forceinline__ void tile_xy(unsigned lt, unsigned ntx, unsigned /*nty*/, int& tx, int& ty) {
+    tx = (int)(lt % ntx);
+    ty = (int)(lt / ntx);
 }
 
 // Launch-wide ring of a (N0, N1) pair (N1 = 0: one box).
