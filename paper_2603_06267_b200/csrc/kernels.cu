@@ -1005,20 +1005,29 @@ void launch_cut_fixup(const CutBatch& B, cudaStream_t s) {
 // Crank-Nicolson update of Phi; weak divergence sum_q w_q |J| Phi^{n+1}(q) . grad phi_i(x_q) and the
 // nodal terms alpha pdot + beta p + gamma psi accumulate (atomics) into the PML acceleration da.
 // ------------------------------------------------------------------------------------------------
+// elements per block of the PML kernels (blocks of ~256 threads: small elements share a block)
 template <int N>
-__global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) pml_element_kernel(const __grid_constant__ PmlParams p) {
-    constexpr int n1 = N + 1, nl = n1 * n1 * n1;
-    __shared__ double sp[nl], ss[nl], sf[3][nl];
-    const int t = threadIdx.x;
+constexpr int pml_epb() { return (N + 1) * (N + 1) * (N + 1) >= 256 ? 1 : 256 / ((N + 1) * (N + 1) * (N + 1)); }
+
+template <int N>
+__global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1)) pml_element_kernel(const __grid_constant__ PmlParams p) {
+    constexpr int n1 = N + 1, nl = n1 * n1 * n1, EPB = pml_epb<N>();
+    __shared__ double sp_[EPB][nl], ss_[EPB][nl], sf_[EPB][3][nl];
+    const int el = threadIdx.x / nl, t = threadIdx.x - el * nl;
+    double* sp = sp_[el];
+    double* ss = ss_[el];
+    double (&sf)[3][nl] = sf_[el];
     const int a = t % n1, b = (t / n1) % n1, c = t / (n1 * n1);
-    const int k = blockIdx.x;
+    const int kraw = blockIdx.x * EPB + el;
+    const bool active = kraw < p.n_el;
+    const int k = active ? kraw : p.n_el - 1;   // idle threads mirror the last element (no writes)
     const int ex = p.elems[3 * k], ey = p.elems[3 * k + 1], ez = p.elems[3 * k + 2];
     const int gx = N * ex + a, gy = N * ey + b, gz = N * ez + c;
     const long long g = ((long long)gz * p.NY + gy) * p.PX + gx;
     const double pv = p.P[g];
     const double so = p.psi_old[g];
     const double sn = fma(p.dt, pv, so);
-    p.psi_new[g] = sn;   // a node shared by several PML elements gets the same value from each
+    if (active) p.psi_new[g] = sn;   // a node shared by several PML elements gets the same value from each
     const double sm = 0.5 * (so + sn);
     sp[t] = pv;
     ss[t] = sm;
@@ -1050,7 +1059,7 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) pml_element_kerne
         const double old = ph[d * nl + t];
         const double rhs = p.c2 * p.s2h[d] * ((alpha - 2.0 * z[d]) * gp[d] + Z3[d] * gs[d]);
         const double nw = fma(cA[d], old, cB[d] * rhs);   // Crank-Nicolson on Z1 = -z_d
-        ph[d * nl + t] = nw;
+        if (active) ph[d * nl + t] = nw;
         sf[d][t] = 0.5 * (old + nw);
     }
     __syncthreads();
@@ -1069,18 +1078,19 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) pml_element_kerne
     // a non-PML owner only occurs where all z vanish)
     const bool own = (a < N || ex == p.nelx - 1) && (b < N || ey == p.nely - 1) && (c < N || ez == p.nelz - 1);
     if (own) da -= alpha * p.W[g] + beta * pv + gamma * sm;
-    atomicAdd(p.da + g, da);
+    if (active) atomicAdd(p.da + g, da);
 }
 
 // After the volume kernel: w^{n+1} += dt da, p^{n+2} += dt^2 da (the update is linear in the
 // acceleration), and clear da for the next step.  Every node of every PML element is visited; the
 // atomic exchange hands each node's value to exactly one thread.
 template <int N>
-__global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) pml_fixup_kernel(const __grid_constant__ PmlParams p) {
-    constexpr int n1 = N + 1;
-    const int t = threadIdx.x;
+__global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1)) pml_fixup_kernel(const __grid_constant__ PmlParams p) {
+    constexpr int n1 = N + 1, nl = n1 * n1 * n1, EPB = pml_epb<N>();
+    const int el = threadIdx.x / nl, t = threadIdx.x - el * nl;
     const int a = t % n1, b = (t / n1) % n1, c = t / (n1 * n1);
-    const int k = blockIdx.x;
+    const int k = blockIdx.x * EPB + el;
+    if (k >= p.n_el) return;
     const int gx = N * p.elems[3 * k] + a, gy = N * p.elems[3 * k + 1] + b, gz = N * p.elems[3 * k + 2] + c;
     const long long g = ((long long)gz * p.NY + gy) * p.PX + gx;
     const unsigned long long bits = atomicExch(reinterpret_cast<unsigned long long*>(p.da + g), 0ull);
@@ -1095,7 +1105,7 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) pml_fixup_kernel(
 void launch_pml_elements(const PmlParams& p, cudaStream_t s) {
     if (p.n_el <= 0) return;
     switch (p.N) {
-#define SEM_PML_CASE(n) case n: pml_element_kernel<n><<<p.n_el, (n + 1) * (n + 1) * (n + 1), 0, s>>>(p); break;
+#define SEM_PML_CASE(n) case n: pml_element_kernel<n><<<(p.n_el + pml_epb<n>() - 1) / pml_epb<n>(), pml_epb<n>() * (n + 1) * (n + 1) * (n + 1), 0, s>>>(p); break;
         SEM_PML_CASE(1) SEM_PML_CASE(2) SEM_PML_CASE(3) SEM_PML_CASE(4)
         SEM_PML_CASE(5) SEM_PML_CASE(6) SEM_PML_CASE(7) SEM_PML_CASE(8)
 #undef SEM_PML_CASE
@@ -1106,7 +1116,7 @@ void launch_pml_elements(const PmlParams& p, cudaStream_t s) {
 void launch_pml_fixup(const PmlParams& p, cudaStream_t s) {
     if (p.n_el <= 0) return;
     switch (p.N) {
-#define SEM_PML_CASE(n) case n: pml_fixup_kernel<n><<<p.n_el, (n + 1) * (n + 1) * (n + 1), 0, s>>>(p); break;
+#define SEM_PML_CASE(n) case n: pml_fixup_kernel<n><<<(p.n_el + pml_epb<n>() - 1) / pml_epb<n>(), pml_epb<n>() * (n + 1) * (n + 1) * (n + 1), 0, s>>>(p); break;
         SEM_PML_CASE(1) SEM_PML_CASE(2) SEM_PML_CASE(3) SEM_PML_CASE(4)
         SEM_PML_CASE(5) SEM_PML_CASE(6) SEM_PML_CASE(7) SEM_PML_CASE(8)
 #undef SEM_PML_CASE
