@@ -75,3 +75,11 @@ def test_interface_lattice_mismatch():
     rec = conforming_cut_config(nel_xy=4, nz_lo=2, nz_hi=2, degree=5, degree_hi=3, ratio=2, h=25e-6)
     rec["boxes"][1]["extent"] = (rec["boxes"][1]["extent"][0] * 1.1,) + tuple(rec["boxes"][1]["extent"][1:])
     assert _status(lambda: Simulation(rec)) == SEM_E_UNMATCHED
+
+
+def test_nccl_loadable_unique_id():
+    """The multi-GPU path dlopens NCCL (the libnccl.so.2 torch ships): a unique id can be created."""
+    import torch.distributed  # noqa: F401  (the same process state bench.py runs in)
+    from paper_2603_06267_b200 import sem_nccl_unique_id
+    uid = sem_nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128 and any(uid)
