@@ -657,21 +657,25 @@ __device__ __forceinline__ double drive_tx(const ModalParams& p, double tp) {
     return p.amp * sin(p.om0 * tp) * 0.5 * (1.0 - cos(p.om0 * tp / p.ncyc));
 }
 
-__global__ void __launch_bounds__(128) modal_kernel(const __grid_constant__ ModalParams p) {
-    const int lane = threadIdx.x & 31;
-    const int k = blockIdx.x * 4 + (threadIdx.x >> 5);
-    if (k >= p.n_pmut) return;
+// One block of kModalWarps warps per PMUT: the warps share the membrane's rows (projection and force
+// plane), warp 0 advances the modes.  (One warp per PMUT left the grid at < 1 block per SM for the
+// 512 PMUTs of a cfg-3 slab: latency-bound.)
+constexpr int kModalWarps = 4;
+
+__global__ void __launch_bounds__(32 * kModalWarps) modal_kernel(const __grid_constant__ ModalParams p) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k = blockIdx.x;
     const unsigned FULL = 0xffffffffu;
     const int M = p.n_modes;
-    const long long n = __ldcg(p.step);
     const double dt = p.dt;
-    const double t1 = (double)(n + 1) * dt, t0 = (double)n * dt;
     const int i0 = p.rect[4 * k], j0 = p.rect[4 * k + 1], ni = p.rect[4 * k + 2], nj = p.rect[4 * k + 3];
     const int L = p.lmax;
     const double* sxk = p.sx + (size_t)k * M * L;
     const double* syk = p.sy + (size_t)k * M * L;
     const double* wxk = p.wx + (size_t)k * L;
     const double* wyk = p.wy + (size_t)k * L;
+    __shared__ double red[kModalWarps][kMaxModes];
+    __shared__ double qv_s[kMaxModes];
 
     // pressure projection G_m = sum_ij m_x(i) S_x(i) m_y(j) S_y(j) p_ij   (Eq. 12: int p U.n = -G)
     double acc[kMaxModes];
@@ -683,7 +687,7 @@ __global__ void __launch_bounds__(128) modal_kernel(const __grid_constant__ Moda
         double bx[kMaxModes];
 #pragma unroll
         for (int m = 0; m < kMaxModes; ++m) bx[m] = (on && m < M) ? wxk[i] * sxk[m * L + i] : 0.0;
-        for (int j = 0; j < nj; ++j) {
+        for (int j = warp; j < nj; j += kModalWarps) {
             const double val = on ? p.P[(long long)(j0 + j) * p.PX + i0 + i] : 0.0;
             const double wj = wyk[j];
 #pragma unroll
@@ -696,44 +700,54 @@ __global__ void __launch_bounds__(128) modal_kernel(const __grid_constant__ Moda
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc[m] += __shfl_xor_sync(FULL, acc[m], o);
     }
-    double G = 0.0;
+    if (lane == 0)
 #pragma unroll
-    for (int m = 0; m < kMaxModes; ++m)
-        if (lane == m) G = acc[m];
+        for (int m = 0; m < kMaxModes; ++m) red[warp][m] = acc[m];
+    __syncthreads();
 
-    const bool act = lane < M;
-    const size_t km = (size_t)k * M + lane;
-    double q = 0, qd = 0, qdd = 0;
-    if (act) { q = p.q[km]; qd = p.qd[km]; qdd = p.qdd[km]; }
-    const double q1 = q + dt * qd + 0.5 * dt * dt * qdd;
-    double qd1 = qd + 0.5 * dt * qdd;
-    const double etam = act ? p.eta[lane] : 0.0;
-    // phi at the coupling time level (R2): predicted -> (t^{n+1}, q^{n+1}); literal -> (t^n, q^n)
-    const double tu = p.literal ? t0 : t1;
-    double s = etam * (p.literal ? q : q1);
-    double s1 = etam * q1;
+    if (warp == 0) {   // modal predictor / solve / corrector (lane m = mode m)
+        const long long n = __ldcg(p.step);
+        const double t1 = (double)(n + 1) * dt, t0 = (double)n * dt;
+        double G = 0.0;
+        if (lane < kMaxModes)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        s += __shfl_xor_sync(FULL, s, o);
-        s1 += __shfl_xor_sync(FULL, s1, o);
+            for (int w = 0; w < kModalWarps; ++w) G += red[w][lane];
+        const bool act = lane < M;
+        const size_t km = (size_t)k * M + lane;
+        double q = 0, qd = 0, qdd = 0;
+        if (act) { q = p.q[km]; qd = p.qd[km]; qdd = p.qdd[km]; }
+        const double q1 = q + dt * qd + 0.5 * dt * dt * qdd;
+        double qd1 = qd + 0.5 * dt * qdd;
+        const double etam = act ? p.eta[lane] : 0.0;
+        // phi at the coupling time level (R2): predicted -> (t^{n+1}, q^{n+1}); literal -> (t^n, q^n)
+        const double tu = p.literal ? t0 : t1;
+        double s = etam * (p.literal ? q : q1);
+        double s1 = etam * q1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s += __shfl_xor_sync(FULL, s, o);
+            s1 += __shfl_xor_sync(FULL, s1, o);
+        }
+        const double tp_delay = p.delay[k];
+        const double phi = (p.rx && tu > p.t_switch) ? s * p.invC : drive_tx(p, tu - tp_delay);
+        const double phi1 = (p.rx && t1 > p.t_switch) ? s1 * p.invC : drive_tx(p, t1 - tp_delay);
+        double qdd1 = 0.0;
+        if (act) {
+            qdd1 = -p.omega2[km] * q1 - p.twozw[km] * qd1 + (-G + etam * phi) * p.invmass[lane];
+            qd1 = qd1 + 0.5 * dt * qdd1;
+            p.q[km] = q1;
+            p.qd[km] = qd1;
+            p.qdd[km] = qdd1;
+        }
+        if (lane == 0) p.phi[k] = phi1;
+        if (lane < kMaxModes) qv_s[lane] = qdd1;
     }
-    const double tp_delay = p.delay[k];
-    const double phi = (p.rx && tu > p.t_switch) ? s * p.invC : drive_tx(p, tu - tp_delay);
-    const double phi1 = (p.rx && t1 > p.t_switch) ? s1 * p.invC : drive_tx(p, t1 - tp_delay);
-    double qdd1 = 0.0;
-    if (act) {
-        qdd1 = -p.omega2[km] * q1 - p.twozw[km] * qd1 + (-G + etam * phi) * p.invmass[lane];
-        qd1 = qd1 + 0.5 * dt * qdd1;
-        p.q[km] = q1;
-        p.qd[km] = qd1;
-        p.qdd[km] = qdd1;
-    }
-    if (lane == 0) p.phi[k] = phi1;
+    __syncthreads();
     double qv[kMaxModes];
 #pragma unroll
-    for (int m = 0; m < kMaxModes; ++m) qv[m] = __shfl_sync(FULL, qdd1, m);
+    for (int m = 0; m < kMaxModes; ++m) qv[m] = qv_s[m];
     // force plane F = kappa sum_m qdd_m S_m  (Eq. 11; the 1/M factor is applied in vol_kernel)
-    for (int j = 0; j < nj; ++j) {
+    for (int j = warp; j < nj; j += kModalWarps) {
         for (int ib = 0; ib < ni; ib += 32) {
             const int i = ib + lane;
             if (i < ni) {
@@ -748,7 +762,7 @@ __global__ void __launch_bounds__(128) modal_kernel(const __grid_constant__ Moda
 }
 
 void launch_modal(const ModalParams& p, cudaStream_t s) {
-    modal_kernel<<<(p.n_pmut + 3) / 4, 128, 0, s>>>(p);
+    if (p.n_pmut > 0) modal_kernel<<<p.n_pmut, 32 * kModalWarps, 0, s>>>(p);
 }
 
 // ------------------------------------------------------------------------------------------------
