@@ -1147,15 +1147,25 @@ void launch_pml_fixup(const PmlParams& p, cudaStream_t s) {
 template <int N>
 __global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) curved_residual_kernel(const __grid_constant__ CurvedParams p) {
     constexpr int n1 = N + 1, nl = n1 * n1 * n1;
-    __shared__ double sp[nl], sf[3][nl], sv[24];
+    __shared__ double sp[nl], sf[3][nl], cc[8][3];
     const int t = threadIdx.x;
     const int a = t % n1, b = (t / n1) % n1, c = t / (n1 * n1);
     const int e = blockIdx.x;
     const int ex = e % p.nelx, ey = (e / p.nelx) % p.nely, ez = e / (p.nelx * p.nely);
-    if (t < 24) {
-        const int v = t / 3, i = t % 3;
-        const int vx = ex + (v & 1), vy = ey + ((v >> 1) & 1), vz = ez + (v >> 2);
-        sv[t] = p.vlat[3 * ((size_t)vx + (size_t)(p.nelx + 1) * ((size_t)vy + (size_t)(p.nely + 1) * vz)) + i];
+    // monomial coefficients of the trilinear map: x = c0 + c1 xi + c2 eta + c3 zeta + c4 xi eta
+    //   + c5 eta zeta + c6 xi zeta + c7 xi eta zeta  (c_j = 1/8 sum_v X_v * sign product)
+    for (int q = t; q < 24; q += nl) {
+        const int j = q / 3, i = q % 3;
+        double acc = 0.0;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+            const int vx = ex + (v & 1), vy = ey + ((v >> 1) & 1), vz = ez + (v >> 2);
+            const double X = p.vlat[3 * ((size_t)vx + (size_t)(p.nelx + 1) * ((size_t)vy + (size_t)(p.nely + 1) * vz)) + i];
+            const double s0 = (v & 1) ? 1.0 : -1.0, s1 = (v & 2) ? 1.0 : -1.0, s2 = (v & 4) ? 1.0 : -1.0;
+            const double sg[8] = {1.0, s0, s1, s2, s0 * s1, s1 * s2, s0 * s2, s0 * s1 * s2};
+            acc = fma(sg[j], X, acc);
+        }
+        cc[j][i] = 0.125 * acc;
     }
     const int gx = N * ex + a, gy = N * ey + b, gz = N * ez + c;
     const long long g = ((long long)gz * p.NY + gy) * p.PX + gx;
@@ -1168,18 +1178,14 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) curved_residual_k
         gh[1] = fma(p.D[b][j], sp[a + n1 * (j + n1 * c)], gh[1]);
         gh[2] = fma(p.D[c][j], sp[a + n1 * (b + n1 * j)], gh[2]);
     }
-    // Jacobian of the trilinear map at (x_a, x_b, x_c): J[i][j] = sum_v X_v,i dN_v/dxi_j
-    const double xi[3] = {p.x[a], p.x[b], p.x[c]};
-    double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    // Jacobian of the trilinear map at (x_a, x_b, x_c) from the monomial coefficients
+    const double xi = p.x[a], et = p.x[b], ze = p.x[c];
+    double J[3][3];
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-        const double s0 = (v & 1) ? 1.0 : -1.0, s1 = (v & 2) ? 1.0 : -1.0, s2 = (v & 4) ? 1.0 : -1.0;
-        const double f0 = 1.0 + s0 * xi[0], f1 = 1.0 + s1 * xi[1], f2 = 1.0 + s2 * xi[2];
-        const double dN[3] = {0.125 * s0 * f1 * f2, 0.125 * s1 * f0 * f2, 0.125 * s2 * f0 * f1};
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int j = 0; j < 3; ++j) J[i][j] = fma(dN[j], sv[3 * v + i], J[i][j]);
+    for (int i = 0; i < 3; ++i) {
+        J[i][0] = cc[1][i] + cc[4][i] * et + cc[6][i] * ze + cc[7][i] * et * ze;
+        J[i][1] = cc[2][i] + cc[4][i] * xi + cc[5][i] * ze + cc[7][i] * xi * ze;
+        J[i][2] = cc[3][i] + cc[5][i] * et + cc[6][i] * xi + cc[7][i] * xi * et;
     }
     // adj = det J^-1 (rows: cofactors); |J| J^-1 J^-T = adj adj^T / det
     double A[3][3];
@@ -1201,26 +1207,27 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) curved_residual_k
 #pragma unroll
     for (int i = 0; i < 3; ++i) sf[i][t] = sc * (A[i][0] * u[0] + A[i][1] * u[1] + A[i][2] * u[2]);
     __syncthreads();
-    double r = 0.0;
+    double rx = 0.0, ry = 0.0, rz = 0.0;   // three independent chains
 #pragma unroll
     for (int j = 0; j <= N; ++j) {
-        r = fma(p.D[j][a], sf[0][j + n1 * (b + n1 * c)], r);
-        r = fma(p.D[j][b], sf[1][a + n1 * (j + n1 * c)], r);
-        r = fma(p.D[j][c], sf[2][a + n1 * (b + n1 * j)], r);
+        rx = fma(p.D[j][a], sf[0][j + n1 * (b + n1 * c)], rx);
+        ry = fma(p.D[j][b], sf[1][a + n1 * (j + n1 * c)], ry);
+        rz = fma(p.D[j][c], sf[2][a + n1 * (b + n1 * j)], rz);
     }
-    atomicAdd(p.res + g, r);
+    atomicAdd(p.res + g, rx + ry + rz);
 }
 
 __global__ void curved_update_kernel(const __grid_constant__ CurvedParams p) {
     const long long ix = (long long)blockIdx.x * blockDim.x + threadIdx.x;   // 2D grid: x, lattice row
     if (ix >= p.NX) return;
     const long long g = (long long)blockIdx.y * p.PX + ix;
-    const double wv = p.W[g];
-    const double a = -p.minv[g] * p.res[g] - p.cdamp[g] * wv;
-    p.res[g] = 0.0;
+    // every load before the first store (the pointers may alias as far as the compiler knows)
+    const double wv = p.W[g], mi = p.minv[g], r = p.res[g], cd = p.cdamp[g], pv = p.P[g];
+    const double a = -mi * r - cd * wv;
     const double wn = fma(p.dt, a, wv);
+    p.res[g] = 0.0;
     p.W[g] = wn;
-    p.Pn[g] = fma(p.dt, wn, p.P[g]);
+    p.Pn[g] = fma(p.dt, wn, pv);
 }
 
 void launch_curved(const CurvedParams& p, cudaStream_t s) {
