@@ -1023,8 +1023,14 @@ void launch_cut_fixup(const CutBatch& B, cudaStream_t s) {
 template <int N>
 constexpr int pml_epb() { return (N + 1) * (N + 1) * (N + 1) >= 256 ? 1 : 256 / ((N + 1) * (N + 1) * (N + 1)); }
 
+// resident blocks per SM the element kernel is compiled for (register budget): more blocks hide the
+// latency of its short, barrier-separated phases (N = 3: 339 vs 458 us per cfg-3 PML step); the larger
+// elements would spill
 template <int N>
-__global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1)) pml_element_kernel(const __grid_constant__ PmlParams p) {
+constexpr int pml_minb() { return N <= 3 ? 4 : (N <= 5 ? 3 : (N == 6 ? 2 : 1)); }
+
+template <int N>
+__global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1), pml_minb<N>()) pml_element_kernel(const __grid_constant__ PmlParams p) {
     constexpr int n1 = N + 1, nl = n1 * n1 * n1, EPB = pml_epb<N>();
     __shared__ double sp_[EPB][nl], ss_[EPB][nl], sf_[EPB][3][nl];
     const int el = threadIdx.x / nl, t = threadIdx.x - el * nl;
@@ -1038,8 +1044,20 @@ __global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1)) pm
     const int ex = p.elems[3 * k], ey = p.elems[3 * k + 1], ez = p.elems[3 * k + 2];
     const int gx = N * ex + a, gy = N * ey + b, gz = N * ez + c;
     const long long g = ((long long)gz * p.NY + gy) * p.PX + gx;
+    // every global load first (memory-level parallelism): nodal p, psi, w, the element-local Phi and the
+    // per-axis tables
     const double pv = p.P[g];
     const double so = p.psi_old[g];
+    const bool own = (a < N || ex == p.nelx - 1) && (b < N || ey == p.nely - 1) && (c < N || ez == p.nelz - 1);
+    const double wv = own ? p.W[g] : 0.0;
+    double* ph = p.phi + (size_t)k * 3 * nl;
+    const double phold[3] = {ph[t], ph[nl + t], ph[2 * nl + t]};
+    const double* __restrict__ Tx = p.tx + 4 * gx;
+    const double* __restrict__ Ty = p.ty + 4 * gy;
+    const double* __restrict__ Tz = p.tz + 4 * gz;
+    const double z[3] = {Tx[0], Ty[0], Tz[0]};
+    const double cA[3] = {Tx[1], Ty[1], Tz[1]}, cB[3] = {Tx[2], Ty[2], Tz[2]};
+    const double minv = Tx[3] * Ty[3] * Tz[3];
     const double sn = fma(p.dt, pv, so);
     if (active) p.psi_new[g] = sn;   // a node shared by several PML elements gets the same value from each
     const double sm = 0.5 * (so + sn);
@@ -1058,19 +1076,13 @@ __global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1)) pm
         gp[2] = fma(p.D[c][j], sp[iz], gp[2]);
         gs[2] = fma(p.D[c][j], ss[iz], gs[2]);
     }
-    const double* __restrict__ Tx = p.tx + 4 * gx;
-    const double* __restrict__ Ty = p.ty + 4 * gy;
-    const double* __restrict__ Tz = p.tz + 4 * gz;
-    const double z[3] = {Tx[0], Ty[0], Tz[0]};
-    const double cA[3] = {Tx[1], Ty[1], Tz[1]}, cB[3] = {Tx[2], Ty[2], Tz[2]};
     const double alpha = z[0] + z[1] + z[2];
     const double beta = z[0] * z[1] + z[1] * z[2] + z[2] * z[0];
     const double gamma = z[0] * z[1] * z[2];
     const double Z3[3] = {z[1] * z[2], z[2] * z[0], z[0] * z[1]};
-    double* ph = p.phi + (size_t)k * 3 * nl;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        const double old = ph[d * nl + t];
+        const double old = phold[d];
         const double rhs = p.c2 * p.s2h[d] * ((alpha - 2.0 * z[d]) * gp[d] + Z3[d] * gs[d]);
         const double nw = fma(cA[d], old, cB[d] * rhs);   // Crank-Nicolson on Z1 = -z_d
         if (active) ph[d * nl + t] = nw;
@@ -1087,11 +1099,10 @@ __global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1)) pm
     }
     const double r = p.jac * (p.s2h[0] * p.w[b] * p.w[c] * rx + p.s2h[1] * p.w[a] * p.w[c] * ry +
                               p.s2h[2] * p.w[a] * p.w[b] * rz);
-    double da = -r * (Tx[3] * Ty[3] * Tz[3]);
+    double da = -r * minv;
     // nodal terms once per node: by the element that owns it (lowest element index containing the node;
     // a non-PML owner only occurs where all z vanish)
-    const bool own = (a < N || ex == p.nelx - 1) && (b < N || ey == p.nely - 1) && (c < N || ez == p.nelz - 1);
-    if (own) da -= alpha * p.W[g] + beta * pv + gamma * sm;
+    if (own) da -= alpha * wv + beta * pv + gamma * sm;
     if (active) atomicAdd(p.da + g, da);
 }
 
