@@ -32,6 +32,7 @@ struct Tables {
     double w[N + 1];
     double R[N][N + 1];   // reference rows R[a], a = 0..N-1
     double L[N + 1];      // left-element row of a shared node
+    double D[N + 1][N + 1];   // differentiation matrix D[i][j] = l_j'(x_i)
 };
 
 template <int N>
@@ -80,6 +81,8 @@ constexpr Tables<N> make_tables() {
             }
         D[i][i] = -s;
     }
+    for (int i = 0; i <= N; ++i)
+        for (int j = 0; j <= N; ++j) t.D[i][j] = D[i][j];
     double A[N + 1][N + 1] = {};
     for (int a = 0; a <= N; ++a)
         for (int b = 0; b <= N; ++b) {

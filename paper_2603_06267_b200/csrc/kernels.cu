@@ -1150,107 +1150,264 @@ void launch_pml_fixup(const PmlParams& p, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------------------------
-// Curved boxes (trilinear vertex lattice): one block per element, one thread per
-// element GLL node.  grad_hat p by the differentiation matrix, flux = w_q c^2 |J| J^-1 J^-T grad_hat p
-// with J recomputed from the element's 8 vertices (cofactor form: |J| J^-1 J^-T = adj adj^T / det),
-// r_i = sum_q grad_hat phi_i(q) . flux(q) (D^T), scatter-add; then a nodal kick-drift.
+// Curved boxes (trilinear vertex lattice): element scatter with the metric
+// recomputed.  A persistent grid of blocks; a block holds EPB elements and one thread per element
+// x-line (b, c), so the x index a of the line's nodes is a compile-time loop index: the x derivative
+// and its transpose use compile-time D entries on the line's own registers; the y and z derivatives
+// read the other lines from shared memory.  The next element group's lines and vertices are
+// prefetched into registers while the current group computes.
+//   grad_hat p  ->  flux = w_q c^2 |J| J^-1 J^-T grad_hat p  (adj(J) adj(J)^T / det J, J recomputed
+//   from the 8 vertices: dx/dxi is constant along an x-line and dx/deta, dx/dzeta are affine in xi)
+//   ->  r_i = sum_q grad_hat phi_i(q) . flux(q)  ->  scatter-add; then a nodal kick-drift.
 // ------------------------------------------------------------------------------------------------
 template <int N>
-__global__ void __launch_bounds__((N + 1) * (N + 1) * (N + 1)) curved_residual_kernel(const __grid_constant__ CurvedParams p) {
-    constexpr int n1 = N + 1, nl = n1 * n1 * n1;
-    __shared__ double sp[nl], sf[3][nl], cc[8][3];
-    const int t = threadIdx.x;
-    const int a = t % n1, b = (t / n1) % n1, c = t / (n1 * n1);
-    const int e = blockIdx.x;
+__device__ __forceinline__ long long curved_node(const CurvedParams& p, int e, int a, int b, int c) {
     const int ex = e % p.nelx, ey = (e / p.nelx) % p.nely, ez = e / (p.nelx * p.nely);
-    // monomial coefficients of the trilinear map: x = c0 + c1 xi + c2 eta + c3 zeta + c4 xi eta
-    //   + c5 eta zeta + c6 xi zeta + c7 xi eta zeta  (c_j = 1/8 sum_v X_v * sign product)
-    for (int q = t; q < 24; q += nl) {
-        const int j = q / 3, i = q % 3;
-        double acc = 0.0;
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-            const int vx = ex + (v & 1), vy = ey + ((v >> 1) & 1), vz = ez + (v >> 2);
-            const double X = p.vlat[3 * ((size_t)vx + (size_t)(p.nelx + 1) * ((size_t)vy + (size_t)(p.nely + 1) * vz)) + i];
-            const double s0 = (v & 1) ? 1.0 : -1.0, s1 = (v & 2) ? 1.0 : -1.0, s2 = (v & 4) ? 1.0 : -1.0;
-            const double sg[8] = {1.0, s0, s1, s2, s0 * s1, s1 * s2, s0 * s2, s0 * s1 * s2};
-            acc = fma(sg[j], X, acc);
-        }
-        cc[j][i] = 0.125 * acc;
-    }
-    const int gx = N * ex + a, gy = N * ey + b, gz = N * ez + c;
-    const long long g = ((long long)gz * p.NY + gy) * p.PX + gx;
-    sp[t] = p.P[g];
-    __syncthreads();
-    double gh[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int j = 0; j <= N; ++j) {
-        gh[0] = fma(p.D[a][j], sp[j + n1 * (b + n1 * c)], gh[0]);
-        gh[1] = fma(p.D[b][j], sp[a + n1 * (j + n1 * c)], gh[1]);
-        gh[2] = fma(p.D[c][j], sp[a + n1 * (b + n1 * j)], gh[2]);
-    }
-    // Jacobian of the trilinear map at (x_a, x_b, x_c) from the monomial coefficients
-    const double xi = p.x[a], et = p.x[b], ze = p.x[c];
-    double J[3][3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        J[i][0] = cc[1][i] + cc[4][i] * et + cc[6][i] * ze + cc[7][i] * et * ze;
-        J[i][1] = cc[2][i] + cc[4][i] * xi + cc[5][i] * ze + cc[7][i] * xi * ze;
-        J[i][2] = cc[3][i] + cc[5][i] * et + cc[6][i] * xi + cc[7][i] * xi * et;
-    }
-    // adj = det J^-1 (rows: cofactors); |J| J^-1 J^-T = adj adj^T / det
-    double A[3][3];
-    A[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
-    A[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
-    A[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
-    A[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
-    A[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
-    A[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
-    A[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
-    A[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
-    A[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
-    const double det = J[0][0] * A[0][0] + J[0][1] * A[1][0] + J[0][2] * A[2][0];
-    const double sc = p.w[a] * p.w[b] * p.w[c] * p.c2 / det;
-    // flux = sc * A A^T gh  (A = adj J, rows i: A[i][:] = d xi_i / d x * det)
-    double u[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) u[i] = A[0][i] * gh[0] + A[1][i] * gh[1] + A[2][i] * gh[2];   // A^T gh
-#pragma unroll
-    for (int i = 0; i < 3; ++i) sf[i][t] = sc * (A[i][0] * u[0] + A[i][1] * u[1] + A[i][2] * u[2]);
-    __syncthreads();
-    double rx = 0.0, ry = 0.0, rz = 0.0;   // three independent chains
-#pragma unroll
-    for (int j = 0; j <= N; ++j) {
-        rx = fma(p.D[j][a], sf[0][j + n1 * (b + n1 * c)], rx);
-        ry = fma(p.D[j][b], sf[1][a + n1 * (j + n1 * c)], ry);
-        rz = fma(p.D[j][c], sf[2][a + n1 * (b + n1 * j)], rz);
-    }
-    atomicAdd(p.res + g, rx + ry + rz);
+    return ((long long)(N * ez + c) * p.NY + (N * ey + b)) * p.PX + (N * ex + a);
 }
 
-__global__ void curved_update_kernel(const __grid_constant__ CurvedParams p) {
-    const long long ix = (long long)blockIdx.x * blockDim.x + threadIdx.x;   // 2D grid: x, lattice row
-    if (ix >= p.NX) return;
-    const long long g = (long long)blockIdx.y * p.PX + ix;
-    // every load before the first store (the pointers may alias as far as the compiler knows)
-    const double wv = p.W[g], mi = p.minv[g], r = p.res[g], cd = p.cdamp[g], pv = p.P[g];
-    const double a = -mi * r - cd * wv;
-    const double wn = fma(p.dt, a, wv);
-    p.res[g] = 0.0;
-    p.W[g] = wn;
-    p.Pn[g] = fma(p.dt, wn, pv);
+// elements per block: up to 256 threads; dynamic shared memory: two staging buffers of the element
+// pressures, two flux arrays, two vertex buffers and D
+template <int N>
+constexpr int curved_epb() {
+    constexpr int by_threads = 256 / ((N + 1) * (N + 1));
+    constexpr int by_smem = 100000 / (32 * (N + 1) * (N + 1) * (N + 1) + 384);
+    constexpr int e = by_threads < by_smem ? by_threads : by_smem;
+    return e > 1 ? e : 1;
 }
+template <int N>
+constexpr int curved_threads() { return curved_epb<N>() * (N + 1) * (N + 1); }
+template <int N>
+constexpr int curved_smem() { return 8 * (curved_epb<N>() * (4 * (N + 1) * (N + 1) * (N + 1) + 48) + (N + 1) * (N + 1)); }
+#ifndef SEM_CV_MINB
+#define SEM_CV_MINB 2
+#endif
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int N>
+__global__ void __launch_bounds__(curved_threads<N>(), SEM_CV_MINB) curved_residual_kernel(const __grid_constant__ CurvedParams p) {
+    constexpr int n1 = N + 1, NL = n1 * n1, nl = n1 * NL, EPB = curved_epb<N>();
+    const auto& RT = kRef<N>;
+    extern __shared__ __align__(16) double cv_smem[];
+    double* const spb = cv_smem;                          // [2][EPB][nl] staged pressures
+    double* const sf1 = spb + 2 * EPB * nl;               // [EPB][nl] eta flux
+    double* const sf2 = sf1 + EPB * nl;                   // [EPB][nl] zeta flux
+    double* const Xvb = sf2 + EPB * nl;                   // [2][EPB][24] vertices
+    double* const Ds = Xvb + 2 * EPB * 24;                // [n1][n1]
+    const int t = threadIdx.x;
+    const int el = t / NL, ln = t - el * NL, b = ln % n1, c = ln / n1;
+    const int nel = p.nelx * p.nely * p.nelz;
+    const int ngroups = (nel + EPB - 1) / EPB;
+    for (int q = t; q < NL; q += blockDim.x) Ds[q] = p.D[q / n1][q % n1];
+    const double xb = p.x[b], xc = p.x[c];
+    const double wbc = p.w[b] * p.w[c] * p.c2;
+    const double ly0 = 0.5 * (1.0 - xb), ly1 = 0.5 * (1.0 + xb);
+    const double lz0 = 0.5 * (1.0 - xc), lz1 = 0.5 * (1.0 + xc);
+    // stage group g's line of this thread and its element's vertices into buffer k (async)
+    auto stage = [&](int g, int k) -> long long {
+        const int e = g * EPB + el;
+        if (g >= ngroups || e >= nel) return -1;
+        const long long g0 = curved_node<N>(p, e, 0, b, c);
+        double* dst = spb + (k * EPB + el) * nl + n1 * ln;
+#pragma unroll
+        for (int a = 0; a <= N; ++a) cp_async8(dst + a, p.P + g0 + a);
+        const int ex = e % p.nelx, ey = (e / p.nelx) % p.nely, ez = e / (p.nelx * p.nely);
+        for (int q = ln; q < 24; q += NL) {
+            const int v = q / 3, i = q - 3 * v;
+            const int vx = ex + (v & 1), vy = ey + ((v >> 1) & 1), vz = ez + (v >> 2);
+            cp_async8(Xvb + (k * EPB + el) * 24 + q,
+                      p.vlat + 3 * ((size_t)vx + (size_t)(p.nelx + 1) * ((size_t)vy + (size_t)(p.nely + 1) * vz)) + i);
+        }
+        return g0;
+    };
+    int gi = blockIdx.x, k = 0;
+    long long g0 = stage(gi, 0);
+    cp_async_commit();
+    for (; gi < ngroups; gi += gridDim.x, k ^= 1) {
+        cp_async_wait_all();
+        __syncthreads();
+        const long long gnext = stage(gi + gridDim.x, k ^ 1);   // overlaps this group's arithmetic
+        cp_async_commit();
+        const double* sp = spb + (k * EPB + el) * nl;
+        const double* Xv = Xvb + (k * EPB + el) * 24;
+        // ---- reference gradient on the line
+        double cur[n1], gx[n1], gy[n1], gz[n1];
+#pragma unroll
+        for (int a = 0; a <= N; ++a) cur[a] = sp[a + n1 * ln];
+#pragma unroll
+        for (int a = 0; a <= N; ++a) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j <= N; ++j) s = fma(RT.D[a][j], cur[j], s);
+            gx[a] = s;
+            gy[a] = 0.0;
+            gz[a] = 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j <= N; ++j) {
+            const double dyj = Ds[b * n1 + j], dzj = Ds[c * n1 + j];
+#pragma unroll
+            for (int a = 0; a <= N; ++a) {
+                gy[a] = fma(dyj, sp[a + n1 * (j + n1 * c)], gy[a]);
+                gz[a] = fma(dzj, sp[a + n1 * (b + n1 * j)], gz[a]);
+            }
+        }
+        // ---- Jacobian pieces of the line: J[:,0] constant, J[:,1] = P1 + xi Q1, J[:,2] = P2 + xi Q2
+        double J0[3], P1[3], Q1[3], P2[3], Q2[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double X0 = Xv[i], X1 = Xv[3 + i], X2 = Xv[6 + i], X3 = Xv[9 + i];
+            const double X4 = Xv[12 + i], X5 = Xv[15 + i], X6 = Xv[18 + i], X7 = Xv[21 + i];
+            // x-edges k = (v1, v2): corners (2k, 2k+1); s_k = mean, h_k = half difference
+            const double h0 = 0.5 * (X1 - X0), h1 = 0.5 * (X3 - X2), h2 = 0.5 * (X5 - X4), h3 = 0.5 * (X7 - X6);
+            const double s0 = 0.5 * (X1 + X0), s1 = 0.5 * (X3 + X2), s2 = 0.5 * (X5 + X4), s3 = 0.5 * (X7 + X6);
+            J0[i] = fma(lz1, fma(ly1, h3, ly0 * h2), lz0 * fma(ly1, h1, ly0 * h0));
+            P1[i] = 0.5 * fma(lz1, s3 - s2, lz0 * (s1 - s0));
+            Q1[i] = 0.5 * fma(lz1, h3 - h2, lz0 * (h1 - h0));
+            P2[i] = 0.5 * fma(ly1, s3 - s1, ly0 * (s2 - s0));
+            Q2[i] = 0.5 * fma(ly1, h3 - h1, ly0 * (h2 - h0));
+        }
+        double f0[n1];
+        double* const f1 = sf1 + el * nl;
+        double* const f2 = sf2 + el * nl;
+#pragma unroll
+        for (int a = 0; a <= N; ++a) {
+            const double xa = RT.x[a];
+            double J[3][3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                J[i][0] = J0[i];
+                J[i][1] = fma(xa, Q1[i], P1[i]);
+                J[i][2] = fma(xa, Q2[i], P2[i]);
+            }
+            // adj = det J^-1 (rows: cofactors); |J| J^-1 J^-T = adj adj^T / det
+            double A[3][3];
+            A[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+            A[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+            A[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+            A[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+            A[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+            A[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+            A[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+            A[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+            A[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+            const double det = J[0][0] * A[0][0] + J[0][1] * A[1][0] + J[0][2] * A[2][0];
+            const double sc = RT.w[a] * wbc / det;
+            double u[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) u[i] = A[0][i] * gx[a] + A[1][i] * gy[a] + A[2][i] * gz[a];   // A^T gh
+            f0[a] = sc * (A[0][0] * u[0] + A[0][1] * u[1] + A[0][2] * u[2]);
+            f1[a + n1 * ln] = sc * (A[1][0] * u[0] + A[1][1] * u[1] + A[1][2] * u[2]);
+            f2[a + n1 * ln] = sc * (A[2][0] * u[0] + A[2][1] * u[1] + A[2][2] * u[2]);
+        }
+        __syncthreads();
+        // ---- D^T: x part on the line's registers, y and z parts from the other lines
+        double r[n1];
+#pragma unroll
+        for (int a = 0; a <= N; ++a) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j <= N; ++j) s = fma(RT.D[j][a], f0[j], s);
+            r[a] = s;
+        }
+#pragma unroll
+        for (int j = 0; j <= N; ++j) {
+            const double dyj = Ds[j * n1 + b], dzj = Ds[j * n1 + c];
+#pragma unroll
+            for (int a = 0; a <= N; ++a) {
+                r[a] = fma(dyj, f1[a + n1 * (j + n1 * c)], r[a]);
+                r[a] = fma(dzj, f2[a + n1 * (b + n1 * j)], r[a]);
+            }
+        }
+        if (g0 >= 0) {
+#pragma unroll
+            for (int a = 0; a <= N; ++a) atomicAdd(p.res + g0 + a, r[a]);
+        }
+        g0 = gnext;
+    }
+    cp_async_wait_all();
+}
+
+static int device_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms < 1) sms = 1;
+    }
+    return sms;
+}
+
+int curved_grid(int N, int nel) {
+    static int per_sm[kMaxN + 1] = {};
+    const int sms = device_sms();
+    if (N < 1 || N > kMaxN) return 1;
+    int epb = 1;
+    switch (N) {
+#define SEM_CV_OCC(n)                                                                                      \
+    case n:                                                                                                \
+        epb = curved_epb<n>();                                                                             \
+        if (!per_sm[n]) {                                                                                  \
+            cudaFuncSetAttribute(curved_residual_kernel<n>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                 curved_smem<n>());                                                         \
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[n], curved_residual_kernel<n>,             \
+                                                          curved_threads<n>(), curved_smem<n>());           \
+        }                                                                                                  \
+        break;
+        SEM_CV_OCC(1) SEM_CV_OCC(2) SEM_CV_OCC(3) SEM_CV_OCC(4)
+        SEM_CV_OCC(5) SEM_CV_OCC(6) SEM_CV_OCC(7) SEM_CV_OCC(8)
+#undef SEM_CV_OCC
+        default: break;
+    }
+    if (per_sm[N] < 1) per_sm[N] = 1;
+    const long long groups = ((long long)nel + epb - 1) / epb;
+    const long long g = (long long)sms * per_sm[N];
+    return (int)(g < groups ? g : (groups > 0 ? groups : 1));
+}
+
+// Nodal kick-drift of a curved box as one flat stream over the padded lattice (16-byte accesses,
+// grid-stride over 8 resident blocks per SM -- the register cap keeps all of them resident, a second
+// wave of blocks would double the time): pad entries carry minv = cdamp = res = 0 and w = p = 0.
+__global__ void __launch_bounds__(256, 8) curved_update_kernel(const __grid_constant__ CurvedParams p) {
+    const long long n2 = p.PX * p.NY * p.NZ / 2;   // PX is a multiple of 8
+    const double2* __restrict__ W2 = reinterpret_cast<const double2*>(p.W);
+    const double2* __restrict__ M2 = reinterpret_cast<const double2*>(p.minv);
+    const double2* __restrict__ R2 = reinterpret_cast<const double2*>(p.res);
+    const double2* __restrict__ C2 = reinterpret_cast<const double2*>(p.cdamp);
+    const double2* __restrict__ P2 = reinterpret_cast<const double2*>(p.P);
+#pragma unroll 1
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+        // read-only (non-coherent) loads: each element is read once, before this thread overwrites it
+        const double2 wv = __ldg(W2 + i), mi = __ldg(M2 + i), r = __ldg(R2 + i), cd = __ldg(C2 + i), pv = __ldg(P2 + i);
+        double2 wn, pn;
+        wn.x = fma(p.dt, -mi.x * r.x - cd.x * wv.x, wv.x);
+        wn.y = fma(p.dt, -mi.y * r.y - cd.y * wv.y, wv.y);
+        pn.x = fma(p.dt, wn.x, pv.x);
+        pn.y = fma(p.dt, wn.y, pv.y);
+        reinterpret_cast<double2*>(p.res)[i] = make_double2(0.0, 0.0);
+        reinterpret_cast<double2*>(p.W)[i] = wn;
+        reinterpret_cast<double2*>(p.Pn)[i] = pn;
+    }
+}
+
 
 void launch_curved(const CurvedParams& p, cudaStream_t s) {
-    const int nel = p.nelx * p.nely * p.nelz;
     switch (p.N) {
-#define SEM_CV_CASE(n) case n: curved_residual_kernel<n><<<nel, (n + 1) * (n + 1) * (n + 1), 0, s>>>(p); break;
+#define SEM_CV_CASE(n) case n: curved_residual_kernel<n><<<p.grid, curved_threads<n>(), curved_smem<n>(), s>>>(p); break;
         SEM_CV_CASE(1) SEM_CV_CASE(2) SEM_CV_CASE(3) SEM_CV_CASE(4)
         SEM_CV_CASE(5) SEM_CV_CASE(6) SEM_CV_CASE(7) SEM_CV_CASE(8)
 #undef SEM_CV_CASE
         default: break;
     }
-    curved_update_kernel<<<dim3((unsigned)((p.NX + 127) / 128), (unsigned)(p.NY * p.NZ)), 128, 0, s>>>(p);
+    const long long n2 = p.PX * p.NY * p.NZ / 2;
+    const long long want = (n2 + 255) / 256, cap = 8LL * device_sms();
+    curved_update_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(p);
 }
 
 __global__ void step_bump_kernel(long long* step) { *step += 1; }

@@ -476,6 +476,7 @@ sem::CurvedParams curved_params(sem_ctx* ctx, Box& b, int cur) {
     p.nelx = b.d.nel[0];
     p.nely = b.d.nel[1];
     p.nelz = b.d.nel[2];
+    p.grid = sem::curved_grid(b.N, p.nelx * p.nely * p.nelz);
     p.vlat = b.vlat;
     p.P = b.P[cur];
     p.res = b.res;

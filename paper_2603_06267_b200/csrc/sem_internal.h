@@ -196,6 +196,7 @@ struct CurvedParams {
     int N;
     long long NX, NY, NZ, PX;
     int nelx, nely, nelz;
+    int grid;                        // persistent residual-kernel blocks (curved_grid)
     const double* __restrict__ vlat;
     const double* __restrict__ P;    // p^{n+1}
     double* res;
@@ -370,6 +371,7 @@ void launch_fill_random(double* p, double* w, double* pn, long long NX, long lon
 void launch_cut_partial(const CutBatch& B, cudaStream_t s);
 void launch_pml_elements(const PmlParams& p, cudaStream_t s);
 void launch_curved(const CurvedParams& p, cudaStream_t s);
+int curved_grid(int N, int nel);   // resident blocks of the curved residual kernel on this device
 void launch_step_bump(long long* step, cudaStream_t s);
 void launch_pml_fixup(const PmlParams& p, cudaStream_t s);
 void launch_cut_fixup(const CutBatch& B, cudaStream_t s);
