@@ -1013,6 +1013,13 @@ void launch_cut_fixup(const CutBatch& B, cudaStream_t s) {
     if (B.n > 0) cut_fixup_kernel<<<dim3(cut_blocks(B, false), B.n), 256, 0, s>>>(B);
 }
 
+// 8-byte asynchronous global -> shared copies (LDGSTS), used to stage element data
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ------------------------------------------------------------------------------------------------
 // PML (Eq. 1; readings R23-R25): one block per PML element, one thread per
 // element GLL node.  psi^{n+3/2} = psi^{n+1/2} + dt p^{n+1}; element-local grad p^{n+1}, grad psi^{n+1};
@@ -1032,8 +1039,15 @@ constexpr int pml_minb() { return N <= 3 ? 4 : (N <= 5 ? 3 : (N == 6 ? 2 : 1)); 
 template <int N>
 __global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1), pml_minb<N>()) pml_element_kernel(const __grid_constant__ PmlParams p) {
     constexpr int n1 = N + 1, nl = n1 * n1 * n1, EPB = pml_epb<N>();
-    __shared__ double sp_[EPB][nl], ss_[EPB][nl], sf_[EPB][3][nl];
+    __shared__ double sp_[EPB][nl], ss_[EPB][nl], sf_[EPB][3][nl], Ds[n1 * n1], DWs[n1 * n1], Ws[n1];
     const int el = threadIdx.x / nl, t = threadIdx.x - el * nl;
+    // D[i][j] and w_i D[i][j] in shared memory: lane-dependent indices into the parameter bank would
+    // serialise (one constant-cache access per distinct address)
+    for (int q = threadIdx.x; q < n1 * n1; q += blockDim.x) {
+        Ds[q] = p.D[q / n1][q % n1];
+        DWs[q] = p.w[q / n1] * p.D[q / n1][q % n1];
+        if (q < n1) Ws[q] = p.w[q];
+    }
     double* sp = sp_[el];
     double* ss = ss_[el];
     double (&sf)[3][nl] = sf_[el];
@@ -1069,12 +1083,13 @@ __global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1), pm
 #pragma unroll
     for (int j = 0; j <= N; ++j) {
         const int ix = j + n1 * (b + n1 * c), iy = a + n1 * (j + n1 * c), iz = a + n1 * (b + n1 * j);
-        gp[0] = fma(p.D[a][j], sp[ix], gp[0]);
-        gs[0] = fma(p.D[a][j], ss[ix], gs[0]);
-        gp[1] = fma(p.D[b][j], sp[iy], gp[1]);
-        gs[1] = fma(p.D[b][j], ss[iy], gs[1]);
-        gp[2] = fma(p.D[c][j], sp[iz], gp[2]);
-        gs[2] = fma(p.D[c][j], ss[iz], gs[2]);
+        const double dx = Ds[a * n1 + j], dy = Ds[b * n1 + j], dz = Ds[c * n1 + j];
+        gp[0] = fma(dx, sp[ix], gp[0]);
+        gs[0] = fma(dx, ss[ix], gs[0]);
+        gp[1] = fma(dy, sp[iy], gp[1]);
+        gs[1] = fma(dy, ss[iy], gs[1]);
+        gp[2] = fma(dz, sp[iz], gp[2]);
+        gs[2] = fma(dz, ss[iz], gs[2]);
     }
     const double alpha = z[0] + z[1] + z[2];
     const double beta = z[0] * z[1] + z[1] * z[2] + z[2] * z[0];
@@ -1093,12 +1108,12 @@ __global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1), pm
     double rx = 0.0, ry = 0.0, rz = 0.0;
 #pragma unroll
     for (int j = 0; j <= N; ++j) {
-        rx = fma(p.w[j] * p.D[j][a], sf[0][j + n1 * (b + n1 * c)], rx);
-        ry = fma(p.w[j] * p.D[j][b], sf[1][a + n1 * (j + n1 * c)], ry);
-        rz = fma(p.w[j] * p.D[j][c], sf[2][a + n1 * (b + n1 * j)], rz);
+        rx = fma(DWs[j * n1 + a], sf[0][j + n1 * (b + n1 * c)], rx);
+        ry = fma(DWs[j * n1 + b], sf[1][a + n1 * (j + n1 * c)], ry);
+        rz = fma(DWs[j * n1 + c], sf[2][a + n1 * (b + n1 * j)], rz);
     }
-    const double r = p.jac * (p.s2h[0] * p.w[b] * p.w[c] * rx + p.s2h[1] * p.w[a] * p.w[c] * ry +
-                              p.s2h[2] * p.w[a] * p.w[b] * rz);
+    const double wa = Ws[a], wb = Ws[b], wc = Ws[c];
+    const double r = p.jac * (p.s2h[0] * wb * wc * rx + p.s2h[1] * wa * wc * ry + p.s2h[2] * wa * wb * rz);
     double da = -r * minv;
     // nodal terms once per node: by the element that owns it (lowest element index containing the node;
     // a non-PML owner only occurs where all z vanish)
@@ -1183,11 +1198,6 @@ constexpr int curved_smem() { return 8 * (curved_epb<N>() * (4 * (N + 1) * (N + 
 #define SEM_CV_MINB 2
 #endif
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int N>
 __global__ void __launch_bounds__(curved_threads<N>(), SEM_CV_MINB) curved_residual_kernel(const __grid_constant__ CurvedParams p) {

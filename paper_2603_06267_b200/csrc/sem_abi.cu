@@ -1233,6 +1233,7 @@ sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size
     if (dalloc(ctx, &b.res, (size_t)b.nalloc())) return SEM_E_OOM;
     CU(cudaMemset(b.res, 0, (size_t)b.nalloc() * sizeof(double)));
     b.curved = true;
+    sem::curved_grid(b.N, b.d.nel[0] * b.d.nel[1] * b.d.nel[2]);   // occupancy query + smem opt-in, outside any capture
     drop_graphs(ctx);
     CU(cudaStreamSynchronize(ctx->stream));
     return SEM_OK;
