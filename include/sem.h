@@ -157,6 +157,19 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
  * Jacobian at a GLL point), SEM_E_STATE, SEM_E_OOM. */
 sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size_t n_verts);
 
+/* Rigid obstacle inside box `box` ("obstacle Neumann surfaces"): solid[n_el],
+ * n_el = nel_x nel_y nel_z, element (ex,ey,ez) at index ex + nel_x (ey + nel_y ez); solid[e] != 0
+ * removes element e from the fluid domain Omega.  The faces it shares with fluid elements become
+ * Neumann (rigid) surfaces -- the natural boundary condition of the weak form, Eq. (4) with no
+ * boundary term there -- so nothing is assembled for them: the element's stiffness, mass and
+ * absorbing-face terms are skipped.  Nodes of no fluid element (obstacle interiors) are held at 0
+ * (sem_read_pressure returns 0 there after the first step).  The box moves to the element-scatter
+ * path of sem_box_set_vertices (with its own affine vertex lattice unless vertices are set, before or
+ * after this call) and carries the same restrictions: no PMUT / interface / PML / plane wave
+ * (SEM_E_STATE), world 1 only (SEM_E_PARTITION).  Caller owns `solid` (copied).  Errors: SEM_E_ARG
+ * (size, every element solid), SEM_E_STATE (already set), SEM_E_OOM. */
+sem_status sem_box_set_obstacle(sem_ctx* ctx, int box, const unsigned char* solid, size_t n_el);
+
 /* Perfectly matched layer (Eq. 1 lines 1-3; coefficients P:L271-277; profile P:L280-289)
  * inside box `box`: thickness[f] [m] for faces f = -x,+x,-y,+y,-z,+z (0 = no layer) is the slab of the
  * box next to face f; z_d(d) = zt (d/l - sin(2 pi d/l)/(2 pi)), d = depth into the layer,

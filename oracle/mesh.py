@@ -86,6 +86,19 @@ class Box:
         self.vlat = None if v is None else np.asarray(v, dtype=np.float64).reshape(-1, 3)
         if self.vlat is not None and len(self.vlat) != (self.nel[0] + 1) * (self.nel[1] + 1) * (self.nel[2] + 1):
             raise ValueError("vertex lattice size mismatch")
+        # obstacle: "solid" elements are removed from the fluid domain Omega, so
+        # their faces towards the fluid are Neumann (rigid) surfaces: the natural boundary condition of
+        # the weak form (Eq. 4 with no boundary term) -- nothing is assembled for them.
+        sol = desc.get("solid")
+        self.solid = np.zeros(self.nelem, dtype=bool)
+        if sol is not None:
+            sol = np.asarray(sol)
+            if sol.dtype == bool:
+                if sol.shape != (self.nelem,):
+                    raise ValueError("solid mask size mismatch")
+                self.solid = sol.copy()
+            else:
+                self.solid[sol.astype(np.int64)] = True
 
     # --- lattice / numbering -------------------------------------------------
     def gid(self, gx, gy, gz):
@@ -140,6 +153,10 @@ class Box:
         d, side = face // 2, face % 2
         ec = self.elem_coords(np.arange(self.nelem))[d]
         return list(np.nonzero(ec == (self.nel[d] - 1 if side else 0))[0])
+
+    def fluid_boundary_faces(self, face):
+        """boundary_faces(face) without the solid (obstacle) elements."""
+        return [e for e in self.boundary_faces(face) if not self.solid[e]]
 
 
 def face_local_nodes(N, face):

@@ -45,6 +45,13 @@ def voltage(pm, t, q):
     return (q * pm["eta"][None, :]).sum(axis=1) / pm["capacitance"]
 
 
+def _div_mass(r, M):
+    """M^-1 r for the lumped mass; nodes outside the fluid (M = 0, obstacle interiors) get 0."""
+    out = np.zeros_like(r)
+    np.divide(r, M, out=out, where=M > 0)
+    return out
+
+
 class Newmark:
     """State and loop of Algorithm 1 for a ``operators.System``."""
 
@@ -105,12 +112,16 @@ class Newmark:
             qd1 = qd1 + 0.5 * dt * qdd1
             f += s.pmut_force(qdd1)
         f += s.plane_wave_load(tn1)
+        inactive = ~s.active                                  # obstacle interiors (no fluid element)
+        if inactive.any():
+            p1[inactive] = 0.0
+            pd1[inactive] = 0.0
         if self.pml is None:
-            pdd1 = (f - s.apply_K(p1) - s.C * pd1) / s.M
+            pdd1 = _div_mass(f - s.apply_K(p1) - s.C * pd1, s.M)
         else:   # R25: PML terms at the predictor velocity, psi^{n+1} and Phi^{n+1}
             rB, psi1 = self.pml.advance(p1, dt)
             pm_ = self.pml
-            pdd1 = ((f - s.apply_K(p1) - s.C * pd1 - rB) / s.M
+            pdd1 = (_div_mass(f - s.apply_K(p1) - s.C * pd1 - rB, s.M)
                     - pm_.alpha * pd1 - pm_.beta * p1 - pm_.gamma * psi1)
         pd1 = pd1 + 0.5 * dt * pdd1
         self.p, self.pd, self.pdd = p1, pd1, pdd1

@@ -125,6 +125,9 @@ class System:
         self.offsets = np.cumsum([0] + [b.ndof for b in self.boxes])
         self.ndof = int(self.offsets[-1])
         self._build_volume()
+        # nodes of the fluid (every node when there is no obstacle): the others have no mass, no
+        # stiffness row and stay 0
+        self.active = self.M > 0
         self._build_abc()
         self._build_pmut(rec.get("pmut"))
         self._build_interface(rec.get("interface"))
@@ -139,12 +142,15 @@ class System:
             cache = {}
             keys = np.empty(box.nelem, dtype=np.int64)
             for e in range(box.nelem):
+                if box.solid[e]:          # obstacle element: not part of the fluid (nothing assembled)
+                    keys[e] = -1
+                    continue
                 v = box.vertices(e)
                 k = _shape_key(v)
                 if k not in cache:
                     cache[k] = (len(cache), element_stiffness(v, box.N, box.c), element_mass(v, box.N))
                 keys[e] = cache[k][0]
-            mats = sorted(cache.values())
+            mats = sorted(cache.values(), key=lambda m: m[0])
             for kid, Ke, Me in mats:
                 sel = np.nonzero(keys == kid)[0]
                 np.add.at(self.M, conn[sel].ravel(), np.tile(Me, len(sel)))
@@ -165,7 +171,7 @@ class System:
                 if box.bc[face] != BC_ABSORBING:
                     continue
                 conn = box.connectivity() + self.offsets[bi]
-                for e in box.boundary_faces(face):
+                for e in box.fluid_boundary_faces(face):
                     ids, _, _, wq, _ = face_quadrature(box.vertices(e), box.N, face)
                     np.add.at(self.C, conn[e, ids], box.c * wq)
 

@@ -10,5 +10,5 @@ from .sem import (  # noqa: F401
     sem_dg_interface_build, sem_destroy, sem_fill_random_state, sem_kernel_time, sem_last_launch_count,
     sem_mesh_create, sem_plane_wave_source, sem_pmut_attach, sem_query, sem_read_modal, sem_read_pressure,
     sem_read_pressure_at, sem_set_profiling, sem_step, sem_sync, sem_write_state, sem_pml_attach, sem_face_match,
-    sem_box_set_vertices,
+    sem_box_set_vertices, sem_box_set_obstacle,
 )

@@ -1222,6 +1222,7 @@ __global__ void __launch_bounds__(curved_threads<N>(), SEM_CV_MINB) curved_resid
     auto stage = [&](int g, int k) -> long long {
         const int e = g * EPB + el;
         if (g >= ngroups || e >= nel) return -1;
+        if (p.solid && p.solid[e]) return -1;   // obstacle element: no contribution
         const long long g0 = curved_node<N>(p, e, 0, b, c);
         double* dst = spb + (k * EPB + el) * nl + n1 * ln;
 #pragma unroll
@@ -1400,6 +1401,9 @@ __global__ void __launch_bounds__(256, 8) curved_update_kernel(const __grid_cons
         wn.y = fma(p.dt, -mi.y * r.y - cd.y * wv.y, wv.y);
         pn.x = fma(p.dt, wn.x, pv.x);
         pn.y = fma(p.dt, wn.y, pv.y);
+        // nodes of no fluid element (obstacle interiors, lattice padding) have M^-1 = 0: held at 0
+        if (mi.x == 0.0) wn.x = pn.x = 0.0;
+        if (mi.y == 0.0) wn.y = pn.y = 0.0;
         reinterpret_cast<double2*>(p.res)[i] = make_double2(0.0, 0.0);
         reinterpret_cast<double2*>(p.W)[i] = wn;
         reinterpret_cast<double2*>(p.Pn)[i] = pn;
@@ -1436,6 +1440,21 @@ void launch_set_state(const double* pprev, double* pcur, const double* w, long l
                       double dt, cudaStream_t s) {
     const long long n = NX * rows;
     set_state_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pprev, pcur, w, NX, PX, rows, dt);
+}
+
+// Obstacle boxes: nodes of no fluid element (M^-1 = 0) are held at 0 (include/sem.h)
+__global__ void zero_inactive_kernel(double* p0, double* p1, double* w, const double* minv, long long NX, long long PX,
+                                     long long rows) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= NX * rows) return;
+    const long long d = (i / NX) * PX + i % NX;
+    if (minv[d] == 0.0) p0[d] = p1[d] = w[d] = 0.0;
+}
+
+void launch_zero_inactive(double* p0, double* p1, double* w, const double* minv, long long NX, long long PX,
+                          long long rows, cudaStream_t s) {
+    const long long n = NX * rows;
+    zero_inactive_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p0, p1, w, minv, NX, PX, rows);
 }
 
 __global__ void gather_kernel(const double* src, const long long* idx, long long n, double* out) {

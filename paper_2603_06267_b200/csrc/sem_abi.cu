@@ -477,6 +477,7 @@ sem::CurvedParams curved_params(sem_ctx* ctx, Box& b, int cur) {
     p.nely = b.d.nel[1];
     p.nelz = b.d.nel[2];
     p.grid = sem::curved_grid(b.N, p.nelx * p.nely * p.nelz);
+    p.solid = b.solid;
     p.vlat = b.vlat;
     p.P = b.P[cur];
     p.res = b.res;
@@ -1164,30 +1165,22 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
     return SEM_OK;
 }
 
-sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size_t n_verts) {
-    sem_status st = check_ctx(ctx);
-    if (st) return st;
-    if (box < 0 || box >= (int)ctx->gdesc.size() || !verts) return fail(ctx, SEM_E_ARG, "bad box / vertices");
-    if (ctx->world > 1 || ctx->parts.size() != 1)
-        return fail(ctx, SEM_E_PARTITION, "curved boxes are implemented for a single slab (world 1) only");
-    sem::Part& pt = ctx->parts[0];
-    Box& b = pt.boxes[box];
-    const sem_box_desc& g = ctx->gdesc[box];
-    if (b.curved) return fail(ctx, SEM_E_STATE, "vertices already set");
-    if ((pt.pm.on && pt.pm.box == box) || b.iface_side != 0 || (pt.pml.on && pt.pml.box == box) ||
-        (ctx->pw.on && ctx->pw.box == box))
-        return fail(ctx, SEM_E_STATE, "curved boxes carry no PMUT / interface / PML / plane wave (set vertices first)");
-    const int nx = g.nel[0] + 1, ny = g.nel[1] + 1, nz = g.nel[2] + 1;
-    if (n_verts != (size_t)nx * ny * nz) return fail(ctx, SEM_E_ARG, "n_verts must be (nel_x+1)(nel_y+1)(nel_z+1)");
-    const int N = b.N, n1 = N + 1;
+// Element-scatter setup of a box (curved vertex lattice and/or obstacle): assembled lumped mass and
+// ABC diagonal over the fluid elements from b.vlat_h / b.solid_h, device copies, kernel occupancy.
+sem_status curved_setup(sem_ctx* ctx, Box& b, const sem_box_desc& g) {
+    const int nx = g.nel[0] + 1, ny = g.nel[1] + 1;
     std::vector<double> x, w;
-    gll_rule(N, x, w);
+    gll_rule(b.N, x, w);
+    const int N = b.N;
     // assembled lumped mass (sum_e w_q |det J|) and ABC diagonal (sum_F c w_s w_t |J_s|), Eq. 8
     std::vector<double> M((size_t)b.nalloc(), 0.0), Cd((size_t)b.nalloc(), 0.0);
+    const double* verts = b.vlat_h.data();
     auto vtx = [&](int vx, int vy, int vz, int i) { return verts[3 * ((size_t)vx + (size_t)nx * ((size_t)vy + (size_t)ny * vz)) + i]; };
     for (int ez = 0; ez < g.nel[2]; ++ez)
         for (int ey = 0; ey < g.nel[1]; ++ey)
-            for (int ex = 0; ex < g.nel[0]; ++ex)
+            for (int ex = 0; ex < g.nel[0]; ++ex) {
+                if (!b.solid_h.empty() && b.solid_h[(size_t)ex + (size_t)g.nel[0] * ((size_t)ey + (size_t)g.nel[1] * ez)])
+                    continue;   // obstacle element: not part of the fluid
                 for (int c = 0; c <= N; ++c)
                     for (int bb = 0; bb <= N; ++bb)
                         for (int a = 0; a <= N; ++a) {
@@ -1222,21 +1215,92 @@ sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size
                                 Cd[gi] += g.c * w[loc[t0]] * w[loc[t1]] * std::sqrt(cx * cx + cy * cy + cz * cz);
                             }
                         }
+            }
     for (size_t i = 0; i < M.size(); ++i) {
         if (M[i] > 0.0) {
             Cd[i] /= M[i];
             M[i] = 1.0 / M[i];
         }
     }
-    std::vector<double> V(verts, verts + 3 * n_verts);
-    if (upload(ctx, &b.vlat, V) || upload(ctx, &b.minv, M) || upload(ctx, &b.cdamp, Cd)) return SEM_E_CUDA;
-    if (dalloc(ctx, &b.res, (size_t)b.nalloc())) return SEM_E_OOM;
-    CU(cudaMemset(b.res, 0, (size_t)b.nalloc() * sizeof(double)));
+    auto put = [&](double** d, const std::vector<double>& h) -> sem_status {
+        if (!*d) return upload(ctx, d, h);
+        CU(cudaMemcpy(*d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+        return SEM_OK;
+    };
+    if (put(&b.vlat, b.vlat_h) || put(&b.minv, M) || put(&b.cdamp, Cd)) return SEM_E_CUDA;
+    if (!b.solid_h.empty()) {
+        if (!b.solid && dalloc(ctx, &b.solid, b.solid_h.size())) return SEM_E_OOM;
+        CU(cudaMemcpy(b.solid, b.solid_h.data(), b.solid_h.size(), cudaMemcpyHostToDevice));
+    }
+    if (!b.res) {
+        if (dalloc(ctx, &b.res, (size_t)b.nalloc())) return SEM_E_OOM;
+        CU(cudaMemset(b.res, 0, (size_t)b.nalloc() * sizeof(double)));
+    }
     b.curved = true;
-    sem::curved_grid(b.N, b.d.nel[0] * b.d.nel[1] * b.d.nel[2]);   // occupancy query + smem opt-in, outside any capture
+    sem::curved_grid(b.N, g.nel[0] * g.nel[1] * g.nel[2]);   // occupancy query + smem opt-in, outside any capture
     drop_graphs(ctx);
     CU(cudaStreamSynchronize(ctx->stream));
     return SEM_OK;
+}
+
+// shared checks of sem_box_set_vertices / sem_box_set_obstacle
+sem_status scatter_box_check(sem_ctx* ctx, int box, const void* data, const char* what) {
+    sem_status st = check_ctx(ctx);
+    if (st) return st;
+    if (box < 0 || box >= (int)ctx->gdesc.size() || !data) return fail(ctx, SEM_E_ARG, std::string("bad box / ") + what);
+    if (ctx->world > 1 || ctx->parts.size() != 1)
+        return fail(ctx, SEM_E_PARTITION, "curved / obstacle boxes are implemented for a single slab (world 1) only");
+    sem::Part& pt = ctx->parts[0];
+    if ((pt.pm.on && pt.pm.box == box) || pt.boxes[box].iface_side != 0 || (pt.pml.on && pt.pml.box == box) ||
+        (ctx->pw.on && ctx->pw.box == box))
+        return fail(ctx, SEM_E_STATE, "curved / obstacle boxes carry no PMUT / interface / PML / plane wave");
+    return SEM_OK;
+}
+
+sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size_t n_verts) {
+    sem_status st = scatter_box_check(ctx, box, verts, "vertices");
+    if (st) return st;
+    Box& b = ctx->parts[0].boxes[box];
+    const sem_box_desc& g = ctx->gdesc[box];
+    if (b.verts_set) return fail(ctx, SEM_E_STATE, "vertices already set");
+    const size_t nv = (size_t)(g.nel[0] + 1) * (g.nel[1] + 1) * (g.nel[2] + 1);
+    if (n_verts != nv) return fail(ctx, SEM_E_ARG, "n_verts must be (nel_x+1)(nel_y+1)(nel_z+1)");
+    const std::vector<double> keep = b.vlat_h;
+    b.vlat_h.assign(verts, verts + 3 * n_verts);
+    st = curved_setup(ctx, b, g);
+    if (st) b.vlat_h = keep;
+    else b.verts_set = true;
+    return st;
+}
+
+sem_status sem_box_set_obstacle(sem_ctx* ctx, int box, const unsigned char* solid, size_t n_el) {
+    sem_status st = scatter_box_check(ctx, box, solid, "solid mask");
+    if (st) return st;
+    Box& b = ctx->parts[0].boxes[box];
+    const sem_box_desc& g = ctx->gdesc[box];
+    if ((long long)n_el != (long long)g.nel[0] * g.nel[1] * g.nel[2])
+        return fail(ctx, SEM_E_ARG, "n_el must be nel_x nel_y nel_z");
+    if (!b.solid_h.empty()) return fail(ctx, SEM_E_STATE, "obstacle already set");
+    size_t n_fluid = 0;
+    for (size_t e = 0; e < n_el; ++e) n_fluid += solid[e] ? 0 : 1;
+    if (n_fluid == 0) return fail(ctx, SEM_E_ARG, "every element is solid");
+    if (b.vlat_h.empty()) {   // affine box: its own vertex lattice
+        const int nx = g.nel[0] + 1, ny = g.nel[1] + 1, nz = g.nel[2] + 1;
+        b.vlat_h.resize((size_t)3 * nx * ny * nz);
+        for (int k = 0; k < nz; ++k)
+            for (int j = 0; j < ny; ++j)
+                for (int i = 0; i < nx; ++i) {
+                    const int ijk[3] = {i, j, k};
+                    for (int d = 0; d < 3; ++d)
+                        b.vlat_h[3 * ((size_t)i + (size_t)nx * ((size_t)j + (size_t)ny * k)) + d] =
+                            g.origin[d] + g.extent[d] * ijk[d] / g.nel[d];
+                }
+    }
+    b.solid_h.assign(solid, solid + n_el);
+    for (auto& v : b.solid_h) v = v ? 1 : 0;
+    st = curved_setup(ctx, b, g);
+    if (st) b.solid_h.clear();
+    return st;
 }
 
 sem_status sem_pml_attach(sem_ctx* ctx, int box, const double* thickness, double R) {
@@ -1574,6 +1638,7 @@ sem_status sem_write_state(sem_ctx* ctx, int box, const double* p, const double*
         CU(copy_slab(const_cast<double*>(p), pprev, b, ctx->gNY[box], b.gy0, 0, false, ctx->stream));
         CU(copy_slab(const_cast<double*>(pdot), b.W, b, ctx->gNY[box], b.gy0, 0, false, ctx->stream));
         sem::launch_set_state(pprev, b.P[ctx->cur], b.W, b.NX, b.PX, b.NY * b.NZ, ctx->dt, ctx->stream);
+        if (b.solid) sem::launch_zero_inactive(b.P[0], b.P[1], b.W, b.minv, b.NX, b.PX, b.NY * b.NZ, ctx->stream);
     }
     st = reset_dynamic(ctx);
     if (st) return st;
@@ -1589,6 +1654,7 @@ sem_status sem_fill_random_state(sem_ctx* ctx, int box, unsigned long long seed,
         Box& b = pt.boxes[box];
         sem::launch_fill_random(b.P[1 - ctx->cur], b.W, b.P[ctx->cur], b.NX, b.PX, b.NY, b.NZ, b.gy0, b.NYg, seed, box,
                                 ps, vs, ctx->dt, ctx->stream);
+        if (b.solid) sem::launch_zero_inactive(b.P[0], b.P[1], b.W, b.minv, b.NX, b.PX, b.NY * b.NZ, ctx->stream);
     }
     st = reset_dynamic(ctx);
     if (st) return st;

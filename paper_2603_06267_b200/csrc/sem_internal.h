@@ -197,6 +197,7 @@ struct CurvedParams {
     long long NX, NY, NZ, PX;
     int nelx, nely, nelz;
     int grid;                        // persistent residual-kernel blocks (curved_grid)
+    const unsigned char* __restrict__ solid;   // [nel] obstacle elements (skipped), or nullptr
     const double* __restrict__ vlat;
     const double* __restrict__ P;    // p^{n+1}
     double* res;
@@ -261,6 +262,10 @@ struct Box {
     double* minv = nullptr;   // pitched: inverse assembled lumped mass
     double* cdamp = nullptr;  // pitched: C_ii / M_ii on absorbing faces, 0 elsewhere
     double* res = nullptr;    // pitched: assembled K p residual (atomics), cleared by the update
+    unsigned char* solid = nullptr;            // [nel] obstacle elements (nullptr: none)
+    std::vector<double> vlat_h;                // host copy of the vertex lattice
+    bool verts_set = false;                    // sem_box_set_vertices called (else affine lattice)
+    std::vector<unsigned char> solid_h;        // host copy of the obstacle mask (empty: none)
     long long ndof() const { return NX * NY * NZ; }
     long long nalloc() const { return PX * NY * NZ; }
 };
@@ -375,6 +380,8 @@ int curved_grid(int N, int nel);   // resident blocks of the curved residual ker
 void launch_step_bump(long long* step, cudaStream_t s);
 void launch_pml_fixup(const PmlParams& p, cudaStream_t s);
 void launch_cut_fixup(const CutBatch& B, cudaStream_t s);
+void launch_zero_inactive(double* p0, double* p1, double* w, const double* minv, long long NX, long long PX,
+                          long long rows, cudaStream_t s);
 void launch_set_state(const double* pprev, double* pcur, const double* w, long long NX, long long PX, long long rows,
                       double dt, cudaStream_t s);
 void launch_gather(const double* src, const long long* idx, long long n, double* out, cudaStream_t s);

@@ -71,6 +71,7 @@ def _load():
                                   C.POINTER(C.c_double)],
         "sem_pml_attach": [P, C.c_int, C.POINTER(C.c_double), C.c_double],
         "sem_box_set_vertices": [P, C.c_int, C.POINTER(C.c_double), C.c_size_t],
+        "sem_box_set_obstacle": [P, C.c_int, C.POINTER(C.c_ubyte), C.c_size_t],
         "sem_face_match": [C.c_int, C.POINTER(FaceSet), C.POINTER(FaceSet), C.c_int, C.c_double,
                            C.POINTER(C.c_longlong), C.POINTER(C.c_double), C.POINTER(C.c_double)],
         "sem_step": [P, C.c_int],
@@ -99,7 +100,7 @@ def _load():
 LIB = _load()
 EXPORTED = ("sem_mesh_create", "sem_nccl_unique_id", "sem_slab_plan", "sem_pmut_attach", "sem_dg_interface_build",
             "sem_plane_wave_source", "sem_pml_attach", "sem_face_match", "sem_box_set_vertices",
-            "sem_step", "sem_sync", "sem_read_pressure", "sem_read_pressure_at", "sem_read_modal",
+            "sem_box_set_obstacle", "sem_step", "sem_sync", "sem_read_pressure", "sem_read_pressure_at", "sem_read_modal",
             "sem_write_state", "sem_fill_random_state", "sem_query", "sem_set_profiling", "sem_kernel_time",
             "sem_last_launch_count", "sem_last_error", "sem_destroy")
 
@@ -195,6 +196,12 @@ def sem_plane_wave_source(ctx, box, face, amp_pa, f0_hz, sigma_s, t0_s, directio
 def sem_box_set_vertices(ctx, box, verts):
     v = np.ascontiguousarray(verts, np.float64).reshape(-1, 3)
     _check(ctx, LIB.sem_box_set_vertices(ctx, int(box), _dptr(v), v.shape[0]))
+
+
+def sem_box_set_obstacle(ctx, box, solid):
+    """solid: bool / 0-1 mask of the box's nel_x nel_y nel_z elements, x fastest (include/sem.h)."""
+    m = np.ascontiguousarray(solid, np.uint8).ravel()
+    _check(ctx, LIB.sem_box_set_obstacle(ctx, int(box), m.ctypes.data_as(C.POINTER(C.c_ubyte)), m.size))
 
 
 def sem_pml_attach(ctx, box, thickness, R):
@@ -316,6 +323,13 @@ class Simulation:
             for bi, b in enumerate(rec["boxes"]):
                 if b.get("vertices") is not None:
                     sem_box_set_vertices(self.ctx, bi, b["vertices"])
+                if b.get("solid") is not None:
+                    sol = np.asarray(b["solid"])
+                    if sol.dtype != bool:
+                        mask = np.zeros(int(np.prod(b["nel"])), dtype=bool)
+                        mask[sol.astype(np.int64)] = True
+                        sol = mask
+                    sem_box_set_obstacle(self.ctx, bi, sol)
             if rec.get("pmut") is not None:
                 sem_pmut_attach(self.ctx, rec["pmut"])
             if rec.get("interface") is not None:

@@ -368,3 +368,30 @@ def curved_config(nel=(3, 3, 3), degree=4, extent=(3e-4, 3e-4, 3e-4), amp=0.12, 
     rec["dt"] = cfl_dt(boxes, cfl)
     return _finish(rec)
 
+
+
+def solid_block(nel, lo, hi):
+    """Element indices (ex + nel_x (ey + nel_y ez)) of the block lo <= (ex, ey, ez) < hi."""
+    ex, ey, ez = np.meshgrid(*[np.arange(a, b) for a, b in zip(lo, hi)], indexing="ij")
+    return np.sort((ex + nel[0] * (ey + nel[1] * ez)).ravel()).astype(np.int64)
+
+
+def obstacle_config(nel=(6, 6, 4), degree=3, h=25e-6, solid_lo=(2, 2, 1), solid_hi=(4, 4, 3), bc=None,
+                    curved_amp=0.0, c=C_WATER, n_steps=100, cfl=0.25, seed=None):
+    """One box with a rigid obstacle: the elements of the index block
+    solid_lo <= (ex, ey, ez) < solid_hi are removed from the fluid, their faces towards the fluid are
+    Neumann (rigid) surfaces.  bc: six face tags (default: rigid, absorbing top).  curved_amp > 0 puts
+    the box on curved_config's displaced vertex lattice (with ``seed``: jittered)."""
+    extent = tuple(h * n for n in nel)
+    if curved_amp > 0.0:
+        rec = curved_config(nel=nel, degree=degree, extent=extent, amp=curved_amp, c=c, n_steps=n_steps,
+                            cfl=cfl, seed=seed)
+    else:
+        rec = {"name": "obstacle", "boxes": [_box((0, 0, 0), extent, nel, degree, [BC_RIGID] * 6, c=c)],
+               "n_steps": n_steps, "seed": 0}
+        rec["dt"] = cfl_dt(rec["boxes"], cfl)
+        rec = _finish(rec)
+    rec["name"] = "obstacle"
+    rec["boxes"][0]["bc"] = list(bc) if bc is not None else [BC_RIGID] * 5 + [BC_ABSORBING]
+    rec["boxes"][0]["solid"] = solid_block(nel, solid_lo, solid_hi)
+    return rec

@@ -1,4 +1,5 @@
-"""Throughput of the curved-box (element-scatter) path vs the structured path on the same box.
+"""Throughput of the curved-box (element-scatter) path vs the structured path on the same box, and of
+the same (affine) box with a rigid obstacle (a centred block of 1/3 x 1/3 x 1/3 of the elements).
 python tools/curved_bench.py [nel_x nel_y nel_z degree steps] -> one JSON line."""
 import json
 import os
@@ -10,17 +11,19 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2603_06267_b200 import Simulation, sem_kernel_time, sem_set_profiling  # noqa: E402
-from sem_inputs import BC_ABSORBING, curved_config  # noqa: E402
+from sem_inputs import BC_ABSORBING, curved_config, solid_block  # noqa: E402
 
 a = [int(v) for v in sys.argv[1:]] or [96, 96, 24, 5, 20]
 nel, N, steps = tuple(a[:3]), a[3], a[4]
 rec = curved_config(nel=nel, degree=N, extent=tuple(25e-6 * n for n in nel), bc_top=BC_ABSORBING, seed=None)
 out = {"what": "curved box (element scatter, metric recomputed) vs the same box structured", "nel": nel, "degree": N}
-for name in ("curved", "structured"):
+for name in ("curved", "structured", "obstacle"):
     r = dict(rec)
     r["boxes"] = [dict(rec["boxes"][0])]
-    if name == "structured":
+    if name != "curved":
         r["boxes"][0]["vertices"] = None
+    if name == "obstacle":
+        r["boxes"][0]["solid"] = solid_block(nel, [n // 3 for n in nel], [n - n // 3 for n in nel])
     t0 = time.perf_counter()
     sim = Simulation(r)
     setup = time.perf_counter() - t0
@@ -39,6 +42,9 @@ for name in ("curved", "structured"):
     ndof = sim.ndof[0]
     out[name] = {"dof": ndof, "setup_s": setup, "ms_per_step": vol_ms / max(n, 1),
                  "gdof_per_s": ndof / (vol_ms / max(n, 1) / 1e3) / 1e9}
+    if name == "obstacle":
+        out[name]["solid_elements"] = int(len(r["boxes"][0]["solid"]))
+        out[name]["note"] = "DOF counts the whole lattice (obstacle interiors included)"
     sim.close()
 out["ratio_structured_over_curved"] = out["structured"]["gdof_per_s"] / out["curved"]["gdof_per_s"]
 print(json.dumps(out))
