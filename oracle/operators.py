@@ -75,10 +75,17 @@ def element_mass(verts, N):
     return w[a] * w[b] * w[cc] * np.abs(np.linalg.det(jacobian(verts, xi)))
 
 
-def face_quadrature(verts, N, face):
-    """Per face node: local id, reference point, physical point, weight w_s w_t |J_s|, outward normal."""
+def face_quadrature(verts, N, face, rule="gll"):
+    """Per face quadrature point: local id (GLL rule: the collocated face node; LG: None), reference
+    point, physical point, weight w_s w_t |J_s|, outward normal.  rule "gll": the face's (N+1)^2 GLL
+    nodes (reading R9); "lg": the (N+1)^2 Gauss-Legendre points of the same face (R9's flag, Fig. 7's
+    "LG" nodes, P:L1058)."""
     x, w = gll(N)
     ids, st, tang = face_local_nodes(N, face)
+    if rule == "lg":
+        x, w = np.polynomial.legendre.leggauss(N + 1)
+    elif rule != "gll":
+        raise ValueError(f"unknown face rule {rule!r}")
     d, side = face // 2, face % 2
     xi = np.zeros((len(ids), 3))
     xi[:, d] = 1.0 if side else -1.0
@@ -92,7 +99,7 @@ def face_quadrature(verts, N, face):
     centroid = verts.mean(axis=0)
     sgn = np.sign(np.einsum("qd,qd->q", n, pts - centroid[None, :]))
     n = n * sgn[:, None]
-    return ids, xi, pts, w[st[:, 0]] * w[st[:, 1]] * js, n
+    return (ids if rule == "gll" else None), xi, pts, w[st[:, 0]] * w[st[:, 1]] * js, n
 
 
 def _shape_key(verts):
@@ -229,11 +236,12 @@ class System:
         lo, hi = cverts.min(axis=1), cverts.max(axis=1)
         tol = 1e-9 * float(np.max(Cx.h))
         groups = {}
+        rule = itf.get("quad", "gll")
         for e in F.boundary_faces(5):                             # fine +z faces
             vF = F.vertices(e)
-            ids, _, pts, wq, nrm = face_quadrature(vF, F.N, 5)
+            _, xiq, pts, wq, nrm = face_quadrature(vF, F.N, 5, rule)
             owners, xim = [], []
-            for q in range(len(ids)):
+            for q in range(len(xiq)):
                 inbox = np.nonzero(np.all((pts[q] >= lo - tol) & (pts[q] <= hi + tol), axis=1))[0]
                 found = None
                 for ci in inbox:                                  # lowest id first (tie-break)
@@ -253,26 +261,23 @@ class System:
             dofs = np.concatenate([connF[e]] + [connC[cands[u]] for u in uniq])
             if key not in groups:
                 KF = self._face_matrix(F, Cx, vF, [cverts[u] for u in uniq], owners, uniq, np.array(xim),
-                                       ids, wq, nrm, gam)
+                                       xiq, wq, nrm, gam)
                 groups[key] = (KF, [])
             groups[key][1].append(dofs)
         for KF, dl in groups.values():
             self.iface.append((np.stack(dl), KF))
 
     @staticmethod
-    def _face_matrix(F, Cx, vF, cvs, owners, uniq, xim, ids, wq, nrm, gam):
+    def _face_matrix(F, Cx, vF, cvs, owners, uniq, xim, xi_p, wq, nrm, gam):
         nF = (F.N + 1) ** 3
         nC = (Cx.N + 1) ** 3
         nd = nF + nC * len(uniq)
-        xF, _ = gll(F.N)
-        # fine side: reference points of the quadrature nodes on the fine face
-        _, _, a, b, c = _lattice_pts(F.N)
-        xi_p = np.stack([xF[a[ids]], xF[b[ids]], xF[c[ids]]], axis=1)
+        # fine side: basis values / gradients at the reference points xi_p of the quadrature points
         phiF, ghF = ref_gradients(F.N, xi_p)
         JF = np.linalg.inv(jacobian(vF, xi_p))
         gF = np.einsum("qid,qde->qie", ghF, JF)
         KF = np.zeros((nd, nd))
-        for q in range(len(ids)):
+        for q in range(len(xi_p)):
             phi = np.zeros(nd)
             dn = np.zeros(nd)          # c^2 grad phi . n+  (own side's c)
             sgn = np.zeros(nd)
