@@ -142,6 +142,9 @@ def main():
     ap.add_argument("--pml", type=int, default=0,
                     help="PML layers of this many elements on the lateral and top faces of the last box "
                          "(SURVEY 8(f) item 1; not part of BASELINE.json's configs)")
+    ap.add_argument("--iface-quad", default="gll", choices=["gll", "lg"],
+                    help="interface quadrature: the fine faces' GLL nodes (reading R9, BASELINE) or their "
+                         "Gauss-Legendre points (R9's flag)")
     args = ap.parse_args()
     assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_SHORT"), "timing rules: warmup >= 3"
 
@@ -165,6 +168,8 @@ def main():
     from sem_inputs import config
 
     rec = config(args.config)
+    if args.iface_quad != "gll" and rec.get("interface") is not None:
+        rec["interface"] = dict(rec["interface"], quad=args.iface_quad)
     if args.pml:
         bl = rec["boxes"][-1]
         hl = [e / n for e, n in zip(bl["extent"], bl["nel"])]
@@ -293,6 +298,8 @@ def main():
     if args.pml:
         out["config"]["pml"] = {"elements_per_layer": args.pml, "box": rec["pml"]["box"], "R": rec["pml"]["R"],
                                 "faces": "lateral + top", "element_kernel_ms_per_step": pml_ms / max(pml_n, 1)}
+    if args.iface_quad != "gll":
+        out["config"]["iface_quad"] = args.iface_quad
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args.cpu_steps)
     if rank == 0:

@@ -139,7 +139,10 @@ sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, cons
 /* Non-conforming SIPG interface between the +z face of `fine_box` and the -z face of
  * `coarse_box` (Eq. 7's three Gamma_I sums), gamma_F = penalty_alpha cbar^2
  * max(N+, N-)^2 / min(h+, h-) with cbar the harmonic mean of c (reading R7).
- * quad_rule 0 = fine-face GLL nodes (reading R9; the only rule implemented).
+ * quad_rule 0 = the fine faces' (N+ + 1)^2 GLL nodes (reading R9, collocated with the fine trace);
+ * quad_rule 1 = their (N+ + 1)^2 Gauss-Legendre points (R9's flag, Fig. 7's "LG" nodes):
+ * the fine trace is interpolated to the points and the fine side's terms projected back onto the
+ * fine face nodes; single slab only (world 1, no emulation: SEM_E_PARTITION otherwise).
  * Requires matching lateral extents and h_coarse = R h_fine for an integer R >= 1.
  * Errors: SEM_E_ARG (geometry), SEM_E_UNMATCHED (lattices do not nest), SEM_E_STATE. */
 sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, double penalty_alpha,

@@ -901,6 +901,188 @@ __global__ void __launch_bounds__(256) iface_gather_x(const __grid_constant__ If
     p.sigc[id] = s2 * inv;
 }
 
+// ---- Gauss-Legendre variant (quad_rule 1).  A block holds FPB = 256 / (Nf+1)^2 fine faces, one
+// thread per face node / LG point; the 2D interpolations are done as two 1D passes through shared
+// memory.  (1) node (a, b): trace p+ and d_n p+.  (2) LG point (kx, ky): p+, d_n p+ by the fine basis
+// at the LG points, p-, d_n p- by the coarse basis (ILG); T = gamma J - A, S = -1/2 c+^2 J weighted by
+// W_q; the coarse side's terms g1 = -W T, g2 = W (c-^2/c+^2) S go to the LG lattice.  (3) node
+// (a, b): sum_q W_q T_q l_a l_b (and S) accumulated into the fine nodes (atomics: face edges are shared).
+__global__ void __launch_bounds__(256) iface_fine_lg(const __grid_constant__ IfaceParams p) {
+    const int Nf = p.Nf, Nc = p.Nc, n1 = Nf + 1, n2 = n1 * n1, R = p.R, nq = n1;
+    const int FPB = blockDim.x / n2;
+    extern __shared__ double lg_smem[];
+    double* const sL = lg_smem;                           // Lf [nq][n1]
+    const int fl = threadIdx.x / n2, t = threadIdx.x - fl * n2;
+    double* const base = lg_smem + n2 + (size_t)(fl < FPB ? fl : 0) * 6 * n2;
+    double* const sPp = base;            // trace at the nodes, then T at the LG points
+    double* const sDp = base + n2;       // d_n p+ at the nodes, then S
+    double* const t1 = base + 2 * n2;    // first-pass buffers
+    double* const t2 = base + 3 * n2;
+    double* const sT = base + 4 * n2;
+    double* const sS = base + 5 * n2;
+    for (int q = threadIdx.x; q < n2; q += blockDim.x) sL[q] = p.Lf[q];
+    const int f = blockIdx.x * FPB + fl;
+    const bool act = fl < FPB && f < p.nelfx * p.nelfy;
+    const int fx = act ? f % p.nelfx : 0, fy = act ? f / p.nelfx : 0;
+    const int a = t % n1, b = t / n1;   // node (a, b) or LG point (kx, ky) = (a, b)
+    const long long S = p.PXf * p.NYf;
+    const int ix = fx * Nf + a, iy = fy * Nf + b;
+    if (act) {
+        const double* top = p.Pf + (p.NZf - 1) * S + (long long)iy * p.PXf + ix;
+        double d = 0.0;
+        for (int c = 0; c <= Nf; ++c) d = fma(p.dfT[c], __ldg(top - (long long)(Nf - c) * S), d);
+        sPp[t] = __ldg(top);
+        sDp[t] = d;
+    }
+    __syncthreads();
+    if (act) {   // x pass: t1(kx, b) = sum_aa l_aa(xq_kx) P(aa, b)
+        const int kx = a;
+        double r1 = 0.0, r2 = 0.0;
+        for (int aa = 0; aa <= Nf; ++aa) {
+            const double l = sL[kx * n1 + aa];
+            r1 = fma(l, sPp[aa + n1 * b], r1);
+            r2 = fma(l, sDp[aa + n1 * b], r2);
+        }
+        t1[t] = r1;
+        t2[t] = r2;
+    }
+    __syncthreads();
+    if (act) {   // y pass and the flux at LG point (kx, ky)
+        const int kx = a, ky = b;
+        double pp = 0.0, dpp = 0.0;
+        for (int bb = 0; bb <= Nf; ++bb) {
+            const double l = sL[ky * n1 + bb];
+            pp = fma(l, t1[kx + n1 * bb], pp);
+            dpp = fma(l, t2[kx + n1 * bb], dpp);
+        }
+        const int ecx = fx / R, ecy = fy / R;
+        const int qx = (fx - ecx * R) * nq + kx, qy = (fy - ecy * R) * nq + ky;
+        const int NXc = (int)p.NXc;
+        const int c0 = ecy * Nc * NXc + ecx * Nc;
+        double pm = 0.0, dpm = 0.0;
+        for (int bb = 0; bb <= Nc; ++bb) {
+            double rt = 0.0, rd = 0.0;
+            for (int aa = 0; aa <= Nc; ++aa) {
+                const double wx = __ldg(p.ILG + qx * (Nc + 1) + aa);
+                rt = fma(wx, __ldg(p.trc + c0 + bb * NXc + aa), rt);
+                rd = fma(wx, __ldg(p.drc + c0 + bb * NXc + aa), rd);
+            }
+            const double wy = __ldg(p.ILG + qy * (Nc + 1) + bb);
+            pm = fma(wy, rt, pm);
+            dpm = fma(wy, rd, dpm);
+        }
+        const double J = pp - pm;
+        const double A = 0.5 * (p.cf2 * dpp + p.cc2 * dpm);
+        const double W = p.wqx[kx] * p.wqy[ky];
+        const double T = W * (p.gamma * J - A), Sg = W * (-0.5 * p.cf2 * J);
+        sT[t] = T;
+        sS[t] = Sg;
+        const long long gq = (long long)(fy * nq + ky) * p.NXq + fx * nq + kx;
+        p.g1[gq] = -T;
+        p.g2[gq] = (p.cc2 / p.cf2) * Sg;
+    }
+    __syncthreads();
+    if (act) {   // projection, x pass: t1(a, ky) = sum_kx l_a(xq_kx) T(kx, ky)
+        const int ky = b;
+        double r1 = 0.0, r2 = 0.0;
+        for (int kx = 0; kx < nq; ++kx) {
+            const double l = sL[kx * n1 + a];
+            r1 = fma(l, sT[kx + n1 * ky], r1);
+            r2 = fma(l, sS[kx + n1 * ky], r2);
+        }
+        t1[t] = r1;
+        t2[t] = r2;
+    }
+    __syncthreads();
+    if (act) {   // y pass and accumulation at node (a, b)
+        double ts = 0.0, ss = 0.0;
+        for (int ky = 0; ky < nq; ++ky) {
+            const double l = sL[ky * n1 + b];
+            ts = fma(l, t1[a + n1 * ky], ts);
+            ss = fma(l, t2[a + n1 * ky], ss);
+        }
+        const long long g = (long long)iy * p.NXf + ix;
+        atomicAdd(p.tacc + g, ts);
+        atomicAdd(p.sacc + g, ss);
+    }
+}
+
+// collocated-equivalent fine values tau = acc / (m_x m_y) (vol_kernel divides by m_z); clears acc
+__global__ void iface_lg_normalise(const __grid_constant__ IfaceParams p) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    const int NXf = (int)p.NXf;
+    if (id >= NXf * (int)p.NYf) return;
+    const int ix = id % NXf, iy = id / NXf;
+    const double inv = 1.0 / (p.mxf[ix] * p.myf[iy]);
+    p.tauf[id] = p.tacc[id] * inv;
+    p.sigf[id] = p.sacc[id] * inv;
+    p.tacc[id] = 0.0;
+    p.sacc[id] = 0.0;
+}
+
+// transposed coarse interpolation over the LG lattice along one direction: coarse node j = e Nc + b
+// collects the RQ = R nq points of element e (weight ILG[k][b]) and, for b = 0, those of e - 1
+// (weight ILG[k][Nc]); no point is shared between elements
+__device__ __forceinline__ void gather_1d_lg(const IfaceParams& p, int j, int nelc, const double* __restrict__ in1,
+                                             const double* __restrict__ in2, long long stride, double& s1, double& s2) {
+    const int Nc = p.Nc, RQ = p.R * (p.Nf + 1);
+    int e = j / Nc, b = j - e * Nc;
+    if (e > nelc - 1) {
+        e = nelc - 1;
+        b = Nc;
+    }
+    s1 = 0.0;
+    s2 = 0.0;
+    for (int k = 0; k < RQ; ++k) {
+        const long long i = (long long)(e * RQ + k) * stride;
+        const double w = __ldg(p.ILG + k * (Nc + 1) + b);
+        s1 = fma(w, __ldg(in1 + i), s1);
+        s2 = fma(w, __ldg(in2 + i), s2);
+    }
+    if (b == 0 && e > 0) {
+        for (int k = 0; k < RQ; ++k) {
+            const long long i = (long long)((e - 1) * RQ + k) * stride;
+            const double w = __ldg(p.ILG + k * (Nc + 1) + Nc);
+            s1 = fma(w, __ldg(in1 + i), s1);
+            s2 = fma(w, __ldg(in2 + i), s2);
+        }
+    }
+}
+
+__global__ void iface_gather_y_lg(const __grid_constant__ IfaceParams p) {
+    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= p.NXq * p.NYc) return;
+    const long long qx = id % p.NXq, jy = id / p.NXq;
+    double s1, s2;
+    gather_1d_lg(p, (int)jy, p.nelcy, p.g1 + qx, p.g2 + qx, p.NXq, s1, s2);
+    p.q1[id] = s1;
+    p.q2[id] = s2;
+}
+
+__global__ void iface_gather_x_lg(const __grid_constant__ IfaceParams p) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    const int NXc = (int)p.NXc;
+    if (id >= NXc * (int)p.NYc) return;
+    const int jx = id % NXc, jy = id / NXc;
+    double s1, s2;
+    gather_1d_lg(p, jx, p.nelcx, p.q1 + (long long)jy * p.NXq, p.q2 + (long long)jy * p.NXq, 1, s1, s2);
+    const double inv = 1.0 / (p.mxc[jx] * p.myc[jy]);
+    p.tauc[id] = s1 * inv;
+    p.sigc[id] = s2 * inv;
+}
+
+static void launch_iface_lg(const IfaceParams& p, cudaStream_t s) {
+    const int T = 256;
+    const long long nc = p.NXc * p.NYc, nf = p.NXf * p.NYf, nfaces = (long long)p.nelfx * p.nelfy;
+    iface_coarse_trace<<<(unsigned)((nc + T - 1) / T), T, 0, s>>>(p);
+    const int n2 = (p.Nf + 1) * (p.Nf + 1), fpb = 256 / n2;
+    const size_t smem = sizeof(double) * (size_t)n2 * (1 + 6 * fpb);
+    iface_fine_lg<<<(unsigned)((nfaces + fpb - 1) / fpb), fpb * n2, smem, s>>>(p);
+    iface_lg_normalise<<<(unsigned)((nf + T - 1) / T), T, 0, s>>>(p);
+    iface_gather_y_lg<<<(unsigned)((p.NXq * p.NYc + T - 1) / T), T, 0, s>>>(p);
+    iface_gather_x_lg<<<(unsigned)((nc + T - 1) / T), T, 0, s>>>(p);
+}
+
 template <int NF, int NC, int R>
 static void launch_iface_t(const IfaceParams& p, cudaStream_t s) {
     const int T = 256;
@@ -912,7 +1094,8 @@ static void launch_iface_t(const IfaceParams& p, cudaStream_t s) {
 }
 
 void launch_iface(const IfaceParams& p, cudaStream_t s) {
-    if (p.Nf == 5 && p.Nc == 3 && p.R == 2) launch_iface_t<5, 3, 2>(p, s);   // configs 2-4
+    if (p.lg) launch_iface_lg(p, s);
+    else if (p.Nf == 5 && p.Nc == 3 && p.R == 2) launch_iface_t<5, 3, 2>(p, s);   // configs 2-4
     else launch_iface_t<0, 0, 0>(p, s);
 }
 

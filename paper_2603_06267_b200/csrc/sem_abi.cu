@@ -118,6 +118,29 @@ std::vector<double> deriv_matrix(const std::vector<double>& x) {
 }
 
 // ell_j(t) by the second barycentric form
+// n-point Gauss-Legendre rule on [-1, 1] (ascending): roots of P_n by Newton, w = 2 / ((1 - x^2) P_n'(x)^2)
+void gl_rule(int n, std::vector<double>& x, std::vector<double>& w) {
+    x.assign(n, 0.0);
+    w.assign(n, 0.0);
+    for (int i = 0; i < n; ++i) {
+        double z = std::cos(M_PI * (i + 0.75) / (n + 0.5)), dp = 1.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = z;
+            for (int k = 2; k <= n; ++k) {
+                const double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+                p0 = p1;
+                p1 = p2;
+            }
+            dp = n * (z * p1 - p0) / (z * z - 1.0);
+            const double dz = p1 / dp;
+            z -= dz;
+            if (std::fabs(dz) < 1e-16) break;
+        }
+        x[n - 1 - i] = z;
+        w[n - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+    }
+}
+
 std::vector<double> lagrange_at(const std::vector<double>& x, double t) {
     const int n = (int)x.size();
     const std::vector<double> l = bary(x);
@@ -1059,7 +1082,10 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
     sem_status st = check_ctx(ctx);
     if (st) return st;
     if (ctx->itf_on) return fail(ctx, SEM_E_STATE, "interface already built");
-    if (quad_rule != 0) return fail(ctx, SEM_E_ARG, "only quad_rule 0 (fine-face GLL nodes) is implemented");
+    if (quad_rule != 0 && quad_rule != 1)
+        return fail(ctx, SEM_E_ARG, "quad_rule must be 0 (fine-face GLL nodes) or 1 (Gauss-Legendre points)");
+    if (quad_rule == 1 && (ctx->world > 1 || ctx->parts.size() != 1))
+        return fail(ctx, SEM_E_PARTITION, "the Gauss-Legendre interface rule is implemented for a single slab only");
     const int nb = (int)ctx->gdesc.size();
     if (fine_box < 0 || coarse_box < 0 || fine_box >= nb || coarse_box >= nb || fine_box == coarse_box)
         return fail(ctx, SEM_E_ARG, "bad box indices");
@@ -1139,6 +1165,41 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
             dalloc(ctx, &p.sigf, nf) || dalloc(ctx, &p.h1, nh) ||
             dalloc(ctx, &p.h2, nh) || dalloc(ctx, &p.tauc, nc) || dalloc(ctx, &p.sigc, nc))
             return SEM_E_OOM;
+        if (quad_rule == 1) {   // Gauss-Legendre points of the fine faces (R9's flag)
+            const int nq = Nf + 1;
+            std::vector<double> xq, wq;
+            gl_rule(nq, xq, wq);
+            std::vector<double> Lf((size_t)nq * (Nf + 1)), ILG((size_t)R * nq * (Nc + 1));
+            for (int k = 0; k < nq; ++k) {
+                const std::vector<double> l = lagrange_at(xf, xq[k]);
+                for (int a = 0; a <= Nf; ++a) Lf[(size_t)k * (Nf + 1) + a] = l[a];
+            }
+            for (int r = 0; r < R; ++r)
+                for (int k = 0; k < nq; ++k) {
+                    const double xm = (2.0 * r + xq[k] + 1.0) / R - 1.0;   // x_hat^- of the LG point
+                    const std::vector<double> l = lagrange_at(xc, xm);
+                    for (int b = 0; b <= Nc; ++b) ILG[(size_t)(r * nq + k) * (Nc + 1) + b] = l[b];
+                }
+            p.lg = 1;
+            p.nelfx = F.d.nel[0];
+            p.nelfy = F.d.nel[1];
+            p.NXq = (long long)p.nelfx * nq;
+            p.NYq = (long long)p.nelfy * nq;
+            for (int k = 0; k < nq; ++k) {
+                p.wqx[k] = 0.5 * hF[0] * wq[k];
+                p.wqy[k] = 0.5 * hF[1] * wq[k];
+            }
+            double *dLf = nullptr, *dILG = nullptr;
+            if (upload(ctx, &dLf, Lf) || upload(ctx, &dILG, ILG)) return SEM_E_CUDA;
+            p.Lf = dLf;
+            p.ILG = dILG;
+            const size_t nqq = (size_t)p.NXq * p.NYq, nqh = (size_t)p.NXq * C.NY;
+            if (dalloc(ctx, &p.g1, nqq) || dalloc(ctx, &p.g2, nqq) || dalloc(ctx, &p.tacc, nf) ||
+                dalloc(ctx, &p.sacc, nf) || dalloc(ctx, &p.q1, nqh) || dalloc(ctx, &p.q2, nqh))
+                return SEM_E_OOM;
+            CU(cudaMemset(p.tacc, 0, nf * sizeof(double)));
+            CU(cudaMemset(p.sacc, 0, nf * sizeof(double)));
+        }
         // layer coefficients: a -= tau ktau[c] + sigma ksig[c]
         F.iface_side = +1;
         F.tau = p.tauf;

@@ -158,6 +158,18 @@ struct IfaceParams {
     double* h1; double* h2;         // [NYc][NXf] after the y gather
     double* tauc; double* sigc;     // coarse outputs [NXc*NYc]
     int skip_iy0;                   // slab with a lower cut: the shared fine cut line belongs to the lower slab
+    // Gauss-Legendre quadrature on the fine faces (quad_rule 1, R9's flag): nq = Nf + 1 points per
+    // direction and fine face, none shared; the fine side's terms are projected back onto the fine
+    // face nodes (collocated-equivalent tau / sigma, so vol_kernel is unchanged)
+    int lg;
+    int nelfx, nelfy;               // fine faces along x / y
+    long long NXq, NYq;             // LG point lattice: nelf * nq
+    const double* __restrict__ Lf;  // [nq][Nf+1] fine GLL basis at the LG points
+    const double* __restrict__ ILG; // [R nq][Nc+1] coarse basis at the fine LG points of a coarse element
+    double wqx[kMaxN + 1], wqy[kMaxN + 1];   // (h_f/2) w_LG per direction
+    double* g1; double* g2;         // [NYq][NXq] weighted coarse-side terms at the LG points
+    double* tacc; double* sacc;     // [NYf][NXf] fine-node accumulators (atomics), cleared by the normaliser
+    double* q1; double* q2;         // [NYc][NXq] after the y gather
 };
 
 // PML auxiliaries of one box (readings R23-R25).  Phi is element-local

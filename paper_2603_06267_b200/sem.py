@@ -334,7 +334,8 @@ class Simulation:
                 sem_pmut_attach(self.ctx, rec["pmut"])
             if rec.get("interface") is not None:
                 it = rec["interface"]
-                sem_dg_interface_build(self.ctx, it["fine_box"], it["coarse_box"], it["alpha"], 0)
+                rule = {"gll": 0, "lg": 1}[it.get("quad", "gll")]
+                sem_dg_interface_build(self.ctx, it["fine_box"], it["coarse_box"], it["alpha"], rule)
             if rec.get("pml") is not None:
                 pl = rec["pml"]
                 sem_pml_attach(self.ctx, pl["box"], pl["thickness"], pl["R"])
