@@ -1366,9 +1366,12 @@ __device__ __forceinline__ long long curved_node(const CurvedParams& p, int e, i
 
 // elements per block: up to 256 threads; dynamic shared memory: two staging buffers of the element
 // pressures, two flux arrays, two vertex buffers and D
+#ifndef SEM_CV_EPB
+#define SEM_CV_EPB 256   // threads per block the element count aims at
+#endif
 template <int N>
 constexpr int curved_epb() {
-    constexpr int by_threads = 256 / ((N + 1) * (N + 1));
+    constexpr int by_threads = SEM_CV_EPB / ((N + 1) * (N + 1));
     constexpr int by_smem = 100000 / (32 * (N + 1) * (N + 1) * (N + 1) + 384);
     constexpr int e = by_threads < by_smem ? by_threads : by_smem;
     return e > 1 ? e : 1;
