@@ -85,6 +85,13 @@ typedef struct {
                                     the coarse elements of an interface -> SEM_E_PARTITION)       */
     const void* nccl_unique_id;  /* ncclUniqueId (128 bytes) when world > 1, else NULL  */
     int flags;                   /* SEM_F_*                                              */
+    /* Optional caller allocator for every persistent device array of the context (e.g. the torch
+     * caching allocator, so the library shares the caller's memory pool); NULL -> cudaMalloc /
+     * cudaFree.  dev_alloc(bytes, alloc_user) returns device memory (>= 256-byte aligned) on
+     * `device` or NULL (-> SEM_E_OOM); dev_free(ptr, alloc_user) is called from sem_destroy. */
+    void* (*dev_alloc)(size_t bytes, void* user);
+    void (*dev_free)(void* ptr, void* user);
+    void* alloc_user;
 } sem_mesh_desc;
 
 /* Create the context: validates boxes, builds the 1D GLL tables and allocates p (two time

@@ -172,8 +172,14 @@ sem_status fail(sem_ctx* c, sem_status st, const std::string& msg) {
 template <typename T>
 sem_status dalloc(sem_ctx* ctx, T** p, size_t n) {
     void* q = nullptr;
-    cudaError_t e = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T));
-    if (e != cudaSuccess) return fail(ctx, SEM_E_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    if (ctx->dev_alloc) {
+        q = ctx->dev_alloc(bytes, ctx->alloc_user);
+        if (!q) return fail(ctx, SEM_E_OOM, "caller allocator returned NULL");
+    } else {
+        cudaError_t e = cudaMalloc(&q, bytes);
+        if (e != cudaSuccess) return fail(ctx, SEM_E_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
     ctx->allocs.push_back(q);
     *p = (T*)q;
     return SEM_OK;
@@ -884,6 +890,10 @@ sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
     if (desc->world < 1 || desc->rank < 0 || desc->rank >= desc->world) return bail(SEM_E_ARG);
     ctx->device = desc->device;
     ctx->flags = desc->flags;
+    if (!desc->dev_alloc != !desc->dev_free) return bail(SEM_E_ARG);   // both or neither
+    ctx->dev_alloc = desc->dev_alloc;
+    ctx->dev_free = desc->dev_free;
+    ctx->alloc_user = desc->alloc_user;
     ctx->dt = desc->dt;
     ctx->rank = desc->rank;
     ctx->world = desc->world;
@@ -1784,7 +1794,10 @@ void sem_destroy(sem_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     drop_graphs(ctx);
     if (ctx->nccl && nccl_api().commDestroy) nccl_api().commDestroy(ctx->nccl);
-    for (void* p : ctx->allocs) cudaFree(p);
+    for (void* p : ctx->allocs) {
+        if (ctx->dev_free) ctx->dev_free(p, ctx->alloc_user);
+        else if (!ctx->dev_alloc) cudaFree(p);
+    }
     for (auto& pe : ctx->ev_pending) {
         cudaEventDestroy(pe.second.first);
         cudaEventDestroy(pe.second.second);

@@ -346,6 +346,9 @@ struct sem_ctx {
     int rank = 0, world = 1;
     bool emulate = false;          // all slabs in this context, exchange by device copies
     double dt = 0;
+    void* (*dev_alloc)(size_t, void*) = nullptr;   // caller allocator (sem_mesh_desc), or cudaMalloc
+    void (*dev_free)(void*, void*) = nullptr;
+    void* alloc_user = nullptr;
     std::vector<sem_box_desc> gdesc;               // global boxes as given
     std::vector<long long> gNX, gNY, gNZ;          // global lattice sizes
     std::vector<sem::Part> parts;

@@ -35,10 +35,29 @@ class BoxDesc(C.Structure):
                 ("degree", C.c_int), ("c", C.c_double), ("rho", C.c_double), ("bc", C.c_int * 6)]
 
 
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+
+
 class MeshDesc(C.Structure):
     _fields_ = [("n_boxes", C.c_int), ("boxes", C.POINTER(BoxDesc)), ("dt", C.c_double),
                 ("device", C.c_int), ("stream", C.c_void_p), ("rank", C.c_int), ("world", C.c_int),
-                ("nccl_unique_id", C.c_void_p), ("flags", C.c_int)]
+                ("nccl_unique_id", C.c_void_p), ("flags", C.c_int),
+                ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_user", C.c_void_p)]
+
+
+def torch_allocator(device=0):
+    """(dev_alloc, dev_free) ctypes callbacks on torch's caching allocator (sem_mesh_desc); keep the
+    returned pair alive as long as the context."""
+    import torch
+
+    def _alloc(nbytes, _user):
+        return torch.cuda.caching_allocator_alloc(int(nbytes), device)
+
+    def _free(ptr, _user):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    return ALLOC_FN(_alloc), FREE_FN(_free)
 
 
 class FaceSet(C.Structure):
@@ -141,10 +160,14 @@ def sem_slab_plan(boxes, world, pm=None):
     return list(x0)
 
 
-def sem_mesh_create(boxes, dt, device=0, stream=None, rank=0, world=1, nccl_unique_id=None, flags=0):
+def sem_mesh_create(boxes, dt, device=0, stream=None, rank=0, world=1, nccl_unique_id=None, flags=0,
+                    allocator=None):
+    """allocator: optional (dev_alloc, dev_free) pair of ctypes callbacks (see torch_allocator)."""
     arr = _box_array(boxes)
     d = MeshDesc(len(boxes), arr, float(dt), int(device), C.c_void_p(stream) if stream else None, int(rank),
                  int(world), C.cast(C.c_char_p(nccl_unique_id), C.c_void_p) if nccl_unique_id else None, int(flags))
+    if allocator is not None:
+        d.dev_alloc, d.dev_free = allocator
     out = C.c_void_p()
     st = LIB.sem_mesh_create(C.byref(d), C.byref(out))
     if st != 0:
@@ -312,11 +335,15 @@ def sem_destroy(ctx):
 class Simulation:
     """One context built from a ``sem_inputs`` workload record (boxes, PMUTs, interface, source)."""
 
-    def __init__(self, rec, device=0, stream=None, flags=0, rank=0, world=1, nccl_unique_id=None):
+    def __init__(self, rec, device=0, stream=None, flags=0, rank=0, world=1, nccl_unique_id=None,
+                 torch_memory=False):
         self.rec = rec
         if rec.get("coupling", "predicted") == "literal":
             flags |= SEM_F_COUPLING_LITERAL
-        self.ctx = sem_mesh_create(rec["boxes"], rec["dt"], device, stream, rank, world, nccl_unique_id, flags)
+        # torch_memory: the context's device arrays come from torch's caching allocator
+        self._allocator = torch_allocator(device) if torch_memory else None
+        self.ctx = sem_mesh_create(rec["boxes"], rec["dt"], device, stream, rank, world, nccl_unique_id, flags,
+                                   self._allocator)
         self.nn = [tuple(b["degree"] * n + 1 for n in b["nel"]) for b in rec["boxes"]]
         self.ndof = [a * b * c for a, b, c in self.nn]
         try:

@@ -83,3 +83,30 @@ def test_nccl_loadable_unique_id():
     from paper_2603_06267_b200 import sem_nccl_unique_id
     uid = sem_nccl_unique_id()
     assert isinstance(uid, bytes) and len(uid) == 128 and any(uid)
+
+
+def test_caller_allocator_torch_pool():
+    """sem_mesh_desc dev_alloc / dev_free: the context's arrays come from torch's caching allocator,
+    the results are bit-identical to the cudaMalloc context's and the memory returns on destroy."""
+    import numpy as np
+    import torch
+
+    from paper_2603_06267_b200 import Simulation
+    from sem_inputs import small_config
+    rec = small_config("cfg2s")
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    a = Simulation(rec, torch_memory=True)
+    held = torch.cuda.memory_allocated() - base
+    a.step(40)
+    pa = [a.pressure(b) for b in range(2)]
+    qa = a.modal()[0]
+    a.close()
+    torch.cuda.synchronize()
+    assert held > 0 and torch.cuda.memory_allocated() == base
+    b = Simulation(rec)
+    b.step(40)
+    for k in range(2):
+        assert np.array_equal(pa[k], b.pressure(k))
+    assert np.array_equal(qa, b.modal()[0])
+    b.close()
