@@ -300,7 +300,7 @@ def main():
                                 "faces": "lateral + top", "element_kernel_ms_per_step": pml_ms / max(pml_n, 1)}
     if args.iface_quad != "gll":
         out["config"]["iface_quad"] = args.iface_quad
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:   # the contract: rank 0 at N = 1 only
         out["cpu_baseline"] = cpu_baseline(args.cpu_steps)
     if rank == 0:
         print(json.dumps(out), flush=True)
