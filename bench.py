@@ -115,14 +115,27 @@ def cpu_baseline(steps, warmup=1, patch=4):
                       f"after {warmup} warm-up, {dt:.1f} s"}
 
 
+def workload_config(rec, cfg, world):
+    """The bench line's "config" (shared by both arms: the reference arm reports on the same workload)."""
+    import numpy as np
+    ndof_total = sum(int(np.prod([b["degree"] * n + 1 for n in b["nel"]])) for b in rec["boxes"])
+    return {"workload": f"cfg{cfg}", "dof": ndof_total,
+            "boxes": [f"{b['nel'][0]}x{b['nel'][1]}x{b['nel'][2]} N={b['degree']}" for b in rec["boxes"]],
+            "n_pmut": len(rec["pmut"]["centers"]) if rec.get("pmut") else 0,
+            "n_modes": len(rec["pmut"]["mode_mn"]) if rec.get("pmut") else 0,
+            "dt": rec["dt"], "l2": "state 24 B/DOF resident = %.1f GB > 126 MB L2; no flush needed"
+            % (24 * ndof_total / 1e9), "parallelism": f"y-slabs x{world}"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    from sem_inputs import config
     cb = cpu_baseline(args.steps, args.warmup, patch=args.ref_patch)
     out = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
-           "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"cfg{args.config} (bounded crop, oracle on host cores)"},
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": workload_config(config(args.config), args.config, world),
            "cpu_baseline": cb,
            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -279,12 +292,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg{args.config}", "dof": ndof_total,
-                   "boxes": [f"{b['nel'][0]}x{b['nel'][1]}x{b['nel'][2]} N={b['degree']}" for b in rec["boxes"]],
-                   "n_pmut": len(rec["pmut"]["centers"]) if rec.get("pmut") else 0,
-                   "n_modes": len(rec["pmut"]["mode_mn"]) if rec.get("pmut") else 0,
-                   "dt": rec["dt"], "l2": "state 24 B/DOF resident = %.1f GB > 126 MB L2; no flush needed"
-                   % (24 * ndof_total / 1e9), "parallelism": f"y-slabs x{world}"},
+        "config": workload_config(rec, args.config, world),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "vol_kernel (both boxes, per step)",
                      "bytes_per_step_algorithmic": BYTES_PER_DOF * ndof_total,
