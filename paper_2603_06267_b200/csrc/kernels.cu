@@ -755,6 +755,7 @@ __global__ void __launch_bounds__(32 * kModalWarps) modal_kernel(const __grid_co
 #pragma unroll
                 for (int m = 0; m < kMaxModes; ++m)
                     if (m < M) f = fma(qv[m], sxk[m * L + i] * syk[m * L + j], f);
+                SEM_CHECK(i0 + i < p.NX);
                 p.F[(long long)(j0 + j) * p.NX + i0 + i] = p.kappa * f;
             }
         }
@@ -803,6 +804,7 @@ __global__ void __launch_bounds__(256) iface_fine(const __grid_constant__ IfaceP
     const int qx = ix - ex * NfR, qy = iy - ey * NfR;
     const int NXc = (int)p.NXc;
     const int c0 = ey * Nc * NXc + ex * Nc;
+    SEM_CHECK(c0 + Nc * NXc + Nc < NXc * (int)p.NYc && p.NZf > Nf);
     // fine trace and normal derivative (n+ = +e_z): the top element layer of the fine box
     const double pp = __ldg(top);
     double dpp = 0.0;
@@ -854,6 +856,7 @@ __device__ __forceinline__ void gather_1d(const IfaceParams& p, int j, int nelc,
 #pragma unroll 4
     for (int q = 0; q <= qend; ++q) {
         const int i = e * NfR + q;
+        SEM_CHECK(i < nf);
         if (skip0 && i == 0) continue;
         double w = __ldg(p.I + q * (Nc + 1) + b);
         if (wi) w *= __ldg(wi + i);
@@ -978,6 +981,7 @@ __global__ void __launch_bounds__(256) iface_fine_lg(const __grid_constant__ Ifa
         sT[t] = T;
         sS[t] = Sg;
         const long long gq = (long long)(fy * nq + ky) * p.NXq + fx * nq + kx;
+        SEM_CHECK(gq < p.NXq * p.NYq && c0 + Nc * NXc + Nc < NXc * (int)p.NYc);
         p.g1[gq] = -T;
         p.g2[gq] = (p.cc2 / p.cf2) * Sg;
     }
@@ -1002,6 +1006,7 @@ __global__ void __launch_bounds__(256) iface_fine_lg(const __grid_constant__ Ifa
             ss = fma(l, t2[a + n1 * ky], ss);
         }
         const long long g = (long long)iy * p.NXf + ix;
+        SEM_CHECK(ix < p.NXf && iy < p.NYf);
         atomicAdd(p.tacc + g, ts);
         atomicAdd(p.sacc + g, ss);
     }
@@ -1241,6 +1246,7 @@ __global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1), pm
     const int ex = p.elems[3 * k], ey = p.elems[3 * k + 1], ez = p.elems[3 * k + 2];
     const int gx = N * ex + a, gy = N * ey + b, gz = N * ez + c;
     const long long g = ((long long)gz * p.NY + gy) * p.PX + gx;
+    SEM_CHECK(k >= 0 && k < p.n_el && gx < p.NX && gy < p.NY && gz < p.NZ);
     // every global load first (memory-level parallelism): nodal p, psi, w, the element-local Phi and the
     // per-axis tables
     const double pv = p.P[g];
@@ -1316,6 +1322,7 @@ __global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1)) pm
     if (k >= p.n_el) return;
     const int gx = N * p.elems[3 * k] + a, gy = N * p.elems[3 * k + 1] + b, gz = N * p.elems[3 * k + 2] + c;
     const long long g = ((long long)gz * p.NY + gy) * p.PX + gx;
+    SEM_CHECK(gx < p.NX && gy < p.NY && gz < p.NZ);
     const unsigned long long bits = atomicExch(reinterpret_cast<unsigned long long*>(p.da + g), 0ull);
     if (bits) {
         const double v = __longlong_as_double((long long)bits);
@@ -1410,6 +1417,7 @@ __global__ void __launch_bounds__(curved_threads<N>(), SEM_CV_MINB) curved_resid
         if (g >= ngroups || e >= nel) return -1;
         if (p.solid && p.solid[e]) return -1;   // obstacle element: no contribution
         const long long g0 = curved_node<N>(p, e, 0, b, c);
+        SEM_CHECK(g0 >= 0 && g0 + N < p.PX * p.NY * p.NZ);
         double* dst = spb + (k * EPB + el) * nl + n1 * ln;
 #pragma unroll
         for (int a = 0; a <= N; ++a) cp_async8(dst + a, p.P + g0 + a);
@@ -1417,6 +1425,7 @@ __global__ void __launch_bounds__(curved_threads<N>(), SEM_CV_MINB) curved_resid
         for (int q = ln; q < 24; q += NL) {
             const int v = q / 3, i = q - 3 * v;
             const int vx = ex + (v & 1), vy = ey + ((v >> 1) & 1), vz = ez + (v >> 2);
+            SEM_CHECK(vx <= p.nelx && vy <= p.nely && vz <= p.nelz);
             cp_async8(Xvb + (k * EPB + el) * 24 + q,
                       p.vlat + 3 * ((size_t)vx + (size_t)(p.nelx + 1) * ((size_t)vy + (size_t)(p.nely + 1) * vz)) + i);
         }

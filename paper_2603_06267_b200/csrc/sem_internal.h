@@ -8,6 +8,24 @@
 
 #include "../../include/sem.h"
 
+// Device-side bounds checks of the debug build (libsem_debug.so, -DSEM_DEBUG_CHECKS): the stand-in for
+// compute-sanitizer memcheck, which this pool does not offer.  A failed check prints the condition and
+// traps (the next sync call reports the CUDA error).
+#ifdef SEM_DEBUG_CHECKS
+#include <cstdio>
+#define SEM_CHECK(cond)                                                                                    \
+    do {                                                                                                   \
+        if (!(cond)) {                                                                                     \
+            printf("libsem debug check failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);                  \
+            __trap();                                                                                      \
+        }                                                                                                  \
+    } while (0)
+#else
+#define SEM_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 namespace sem {
 
 constexpr int kMaxN = 8;          // supported GLL degrees 1..8
