@@ -164,11 +164,15 @@ class System:
                 self.vol.append((conn[sel], Ke))
 
     def apply_volume(self, p):
-        r = np.zeros(self.ndof)
+        """r = sum_e P_e^T K_e P_e p: element products, then one scatter-add of every element's
+        contributions (a single bincount: one pass over the global vector however many shape groups)."""
+        idx, val = [], []
         for conn, Ke in self.vol:
-            re = p[conn] @ Ke.T
-            r += np.bincount(conn.ravel(), re.ravel(), minlength=self.ndof)
-        return r
+            idx.append(conn.ravel())
+            val.append((p[conn] @ Ke.T).ravel())
+        if not idx:
+            return np.zeros(self.ndof)
+        return np.bincount(np.concatenate(idx), np.concatenate(val), minlength=self.ndof)
 
     # ------------------------------------------------------------------- ABC
     def _build_abc(self):
@@ -193,10 +197,15 @@ class System:
         face = pm["face"]
         n_p, n_m = len(pm["centers"]), len(pm["mode_mn"])
         acc = [dict() for _ in range(n_p)]
+        cen = np.asarray(pm["centers"], dtype=np.float64)
+        half = 0.5 * pm["side"]
         for e in box.boundary_faces(face):
             ids, _, pts, wq, _ = face_quadrature(box.vertices(e), box.N, face)
             g = conn[e, ids]
-            for k in range(n_p):
+            # only membranes whose square meets the face's bounding box can have S != 0 on it
+            lo, hi = pts[:, :2].min(axis=0), pts[:, :2].max(axis=0)
+            near = np.nonzero(np.all((cen + half >= lo) & (cen - half <= hi), axis=1))[0]
+            for k in near:
                 for m in range(n_m):
                     s = mode_shape(pm, k, m, pts[:, 0], pts[:, 1])
                     for j, val in zip(g[s != 0], (wq * s)[s != 0]):
@@ -298,11 +307,13 @@ class System:
         return KF
 
     def apply_interface(self, p):
-        r = np.zeros(self.ndof)
+        idx, val = [], []
         for dofs, KF in self.iface:
-            re = p[dofs] @ KF.T
-            r += np.bincount(dofs.ravel(), re.ravel(), minlength=self.ndof)
-        return r
+            idx.append(dofs.ravel())
+            val.append((p[dofs] @ KF.T).ravel())
+        if not idx:
+            return np.zeros(self.ndof)
+        return np.bincount(np.concatenate(idx), np.concatenate(val), minlength=self.ndof)
 
     def apply_K(self, p):
         r = self.apply_volume(p)

@@ -326,3 +326,72 @@ def test_literal_coupling_diverges_predicted_bounded():
         amp[cp] = np.abs(nm.q).max()
     assert amp["literal"] > 1e3 * amp["predicted"]
     assert amp["predicted"] < 1e-9
+
+
+def _oblique_column(x_ref=None):
+    """Laterally wide, one-element-thick box, rigid bottom and sides, total-field ABC top with an
+    incident plane pulse at 20 deg (reading R13).  Returns (system, time axis, histories at three
+    observation points, their coordinates)."""
+    h, nel_x, nz = 50e-6, 80, 24
+    rec = cavity_config(nel=(nel_x, 1, nz), degree=3, extent=(nel_x * h, h, nz * h), cfl=0.45)
+    rec["boxes"][0]["bc"][5] = 1
+    f0 = 5e6
+    sig = 1 / (2 * f0)
+    th = math.radians(20.0)
+    rec["plane_wave"] = {"box": 0, "face": 5, "amp_pa": 1e3, "f0_hz": f0, "sigma_s": sig, "t0_s": 4 * sig,
+                         "direction": (math.sin(th), 0.0, -math.cos(th)), "x_ref": x_ref}
+    s = System(rec)
+    xyz = s.node_coords()
+    top = nz * h
+    # observation points (x, depth below the top): far enough from the source corner, the downstream
+    # wall and the rigid bottom that no diffracted or reflected wave reaches them inside the window
+    obs = [(1.9e-3, 0.6e-3), (2.4e-3, 0.6e-3), (2.4e-3, 0.4e-3)]
+    ids = [int(np.argmin(np.abs(xyz[:, 0] - X) + np.abs(xyz[:, 2] - (top - d)) + np.abs(xyz[:, 1])))
+           for X, d in obs]
+    dt = rec["dt"]
+    n = int((7 * sig + (2.6e-3 * math.sin(th) + 0.6e-3 * math.cos(th)) / 1500.0) / dt)
+    nm = Newmark(s)
+    hist = []
+    for _ in range(n):
+        nm.step()
+        hist.append(nm.p[ids])
+    return s, dt * np.arange(1, n + 1), np.array(hist), xyz[ids], (f0, sig, th, top)
+
+
+def test_plane_wave_source_oblique_incidence():
+    """Reading R13 away from normal incidence (k = (sin 20, 0, -cos 20)): the injected field is the
+    plane wave A s(t - k.(x - x_ref)/c) itself (the total-field ABC data makes the incident wave satisfy
+    the boundary condition exactly, so nothing is reflected at the top), which fixes
+      * the waveform and amplitude at interior points (the (1 - n.k) factor),
+      * the delay law's sign: arrivals along x are later by dx sin(th)/c (trace speed c/sin th),
+      * the depth trace: arrivals deeper by dz are later by dz cos(th)/c (trace speed c/cos th),
+      * x_ref = the top corner the wavefront reaches first: with the other corner the absolute timing
+        is off by L_x sin(th)/c and the waveform check fails."""
+    s, t, hist, pts, (f0, sig, th, top) = _oblique_column()
+    c = 1500.0
+    kd = np.array([math.sin(th), 0.0, -math.cos(th)])
+    xref = np.array([0.0, 0.0, top])
+    assert np.allclose(s.pw_xref, xref)
+
+    def src(u):
+        u = u - 4 * sig
+        return 1e3 * np.exp(-u * u / (2 * sig * sig)) * np.sin(2 * math.pi * f0 * u)
+
+    for j in range(3):
+        ref = src(t - (pts[j] - xref) @ kd / c)
+        assert np.max(np.abs(hist[:, j])) > 0.8e3
+        assert np.max(np.abs(hist[:, j] - ref)) < 0.03e3, j
+
+    def centroid(v):   # energy-centroid arrival time of a pulse
+        return float(np.sum(t * v * v) / np.sum(v * v))
+
+    ta = [centroid(hist[:, j]) for j in range(3)]
+    dx = pts[1][0] - pts[0][0]
+    assert abs((ta[1] - ta[0]) - dx * math.sin(th) / c) < 0.02 * dx * math.sin(th) / c
+    depth_delay = (pts[2][2] - pts[1][2]) * math.cos(th) / c
+    assert abs((ta[1] - ta[2]) - depth_delay) < 0.02 * abs(depth_delay)
+
+    # the other top corner as x_ref: the same delay law, shifted by L_x sin(th)/c -> visibly wrong
+    s2, t2, hist2, pts2, _ = _oblique_column(x_ref=(4e-3, 0.0, top))
+    ref = src(t2 - (pts2[1] - xref) @ kd / c)
+    assert np.max(np.abs(hist2[:, 1] - ref)) > 0.5e3
