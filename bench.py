@@ -8,7 +8,12 @@ both boxes.  Workload: BASELINE.json configs[3] (64x64 PMUT array, 526,755,050 F
 largest config and the one the north-star's roofline / scaling targets name), synthetic inputs
 (sem_inputs), state resident in HBM (12.6 GB > L2, so no flush is needed between steps).
 
-Prints ONE JSON line on rank 0.  For N > 1 (torchrun), ranks run the slab decomposition.
+Prints ONE JSON line on rank 0.  For N > 1 the ranks run the y-slab decomposition: under torchrun, or
+spawned by this script itself (torch.distributed.run on 127.0.0.1) when WORLD_SIZE is unset.
+
+Timing: the CUDA-graph path users get (profiling off), K steps per repeat, median of 5 repeats (each
+bracketed by barrier + synchronize, max over ranks); per-kernel times for the roofline come from a
+separate profiling pass over K more steps (direct launches with CUDA events on the launching stream).
 """
 from __future__ import annotations
 
@@ -89,6 +94,34 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
+SPEC_HBM_GBS = 8000.0         # B200 HBM3e spec (~8 TB/s) named by BASELINE.json north_star
+N_REPEATS = 5                 # median of 5 timed runs
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _spawn_ranks(n):
+    """`python bench.py --gpus N` outside torchrun: re-launch this script as N local ranks (one per GPU)
+    under torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def cpu_baseline(steps, warmup=1, patch=4):
     """The oracle as it stands (numpy, FP64) on a bounded sample of the config-3 workload: a
     patch x patch PMUT lateral crop with the full config-3 depth, N, h, interface and modes."""
@@ -109,7 +142,8 @@ def cpu_baseline(steps, warmup=1, patch=4):
     nm.run(steps)
     dt = time.perf_counter() - t0
     val = sys_.ndof * steps / dt / 1e9
-    return {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "ms_per_step": dt / steps * 1e3,
+    return {"value": val, "unit": UNIT, "cores": cores, "cpu_model": _cpu_model(), "host_cpus": os.cpu_count(),
+            "kind": "oracle", "ms_per_step": dt / steps * 1e3,
             "sample": f"config-3 crop: {patch}x{patch} PMUTs ({rec['boxes'][0]['nel']} fine + "
                       f"{rec['boxes'][1]['nel']} coarse elements, {sys_.ndof} DOF), {steps} timed steps "
                       f"after {warmup} warm-up, {dt:.1f} s"}
@@ -150,7 +184,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=20)
+    ap.add_argument("--cpu-steps", type=int, default=150)
     ap.add_argument("--ref-patch", type=int, default=4)
     ap.add_argument("--pml", type=int, default=0,
                     help="PML layers of this many elements on the lateral and top faces of the last box "
@@ -161,10 +195,15 @@ def main():
     args = ap.parse_args()
     assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_SHORT"), "timing rules: warmup >= 3"
 
+    if args.impl == "reference":
+        # the oracle arm runs on rank 0 only (other torchrun ranks exit 0 without work)
+        return run_reference(args, int(os.environ.get("RANK", "0")), args.gpus)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if args.impl == "reference":
-        return run_reference(args, rank, world)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     import numpy as np
     import torch
@@ -201,39 +240,56 @@ def main():
             idt.copy_(torch.frombuffer(bytearray(sem_nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().numpy().tobytes())
-        flags |= SEM_F_NO_GRAPH
+        if os.environ.get("BENCH_NCCL_NO_GRAPH"):
+            flags |= SEM_F_NO_GRAPH     # NCCL send/recv are otherwise captured in the step graph
     sim = Simulation(rec, device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_unique_id=nccl_id,
                      flags=flags)
     ndof_total = sum(sim.ndof)      # global node count (every rank holds one y-slab of it)
 
-    # ---- device-resident timed region ----------------------------------------------------------
+    # ---- device-resident timed region: the CUDA-graph path users get (profiling off), K steps per
+    #      repeat, N_REPEATS repeats, each bracketed by barrier + synchronize; max over ranks per repeat,
+    #      median over repeats
     sim.step(args.warmup)
     sim.sync()
-    sem_set_profiling(sim.ctx, 1)            # CUDA events around each kernel group on this stream
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    launches = 0
+    for _ in range(N_REPEATS):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        sim.step(args.steps)
+        launches = sem_last_launch_count(sim.ctx)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        r = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([r], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            r = float(t.item())
+        reps.append(r)
+    clk = clocks.stop()
+    ms = statistics.median(reps)
+    # ---- per-kernel pass (same K steps, direct launches with CUDA events around each kernel group on
+    #      the launching stream): the roofline's kernel time and the step shares
+    sem_set_profiling(sim.ctx, 1)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches = 0
     e0.record(stream)
     sim.step(args.steps)
-    launches += sem_last_launch_count(sim.ctx)
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    clk = clocks.stop()
+    ms_prof = e0.elapsed_time(e1)
     vol_ms, vol_n = sem_kernel_time(sim.ctx, 0)
     ifc_ms, ifc_n = sem_kernel_time(sim.ctx, 1)
     mod_ms, mod_n = sem_kernel_time(sim.ctx, 2)
     pml_ms, pml_n = sem_kernel_time(sim.ctx, 3)
     sem_set_profiling(sim.ctx, 0)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     ms_step = ms / args.steps
     value = ndof_total * args.steps / (ms / 1e3) / 1e9     # strong scaling: fixed global problem
 
@@ -297,9 +353,15 @@ def main():
                      "traffic": traffic, "kernel": "vol_kernel (both boxes, per step)",
                      "bytes_per_step_algorithmic": BYTES_PER_DOF * ndof_total,
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                     "share_of_step": vol_ms / ms if ms > 0 else None,
+                     "frac_spec_8tbs": achieved / SPEC_HBM_GBS,
+                     "step_frac": BYTES_PER_DOF * ndof_total / world / (ms_step / 1e3) / 1e9 / peak,
+                     "share_of_step": vol_ms / ms_prof if ms_prof > 0 else None,
+                     "timing": "kernel times from a separate profiling pass of the same K steps (direct "
+                               "launches, CUDA events on the launching stream)",
                      "interface_ms_per_step": ifc_ms / max(ifc_n, 1), "modal_ms_per_step": mod_ms / max(mod_n, 1)},
         "gpu_launches": launches,
+        "repeats_ms": reps,
+        "timed_path": f"CUDA graph (sem_step), median of {N_REPEATS} repeats of K steps",
         "clocks": clk,
         "e2e": e2e,
     }

@@ -189,7 +189,10 @@ template <typename T>
 sem_status upload(sem_ctx* ctx, T** p, const std::vector<T>& h) {
     sem_status st = dalloc(ctx, p, h.size());
     if (st != SEM_OK) return st;
-    CU(cudaMemcpy(*p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    // setup copies run on the context stream (not the legacy default stream, which does not order
+    // with the non-blocking streams the steps use) and complete before the call returns
+    CU(cudaMemcpyAsync(*p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
     return SEM_OK;
 }
 
@@ -813,9 +816,9 @@ sem_status setup_part_buffers(sem_ctx* ctx, sem::Part& pt) {
     for (auto& b : pt.boxes) {
         const size_t n = (size_t)b.nalloc();
         if (dalloc(ctx, &b.P[0], n) || dalloc(ctx, &b.P[1], n) || dalloc(ctx, &b.W, n)) return SEM_E_OOM;
-        CU(cudaMemset(b.P[0], 0, n * 8));
-        CU(cudaMemset(b.P[1], 0, n * 8));
-        CU(cudaMemset(b.W, 0, n * 8));
+        CU(cudaMemsetAsync(b.P[0], 0, n * 8, ctx->stream));
+        CU(cudaMemsetAsync(b.P[1], 0, n * 8, ctx->stream));
+        CU(cudaMemsetAsync(b.W, 0, n * 8, ctx->stream));
         if (upload(ctx, &b.xc, b.xh) || upload(ctx, &b.yc, b.yh) || upload(ctx, &b.mx, b.mxh) ||
             upload(ctx, &b.my, b.myh))
             return SEM_E_CUDA;
@@ -837,8 +840,8 @@ sem_status setup_part_buffers(sem_ctx* ctx, sem::Part& pt) {
     pt.xcount = off;
     for (int s = 0; s < 2; ++s) {
         if (dalloc(ctx, &pt.send[s], (size_t)off) || dalloc(ctx, &pt.recv[s], (size_t)off)) return SEM_E_OOM;
-        CU(cudaMemset(pt.send[s], 0, (size_t)off * 8));
-        CU(cudaMemset(pt.recv[s], 0, (size_t)off * 8));
+        CU(cudaMemsetAsync(pt.send[s], 0, (size_t)off * 8, ctx->stream));
+        CU(cudaMemsetAsync(pt.recv[s], 0, (size_t)off * 8, ctx->stream));
     }
     return SEM_OK;
 }
@@ -1207,8 +1210,8 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
             if (dalloc(ctx, &p.g1, nqq) || dalloc(ctx, &p.g2, nqq) || dalloc(ctx, &p.tacc, nf) ||
                 dalloc(ctx, &p.sacc, nf) || dalloc(ctx, &p.q1, nqh) || dalloc(ctx, &p.q2, nqh))
                 return SEM_E_OOM;
-            CU(cudaMemset(p.tacc, 0, nf * sizeof(double)));
-            CU(cudaMemset(p.sacc, 0, nf * sizeof(double)));
+            CU(cudaMemsetAsync(p.tacc, 0, nf * sizeof(double), ctx->stream));
+            CU(cudaMemsetAsync(p.sacc, 0, nf * sizeof(double), ctx->stream));
         }
         // layer coefficients: a -= tau ktau[c] + sigma ksig[c]
         F.iface_side = +1;
@@ -1295,17 +1298,19 @@ sem_status curved_setup(sem_ctx* ctx, Box& b, const sem_box_desc& g) {
     }
     auto put = [&](double** d, const std::vector<double>& h) -> sem_status {
         if (!*d) return upload(ctx, d, h);
-        CU(cudaMemcpy(*d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CU(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
         return SEM_OK;
     };
     if (put(&b.vlat, b.vlat_h) || put(&b.minv, M) || put(&b.cdamp, Cd)) return SEM_E_CUDA;
     if (!b.solid_h.empty()) {
         if (!b.solid && dalloc(ctx, &b.solid, b.solid_h.size())) return SEM_E_OOM;
-        CU(cudaMemcpy(b.solid, b.solid_h.data(), b.solid_h.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpyAsync(b.solid, b.solid_h.data(), b.solid_h.size(), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
     }
     if (!b.res) {
         if (dalloc(ctx, &b.res, (size_t)b.nalloc())) return SEM_E_OOM;
-        CU(cudaMemset(b.res, 0, (size_t)b.nalloc() * sizeof(double)));
+        CU(cudaMemsetAsync(b.res, 0, (size_t)b.nalloc() * sizeof(double), ctx->stream));
     }
     b.curved = true;
     sem::curved_grid(b.N, g.nel[0] * g.nel[1] * g.nel[2]);   // occupancy query + smem opt-in, outside any capture
@@ -1510,9 +1515,9 @@ sem_status sem_step(sem_ctx* ctx, int n_steps) {
     if (st) return st;
     if (n_steps < 0) return fail(ctx, SEM_E_ARG, "n_steps < 0");
     long long launches = 0;
-    const bool direct = ctx->profiling || (ctx->flags & SEM_F_NO_GRAPH);
     int left = n_steps;
     while (left > 0) {
+        const bool direct = ctx->profiling || (ctx->flags & SEM_F_NO_GRAPH) || ctx->graph_failed;
         if (direct) {
             launches += enqueue_step(ctx, ctx->cur, ctx->profiling);
             ctx->cur ^= 1;
@@ -1526,10 +1531,20 @@ sem_status sem_step(sem_ctx* ctx, int n_steps) {
             CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
             int nl = 0;
             for (int k = 0; k < len; ++k) nl += enqueue_step(ctx, ctx->cur ^ (k & 1), false);
-            CU(cudaStreamEndCapture(ctx->stream, &graph));
-            cudaError_t e = cudaGraphInstantiate(&g, graph, 0);
-            cudaGraphDestroy(graph);
-            if (e != cudaSuccess) return fail(ctx, SEM_E_CUDA, std::string("graph: ") + cudaGetErrorString(e));
+            cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+            if (e == cudaSuccess) {
+                e = cudaGraphInstantiate(&g, graph, 0);
+                cudaGraphDestroy(graph);
+            }
+            if (e != cudaSuccess) {
+                g = nullptr;
+                if (nccl_mode(ctx)) {   // NCCL build without capture support: direct launches from now on
+                    (void)cudaGetLastError();
+                    ctx->graph_failed = true;
+                    continue;
+                }
+                return fail(ctx, SEM_E_CUDA, std::string("graph: ") + cudaGetErrorString(e));
+            }
             ctx->graph_launches[ctx->cur][len - 1] = nl;
         }
         CU(cudaGraphLaunch(g, ctx->stream));

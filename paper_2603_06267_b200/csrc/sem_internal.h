@@ -384,6 +384,7 @@ struct sem_ctx {
     long long graph_launches[2][2] = {{0, 0}, {0, 0}};
     long long last_launches = 0;
     bool profiling = false;
+    bool graph_failed = false;   // stream capture refused (NCCL without capture support): direct launches
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
     double kt_ms[4] = {0, 0, 0, 0};   // kernel groups: 0 volume, 1 interface, 2 modal, 3 PML

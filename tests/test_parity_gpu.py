@@ -140,3 +140,22 @@ def test_error_paths():
     sim = Simulation(rec)
     with pytest.raises(SemError):
         sim.write_state(0, np.zeros(5), np.zeros(5))
+
+
+@pytest.mark.parametrize("ratio,nh", [(2, 3), (1, 5)])
+def test_two_material_interface_random_state(ratio, nh):
+    """c+ != c- across Gamma_I (the paper's lens material rho = 1140, c = 1130 under water):
+    exercises the per-side c^2 of the average flux and the coarse side's c-^2 / c+^2 factor, and the
+    harmonic-mean penalty, from a rough random state."""
+    from sem_inputs.workloads import cfl_dt
+    rec = conforming_cut_config(nel_xy=6, nz_lo=2, nz_hi=3, degree=5, degree_hi=nh, ratio=ratio, h=25e-6,
+                                bc_top=1)
+    rec["boxes"][0]["c"], rec["boxes"][0]["rho"] = 1130.0, 1140.0
+    rec["dt"] = cfl_dt(rec["boxes"])
+    st = random_state(rec, seed=13)
+    for n in (1, 3, 30):
+        nm = oracle_run(rec, n, state=st)
+        sim = gpu_run(rec, n, state=st)
+        for k, v in compare(sim, nm).items():
+            assert v < TOL, (n, k, v)
+        sim.close()
