@@ -395,3 +395,80 @@ def obstacle_config(nel=(6, 6, 4), degree=3, h=25e-6, solid_lo=(2, 2, 1), solid_
     rec["boxes"][0]["bc"] = list(bc) if bc is not None else [BC_RIGID] * 5 + [BC_ABSORBING]
     rec["boxes"][0]["solid"] = solid_block(nel, solid_lo, solid_hi)
     return rec
+
+
+def obstacle_pmut_config(n_cycles=1, n_steps=2160, with_obstacle=True):
+    """The paper's Section 6.2 scenario at desk scale: one PMUT on the bottom face
+    transmits a tone burst, switches to open-circuit reception (Eq. 3) at t_bar = the burst's end, and
+    receives the echo of a rigid obstacle -- a 250 x 250 x 25 um solid slab (the paper's obstacle
+    thickness h_2 = 25 um; it spans 5/6 of the box width as r_obs / r = 1700 / 2000 does) 300 um above
+    the membrane.  Water, N = 3, h = 25 um, 12 x 12 x 16 elements;
+    absorbing lateral and top faces (the paper's absorbing outer boundary), rigid bottom around the
+    membrane.  Config-0 membrane physics (100 um square, 3 modes); n_cycles = 1 keeps the burst
+    (1/3 us) shorter than the echo delay (0.4 us).  RX capacitance: reading R14."""
+    h, nel = 25 * UM, (12, 12, 16)
+    boxes = [_box((0, 0, 0), tuple(h * n for n in nel), nel, 3,
+                  [BC_ABSORBING] * 4 + [BC_RIGID, BC_ABSORBING])]
+    pm = _pmut([[150 * UM, 150 * UM]], MODES_3, FREQS_3, None, [0.0])
+    pm["n_cycles"] = int(n_cycles)
+    pm["rx"] = True
+    pm["amp_v"] = DRIVE_V
+    pm["t_switch"] = n_cycles / DRIVE_F0
+    rec = {"name": "obstacle_pmut", "boxes": boxes, "pmut": pm, "n_steps": int(n_steps), "seed": 0}
+    rec = _finish(rec)
+    if with_obstacle:
+        rec["boxes"][0]["solid"] = solid_block(nel, (1, 1, 12), (11, 11, 13))
+    return rec
+
+
+def curved_interface_config(nf=(6, 6, 2), nc=(4, 4, 2), degree_f=4, degree_c=3, hf=25e-6, jitter=0.15, seed=0,
+                            bc_top=BC_RIGID, c_f=C_WATER, c_c=C_WATER, alpha=PENALTY_ALPHA, n_steps=100, cfl=0.25,
+                            coarse_height=75e-6, nested_jitter=False):
+    """Two curved (vertex-lattice) boxes stacked in z, joined by a general non-conforming DG interface
+    (the interface quadrature of P:L912-938 with Algorithm 3's matching,
+    P:L1062-1080, on trilinear faces).  The fine box has nf elements of degree degree_f and edge hf, the
+    coarse box above it nc elements of degree degree_c over the same lateral extent L = nf[0] hf, so the
+    lattices need not nest (6 : 4 is a 1.5 : 1 ratio); the coarse box is coarse_height tall.  The interior vertices of the interface plane move
+    in-plane by U(-jitter, jitter) x edge, independently on the two sides (seeded), so the two face sets
+    tile the same plane without matching; every other vertex stays on the affine lattice.  With
+    nested_jitter (nf a multiple of nc) only the coarse vertices are drawn and the fine interface
+    vertices are the coarse faces' bilinear maps at the sub-lattice points: curved faces that nest.  Faces rigid
+    except the coarse top (bc_top)."""
+    rng = np.random.default_rng(seed)
+    L = nf[0] * hf
+    hc = L / nc[0]
+    hcz = coarse_height / nc[2]
+    z0 = nf[2] * hf
+
+    def lattice(nel, h, zb, jitter_layer):
+        nx, ny, nz = (n + 1 for n in nel)
+        Z, Y, X = np.meshgrid(zb + np.arange(nz) * h[2], np.arange(ny) * h[1], np.arange(nx) * h[0], indexing="ij")
+        pts = np.stack([X, Y, Z], axis=-1)            # [nz][ny][nx][3]
+        if jitter > 0.0:
+            J = rng.uniform(-jitter, jitter, size=(ny, nx, 2)) * np.array(h[:2])
+            J[0, :, :] = J[-1, :, :] = 0.0
+            J[:, 0, :] = J[:, -1, :] = 0.0
+            pts[jitter_layer, :, :, :2] += J
+        return pts.reshape(-1, 3)
+
+    fine = _box((0, 0, 0), (L, L, z0), nf, degree_f, [BC_RIGID] * 5 + [BC_INTERFACE], c=c_f)
+    coarse = _box((0, 0, z0), (L, L, coarse_height), nc, degree_c, [BC_RIGID] * 4 + [BC_INTERFACE, bc_top], c=c_c)
+    fine["vertices"] = lattice(nf, (hf, hf, hf), 0.0, nf[2])
+    coarse["vertices"] = lattice(nc, (hc, hc, hcz), z0, 0)
+    if nested_jitter:
+        R = nf[0] // nc[0]
+        if nf[0] != R * nc[0] or nf[1] != R * nc[1]:
+            raise ValueError("nested_jitter needs nf = R nc laterally")
+        cv = coarse["vertices"].reshape(nc[2] + 1, nc[1] + 1, nc[0] + 1, 3)[0]     # interface layer
+        fv = fine["vertices"].reshape(nf[2] + 1, nf[1] + 1, nf[0] + 1, 3)
+        for j in range(nf[1] + 1):
+            for i in range(nf[0] + 1):
+                I, Jc = min(i // R, nc[0] - 1), min(j // R, nc[1] - 1)
+                u, v = i / R - I, j / R - Jc
+                fv[nf[2], j, i] = ((1 - u) * (1 - v) * cv[Jc, I] + u * (1 - v) * cv[Jc, I + 1] +
+                                   (1 - u) * v * cv[Jc + 1, I] + u * v * cv[Jc + 1, I + 1])
+        fine["vertices"] = fv.reshape(-1, 3)
+    rec = {"name": "curved_iface", "boxes": [fine, coarse], "n_steps": n_steps, "seed": seed,
+           "interface": {"fine_box": 0, "coarse_box": 1, "alpha": alpha}}
+    rec["dt"] = cfl_dt(rec["boxes"], cfl)
+    return _finish(rec)
