@@ -79,10 +79,9 @@ typedef struct {
     double dt;                   /* time step [s], caller-computed (reading R8)          */
     int device;                  /* CUDA device ordinal                                  */
     void* stream;                /* cudaStream_t to enqueue on; NULL -> library stream   */
-    int rank, world;             /* y-slab decomposition: rank's slab = elements
-                                    [r nel_y/world, (r+1) nel_y/world) of every box (nel_y must be
-                                    divisible by world; cuts must miss the membranes and align with
-                                    the coarse elements of an interface -> SEM_E_PARTITION)       */
+    int rank, world;             /* y-slab decomposition: rank r's slab = box-0 elements
+                                    [slab_y0[r], slab_y0[r+1]) along y and the same y range of every
+                                    other box (see slab_y0)                                      */
     const void* nccl_unique_id;  /* ncclUniqueId (128 bytes) when world > 1, else NULL  */
     int flags;                   /* SEM_F_*                                              */
     /* Optional caller allocator for every persistent device array of the context (e.g. the torch
@@ -92,6 +91,12 @@ typedef struct {
     void* (*dev_alloc)(size_t bytes, void* user);
     void (*dev_free)(void* ptr, void* user);
     void* alloc_user;
+    /* Optional slab plan [world + 1]: box-0 element y index where each slab starts (0 first, nel_y
+     * last, increasing; from sem_slab_plan).  NULL -> equal slabs (nel_y divisible by world).  Every
+     * cut must be an element boundary of every box (so the cuts of a 2:1 interface sit on coarse
+     * elements) -> SEM_E_PARTITION otherwise; cuts crossing a membrane are rejected by
+     * sem_pmut_attach (SEM_E_PARTITION). */
+    const long long* slab_y0;
 } sem_mesh_desc;
 
 /* Create the context: validates boxes, builds the 1D GLL tables and allocates p (two time
@@ -115,8 +120,10 @@ sem_status sem_nccl_unique_id(void* out128);
  * in [0, n_cycles/f0] (reading R10) for t <= t_switch; (1/C) sum_m eta_m q_m after (Eq. 3).
  * Arrays: center [n_pmut*2] (x, y), mode_mn [n_modes*2], freq_hz [n_pmut*n_modes] (k-major),
  * modal_mass / damping_ratio / eta [n_modes], delay_s [n_pmut].  n_modes <= 8.
- * Errors: SEM_E_ARG (membranes overlapping or off the face, zero-node membrane, rx with C <= 0),
- * SEM_E_STATE (already attached). */
+ * The box may be a structured box or an affine obstacle box (sem_box_set_obstacle, called first);
+ * curved (vertex-lattice) boxes carry no PMUT (SEM_E_STATE).
+ * Errors: SEM_E_ARG (membranes overlapping or off the face, zero-node membrane, membrane on a solid
+ * element's face, rx with C <= 0), SEM_E_STATE (already attached, curved box). */
 typedef struct {
     int box, face;
     int n_pmut, n_modes;
@@ -137,9 +144,11 @@ typedef struct {
 sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pm);
 
 /* Host-only (no device touched): the y-slab plan of `world` slabs for these global boxes and (optional)
- * PMUT array.  slab_x0[world+1] receives the box-0 element y index where each slab starts.
- * SEM_E_PARTITION if nel_y is not divisible by world, a cut crosses a membrane, or a cut is not
- * aligned with the coarse elements of a 2:1 interface (box 0 +z / box 1 -z tagged INTERFACE). */
+ * PMUT array.  slab_x0[world+1] receives the box-0 element y index where each slab starts: equal slabs
+ * when they are admissible, else the admissible cuts nearest to the equal ones (uneven slabs): every cut
+ * on an element boundary of every box (so a 2:1 interface's face pairs stay slab-local) and in a gap
+ * between membranes (the paper's membrane-preserving partition).  SEM_E_PARTITION if
+ * no admissible plan exists. */
 sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, const sem_pmut_desc* pm,
                          long long* slab_x0);
 
@@ -151,6 +160,13 @@ sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, cons
  * the fine trace is interpolated to the points and the fine side's terms projected back onto the
  * fine face nodes; single slab only (world 1, no emulation: SEM_E_PARTITION otherwise).
  * Requires matching lateral extents and h_coarse = R h_fine for an integer R >= 1.
+ * Curved boxes (sem_box_set_vertices / sem_box_set_obstacle on BOTH boxes, before this call): the
+ * general non-conforming interface -- any trilinear face sets that tile the same surface, lattices that
+ * need not nest.  Algorithm 3 (sem_face_match) gives every
+ * fine-face GLL node its coarse owner and x_hat^- at setup; per step one kernel evaluates the face terms
+ * of Eq. 7 at those points (J = p+ - p-(x_hat^-), A = {c^2 d_n p}, n = n+ of the fine face) and adds them
+ * to both boxes' assembled residuals.  GLL rule only, world 1 only (SEM_E_PARTITION), SEM_E_STATE if only
+ * one of the boxes is curved, SEM_E_UNMATCHED if a quadrature node has no owner.
  * Errors: SEM_E_ARG (geometry), SEM_E_UNMATCHED (lattices do not nest), SEM_E_STATE. */
 sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, double penalty_alpha,
                                   int quad_rule);
@@ -162,8 +178,9 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
  * metric terms w_q c^2 |J| J^-1 J^-T recomputed from the 8 vertices at every GLL point (nothing
  * stored per quadrature point), FP64 atomics into an assembled residual, and a nodal kick-drift with
  * the assembled lumped mass and ABC diagonal (computed here on the host).  Call right after
- * sem_mesh_create: curved boxes carry no PMUT / interface / PML / plane wave (SEM_E_STATE), world 1
- * only (SEM_E_PARTITION).  Caller owns `verts` (copied).  Errors: SEM_E_ARG (size, non-positive
+ * sem_mesh_create: curved boxes carry no PMUT / PML / plane wave (SEM_E_STATE); an interface between
+ * two curved boxes is the general one of sem_dg_interface_build (call that afterwards); world 1 only
+ * (SEM_E_PARTITION).  Caller owns `verts` (copied).  Errors: SEM_E_ARG (size, non-positive
  * Jacobian at a GLL point), SEM_E_STATE, SEM_E_OOM. */
 sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size_t n_verts);
 
@@ -175,9 +192,14 @@ sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size
  * absorbing-face terms are skipped.  Nodes of no fluid element (obstacle interiors) are held at 0
  * (sem_read_pressure returns 0 there after the first step).  The box moves to the element-scatter
  * path of sem_box_set_vertices (with its own affine vertex lattice unless vertices are set, before or
- * after this call) and carries the same restrictions: no PMUT / interface / PML / plane wave
- * (SEM_E_STATE), world 1 only (SEM_E_PARTITION).  Caller owns `solid` (copied).  Errors: SEM_E_ARG
- * (size, every element solid), SEM_E_STATE (already set), SEM_E_OOM. */
+ * after this call) and carries the same restrictions (no PML / plane wave: SEM_E_STATE; a general
+ * interface only with another curved / obstacle box;
+ * world 1 only: SEM_E_PARTITION) except one: an affine obstacle box (no vertices set) may carry the
+ * PMUT array (the paper's Section 6.2 scenario, a PMUT transmitting to an obstacle and receiving its
+ * echo): the modal kernel is unchanged and the nodal update adds f = kappa B^T qdd on
+ * the z = 0 face.  Call it before sem_pmut_attach (SEM_E_STATE otherwise); a membrane on the face of
+ * a solid element is rejected by sem_pmut_attach (SEM_E_ARG).  Caller owns `solid` (copied).
+ * Errors: SEM_E_ARG (size, every element solid), SEM_E_STATE (already set), SEM_E_OOM. */
 sem_status sem_box_set_obstacle(sem_ctx* ctx, int box, const unsigned char* solid, size_t n_el);
 
 /* Perfectly matched layer (Eq. 1 lines 1-3; coefficients P:L271-277; profile P:L280-289)

@@ -1088,6 +1088,184 @@ static void launch_iface_lg(const IfaceParams& p, cudaStream_t s) {
     iface_gather_x_lg<<<(unsigned)((nc + T - 1) / T), T, 0, s>>>(p);
 }
 
+// Fused SIPG flux on the 2:1 face lattice for compile-time (NF, NC, R) (configs 2-4: 5, 3, 2): one block
+// per TC x TC tile of coarse elements does what iface_coarse_trace -> iface_fine -> iface_gather_y ->
+// iface_gather_x do, with the intermediate face arrays in shared memory.  The tile's footprint extends
+// one coarse element below it in x and y (the coarse nodes on its lower edges also collect the fine
+// points of that element), so every coarse node it owns gets its complete sum: the halo element's fine
+// flux is recomputed (L2-resident inputs) instead of exchanged.
+//   (1) coarse trace p- and d_n p- at the footprint's coarse face nodes (bottom element layer);
+//   (2) fine flux at the footprint's fine face nodes: J = p+ - p-(x_q), A = 1/2 (c+^2 d_n p+ + c-^2 d_n p-),
+//       tau = gamma J - A, sigma = -1/2 c+^2 J (written for the fine nodes the tile owns) and the weighted
+//       coarse-side terms g1 = -W tau, g2 = W (c-^2/c+^2) sigma (W = m_x m_y) in shared memory;
+//   (3) transposed interpolation along y, then (4) along x, divided by the coarse face masses.
+constexpr int kIfTC = 4;   // coarse elements per tile edge
+template <int NF, int NC, int R>
+struct IfFused {
+    static constexpr int NFR = NF * R;                 // fine nodes per coarse element edge
+    static constexpr int FW = (kIfTC + 1) * NFR + 1;   // fine footprint nodes per direction
+    static constexpr int CW = (kIfTC + 1) * NC + 1;    // coarse footprint nodes per direction
+    static constexpr int CO = kIfTC * NC + 1;          // owned coarse rows (the last tile: + the box's last)
+    static constexpr int SMEM = 8 * (2 * CW * CW + 2 * FW * FW + 2 * CO * FW);
+};
+
+template <int NF, int NC, int R>
+__global__ void __launch_bounds__(256) iface_fused(const __grid_constant__ IfaceParams p) {
+    using G = IfFused<NF, NC, R>;
+    constexpr int NFR = G::NFR, FW = G::FW, CW = G::CW, CO = G::CO, TC = kIfTC;
+    extern __shared__ double ifs[];
+    double* const st = ifs;                 // [CW][CW] coarse trace
+    double* const sd = st + CW * CW;        // [CW][CW] coarse normal derivative
+    double* const g1 = sd + CW * CW;        // [FW][FW] weighted fine terms (row = y)
+    double* const g2 = g1 + FW * FW;
+    double* const h1 = g2 + FW * FW;        // [CO][FW] after the y pass
+    double* const h2 = h1 + CO * FW;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int ex0 = (int)blockIdx.x * TC - 1, ey0 = (int)blockIdx.y * TC - 1;   // footprint's first element
+    const long long NXf = p.NXf, NYf = p.NYf, NXc = p.NXc, NYc = p.NYc;
+    const int nelcx = p.nelcx, nelcy = p.nelcy;
+    // (1) coarse trace
+    const long long Sc = p.PXc * NYc;
+    for (int k = tid; k < CW * CW; k += nth) {
+        const int i = k % CW, j = k / CW;
+        const long long jx = (long long)ex0 * NC + i, jy = (long long)ey0 * NC + j;
+        double t = 0.0, d = 0.0;
+        if (jx >= 0 && jx < NXc && jy >= 0 && jy < NYc) {
+            const double* col = p.Pc + jy * p.PXc + jx;
+            t = __ldg(col);
+#pragma unroll
+            for (int c = 0; c <= NC; ++c) d = fma(p.dcB[c], __ldg(col + c * Sc), d);
+        }
+        st[k] = t;
+        sd[k] = d;
+    }
+    __syncthreads();
+    // (2) fine flux
+    const long long Sf = p.PXf * NYf;
+    const double* top = p.Pf + (p.NZf - 1) * Sf;
+    const long long ox = (long long)blockIdx.x * TC * NFR, oy = (long long)blockIdx.y * TC * NFR;   // owned start
+    const double crat = p.cc2 / p.cf2;
+    for (int k = tid; k < FW * FW; k += nth) {
+        const int i = k % FW, j = k / FW;
+        const long long ix = (long long)ex0 * NFR + i, iy = (long long)ey0 * NFR + j;
+        double v1 = 0.0, v2 = 0.0;
+        if (ix >= 0 && ix < NXf && iy >= 0 && iy < NYf) {
+            const double* node = top + iy * p.PXf + ix;
+            const double pp = __ldg(node);
+            double dpp = 0.0;
+#pragma unroll
+            for (int c = 0; c <= NF; ++c) dpp = fma(p.dfT[c], __ldg(node - (long long)(NF - c) * Sf), dpp);
+            // coarse element (footprint-local) and local fine index of this node in it
+            const int elx = i / NFR < TC ? i / NFR : TC, ely = j / NFR < TC ? j / NFR : TC;
+            const int qx = i - elx * NFR, qy = j - ely * NFR;
+            double pm = 0.0, dpm = 0.0;
+#pragma unroll
+            for (int b = 0; b <= NC; ++b) {
+                const double wy = __ldg(p.I + qy * (NC + 1) + b);
+                const int row = (ely * NC + b) * CW + elx * NC;
+                double rt = 0.0, rd = 0.0;
+#pragma unroll
+                for (int a = 0; a <= NC; ++a) {
+                    const double wx = __ldg(p.I + qx * (NC + 1) + a);
+                    rt = fma(wx, st[row + a], rt);
+                    rd = fma(wx, sd[row + a], rd);
+                }
+                pm = fma(wy, rt, pm);
+                dpm = fma(wy, rd, dpm);
+            }
+            const double J = pp - pm;
+            const double A = 0.5 * (p.cf2 * dpp + p.cc2 * dpm);
+            const double tau = p.gamma * J - A, sig = -0.5 * p.cf2 * J;
+            const bool own = ix >= ox && (ix < ox + TC * NFR || ix == NXf - 1) && iy >= oy &&
+                             (iy < oy + TC * NFR || iy == NYf - 1);
+            if (own) {
+                p.tauf[iy * NXf + ix] = tau;
+                p.sigf[iy * NXf + ix] = sig;
+            }
+            if (!(p.skip_iy0 && iy == 0)) {   // the fine cut line of a slab belongs to the lower slab
+                const double W = __ldg(p.mxf + ix) * __ldg(p.myf + iy);
+                v1 = -W * tau;
+                v2 = crat * W * sig;
+            }
+        }
+        g1[k] = v1;
+        g2[k] = v2;
+    }
+    __syncthreads();
+    // coarse node (footprint-local index jl) -> element el and local index b as in gather_1d
+    auto split = [](int jl, int e0, int nelc, int& el, int& b) {
+        el = jl / NC;
+        b = jl - el * NC;
+        if (e0 + el > nelc - 1) {   // the box's last coarse node: b = NC of the last element
+            el -= 1;
+            b = NC;
+        }
+    };
+    // owned coarse rows / columns: footprint-local jl in [NC, NC + CO), global j < n, and j in the tile's
+    // range (the box's last node belongs to the last tile)
+    auto owned = [](long long j, long long j0, long long n) { return j < n && (j < j0 + TC * NC || j == n - 1); };
+    const long long jx0 = (long long)blockIdx.x * TC * NC, jy0 = (long long)blockIdx.y * TC * NC;
+    // (3) y pass: h[jr][i] = sum_q psi_b(x_q) g[q][i] over the fine rows of the coarse row's support
+    for (int k = tid; k < CO * FW; k += nth) {
+        const int i = k % FW, jr = k / FW, jl = NC + jr;
+        const long long jy = (long long)ey0 * NC + jl;
+        double s1 = 0.0, s2 = 0.0;
+        if (owned(jy, jy0, NYc)) {
+            int el, b;
+            split(jl, ey0, nelcy, el, b);
+            const int qend = (ey0 + el == nelcy - 1) ? NFR : NFR - 1;
+            for (int q = 0; q <= qend; ++q) {
+                const double w = __ldg(p.I + q * (NC + 1) + b);
+                s1 = fma(w, g1[(el * NFR + q) * FW + i], s1);
+                s2 = fma(w, g2[(el * NFR + q) * FW + i], s2);
+            }
+            if (b == 0 && el > 0) {   // the element below (its q = 0 node has weight I[0][NC] = 0)
+                for (int q = 1; q < NFR; ++q) {
+                    const double w = __ldg(p.I + q * (NC + 1) + NC);
+                    s1 = fma(w, g1[((el - 1) * NFR + q) * FW + i], s1);
+                    s2 = fma(w, g2[((el - 1) * NFR + q) * FW + i], s2);
+                }
+            }
+        }
+        h1[k] = s1;
+        h2[k] = s2;
+    }
+    __syncthreads();
+    // (4) x pass and the coarse face masses
+    for (int k = tid; k < CO * CO; k += nth) {
+        const int ir = k % CO, jr = k / CO, il = NC + ir;
+        const long long jx = (long long)ex0 * NC + il, jy = (long long)ey0 * NC + NC + jr;
+        if (!owned(jx, jx0, NXc) || !owned(jy, jy0, NYc)) continue;
+        int el, b;
+        split(il, ex0, nelcx, el, b);
+        const int qend = (ex0 + el == nelcx - 1) ? NFR : NFR - 1;
+        double s1 = 0.0, s2 = 0.0;
+        for (int q = 0; q <= qend; ++q) {
+            const double w = __ldg(p.I + q * (NC + 1) + b);
+            s1 = fma(w, h1[jr * FW + el * NFR + q], s1);
+            s2 = fma(w, h2[jr * FW + el * NFR + q], s2);
+        }
+        if (b == 0 && el > 0) {
+            for (int q = 1; q < NFR; ++q) {
+                const double w = __ldg(p.I + q * (NC + 1) + NC);
+                s1 = fma(w, h1[jr * FW + (el - 1) * NFR + q], s1);
+                s2 = fma(w, h2[jr * FW + (el - 1) * NFR + q], s2);
+            }
+        }
+        const double inv = 1.0 / (__ldg(p.mxc + jx) * __ldg(p.myc + jy));
+        p.tauc[jy * NXc + jx] = s1 * inv;
+        p.sigc[jy * NXc + jx] = s2 * inv;
+    }
+}
+
+template <int NF, int NC, int R>
+static int launch_iface_fused(const IfaceParams& p, cudaStream_t s) {
+    using G = IfFused<NF, NC, R>;
+    const dim3 grid((unsigned)((p.nelcx + kIfTC - 1) / kIfTC), (unsigned)((p.nelcy + kIfTC - 1) / kIfTC));
+    iface_fused<NF, NC, R><<<grid, 256, G::SMEM, s>>>(p);
+    return 1;
+}
+
 template <int NF, int NC, int R>
 static void launch_iface_t(const IfaceParams& p, cudaStream_t s) {
     const int T = 256;
@@ -1098,10 +1276,26 @@ static void launch_iface_t(const IfaceParams& p, cudaStream_t s) {
     iface_gather_x<NF, NC, R><<<(unsigned)((nc + T - 1) / T), T, 0, s>>>(p);
 }
 
-void launch_iface(const IfaceParams& p, cudaStream_t s) {
-    if (p.lg) launch_iface_lg(p, s);
-    else if (p.Nf == 5 && p.Nc == 3 && p.R == 2) launch_iface_t<5, 3, 2>(p, s);   // configs 2-4
-    else launch_iface_t<0, 0, 0>(p, s);
+#ifndef SEM_IFACE_FUSED
+#define SEM_IFACE_FUSED 1
+#endif
+void iface_prepare(int Nf, int Nc, int R) {   // outside any stream capture (function attributes)
+    if (SEM_IFACE_FUSED && Nf == 5 && Nc == 3 && R == 2)
+        cudaFuncSetAttribute(iface_fused<5, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, IfFused<5, 3, 2>::SMEM);
+}
+
+int launch_iface(const IfaceParams& p, cudaStream_t s) {
+    if (p.lg) {
+        launch_iface_lg(p, s);
+        return 5;
+    }
+    if (p.Nf == 5 && p.Nc == 3 && p.R == 2) {   // configs 2-4
+        if (SEM_IFACE_FUSED) return launch_iface_fused<5, 3, 2>(p, s);
+        launch_iface_t<5, 3, 2>(p, s);
+        return 4;
+    }
+    launch_iface_t<0, 0, 0>(p, s);
+    return 4;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1590,7 +1784,13 @@ __global__ void __launch_bounds__(256, 8) curved_update_kernel(const __grid_cons
 #pragma unroll 1
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
         // read-only (non-coherent) loads: each element is read once, before this thread overwrites it
-        const double2 wv = __ldg(W2 + i), mi = __ldg(M2 + i), r = __ldg(R2 + i), cd = __ldg(C2 + i), pv = __ldg(P2 + i);
+        const double2 wv = __ldg(W2 + i), mi = __ldg(M2 + i), cd = __ldg(C2 + i), pv = __ldg(P2 + i);
+        double2 r = __ldg(R2 + i);
+        if (p.F && 2 * i < p.PX * p.NY) {   // z = 0 plane: PMUT forcing f = kappa B^T qdd (Eq. 11)
+            const long long d = 2 * i, ix = d % p.PX, iy = d / p.PX;   // PX even: both nodes on one row
+            if (ix < p.NX) r.x -= __ldg(p.F + iy * p.NX + ix) * __ldg(p.fmx + ix) * __ldg(p.fmy + iy);
+            if (ix + 1 < p.NX) r.y -= __ldg(p.F + iy * p.NX + ix + 1) * __ldg(p.fmx + ix + 1) * __ldg(p.fmy + iy);
+        }
         double2 wn, pn;
         wn.x = fma(p.dt, -mi.x * r.x - cd.x * wv.x, wv.x);
         wn.y = fma(p.dt, -mi.y * r.y - cd.y * wv.y, wv.y);
@@ -1617,6 +1817,78 @@ void launch_curved(const CurvedParams& p, cudaStream_t s) {
     const long long n2 = p.PX * p.NY * p.NZ / 2;
     const long long want = (n2 + 255) / 256, cap = 8LL * device_sms();
     curved_update_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(p);
+}
+
+// ------------------------------------------------------------------------------------------------
+// General non-conforming SIPG interface (curved boxes, lattices that need not
+// nest): one thread per fine-face quadrature point x_q (a fine face GLL node, reading R9), the owner
+// coarse element and x_hat^- from Algorithm 3 (setup).  With J = p+ - p-(x_hat^-), A = 1/2 (c+^2 d_n p+
+// + c-^2 d_n p-) (n = n+ on both sides), T = W (gamma J - A), S = -1/2 W J, the rows of the face matrix
+// of Eq. 7 (the oracle's K_F) give
+//   fine i:   r_i += T phi_i(x_q) + c+^2 S d_n phi_i(x_q)      (collocated: phi_i(x_q) = delta)
+//   coarse i: r_i += -T phi_i(x_hat^-) + c-^2 S d_n phi_i(x_hat^-)
+// with d_n phi = (J^-1 n) . grad_hat phi; added to the boxes' assembled residuals with FP64 atomics.
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) iface_general_kernel(const __grid_constant__ GIfaceParams p) {
+    const long long qp = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (qp >= p.nqp) return;
+    const int Nf = p.Nf, Nc = p.Nc, q1 = Nf + 1, c1 = Nc + 1;
+    const int q = (int)(qp % (q1 * q1)), a = q % q1, b = q / q1;
+    const long long SF = p.PXf * p.NYf, SC = p.PXc * p.NYc;
+    const long long fb = p.fbase[qp] + a + b * p.PXf + Nf * SF;   // fine node (a, b, Nf)
+    const double pp = __ldg(p.Pf + fb);
+    double dxi = 0.0, deta = 0.0, dzeta = 0.0;
+    for (int j = 0; j <= Nf; ++j) {
+        dxi = fma(p.Df[a][j], __ldg(p.Pf + fb + (j - a)), dxi);
+        deta = fma(p.Df[b][j], __ldg(p.Pf + fb + (long long)(j - b) * p.PXf), deta);
+        dzeta = fma(p.Df[Nf][j], __ldg(p.Pf + fb + (long long)(j - Nf) * SF), dzeta);
+    }
+    const double* G = p.geo + qp * 7;
+    const double W = __ldg(G), gp0 = __ldg(G + 1), gp1 = __ldg(G + 2), gp2 = __ldg(G + 3);
+    const double gm0 = __ldg(G + 4), gm1 = __ldg(G + 5), gm2 = __ldg(G + 6);
+    const double dnp = gp0 * dxi + gp1 * deta + gp2 * dzeta;
+    const double* B = p.bas + qp * 6 * c1;   // lx, dlx, ly, dly, lz, dlz
+    const long long cb = p.cbase[qp];
+    double pm = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+    for (int c = 0; c <= Nc; ++c)
+        for (int bb = 0; bb <= Nc; ++bb) {
+            const double ly = __ldg(B + 2 * c1 + bb), dly = __ldg(B + 3 * c1 + bb);
+            const double lz = __ldg(B + 4 * c1 + c), dlz = __ldg(B + 5 * c1 + c);
+            for (int aa = 0; aa <= Nc; ++aa) {
+                const double v = __ldg(p.Pc + cb + aa + (long long)bb * p.PXc + (long long)c * SC);
+                const double lx = __ldg(B + aa), dlx = __ldg(B + c1 + aa);
+                pm = fma(lx * ly * lz, v, pm);
+                gx = fma(dlx * ly * lz, v, gx);
+                gy = fma(lx * dly * lz, v, gy);
+                gz = fma(lx * ly * dlz, v, gz);
+            }
+        }
+    const double dnm = gm0 * gx + gm1 * gy + gm2 * gz;
+    const double J = pp - pm;
+    const double A = 0.5 * (p.cf2 * dnp + p.cc2 * dnm);
+    const double T = W * (p.gamma * J - A), S = -0.5 * W * J;
+    atomicAdd(p.resF + fb, T);
+    const double sF = p.cf2 * S;
+    for (int j = 0; j <= Nf; ++j) {
+        atomicAdd(p.resF + fb + (j - a), sF * gp0 * p.Df[a][j]);
+        atomicAdd(p.resF + fb + (long long)(j - b) * p.PXf, sF * gp1 * p.Df[b][j]);
+        atomicAdd(p.resF + fb + (long long)(j - Nf) * SF, sF * gp2 * p.Df[Nf][j]);
+    }
+    const double sC = p.cc2 * S;
+    for (int c = 0; c <= Nc; ++c)
+        for (int bb = 0; bb <= Nc; ++bb) {
+            const double ly = __ldg(B + 2 * c1 + bb), dly = __ldg(B + 3 * c1 + bb);
+            const double lz = __ldg(B + 4 * c1 + c), dlz = __ldg(B + 5 * c1 + c);
+            for (int aa = 0; aa <= Nc; ++aa) {
+                const double lx = __ldg(B + aa), dlx = __ldg(B + c1 + aa);
+                const double v = -T * lx * ly * lz + sC * (gm0 * dlx * ly * lz + gm1 * lx * dly * lz + gm2 * lx * ly * dlz);
+                atomicAdd(p.resC + cb + aa + (long long)bb * p.PXc + (long long)c * SC, v);
+            }
+        }
+}
+
+void launch_iface_general(const GIfaceParams& p, cudaStream_t s) {
+    if (p.nqp > 0) iface_general_kernel<<<(unsigned)((p.nqp + 127) / 128), 128, 0, s>>>(p);
 }
 
 __global__ void step_bump_kernel(long long* step) { *step += 1; }

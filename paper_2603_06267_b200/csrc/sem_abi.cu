@@ -321,32 +321,103 @@ NcclApi& nccl_api() {
 bool nccl_mode(const sem_ctx* ctx) { return ctx->world > 1 && !ctx->emulate; }
 
 // ---- partition rules (shared by sem_mesh_create / sem_pmut_attach / sem_dg_interface_build and the
-//      host-only sem_slab_plan): G equal y-slabs of every box, cuts at the same y for all boxes.
+//      host-only sem_slab_plan): y-slabs, cuts at the same y for all boxes, given as box-0 element y
+//      indices cuts[0] = 0 < cuts[1] < ... < cuts[G] = nel_y(box 0).
 //      y (not x): a cut plane iy = const is, per z-plane, one contiguous lattice row, so the cut-plane
 //      partial rows and fix-ups are coalesced (an x cut touches one node per row).
-const char* slabs_divisible(const sem_box_desc* boxes, int n, int G) {
-    for (int i = 0; i < n; ++i)
-        if (boxes[i].nel[1] % G) return "nel_y of every box must be divisible by the number of slabs";
+// box b's element index of box-0 element boundary k, or -1 if it is not an element boundary of box b
+long long cut_in_box(const sem_box_desc& b0, const sem_box_desc& b, long long k) {
+    const long long num = k * (long long)b.nel[1];
+    return num % b0.nel[1] ? -1 : num / b0.nel[1];
+}
+
+const char* plan_invalid(const sem_box_desc* boxes, int n, const std::vector<long long>& cuts) {
+    const int G = (int)cuts.size() - 1;
+    if (G < 1 || cuts[0] != 0 || cuts[G] != boxes[0].nel[1]) return "slab plan must run from 0 to nel_y";
+    for (int r = 0; r < G; ++r) {
+        if (cuts[r + 1] <= cuts[r]) return "slab plan must be increasing";
+        for (int i = 0; i < n; ++i)
+            if (cut_in_box(boxes[0], boxes[i], cuts[r + 1]) < 0)
+                return "every slab cut must be an element boundary of every box";
+    }
     return nullptr;
 }
 
-// slab owning a membrane spanning [y0, y0 + a] on box g; -1 if a cut crosses or touches it (membranes
-// are never split across GPUs: the paper's membrane-preserving partition)
-int membrane_slab(const sem_box_desc& g, int G, double y0, double a) {
-    const double hy = g.extent[1] / g.nel[1];
+// y position of box-0 element boundary k
+double cut_y(const sem_box_desc& b0, long long k) { return b0.origin[1] + b0.extent[1] / b0.nel[1] * (double)k; }
+
+// slab owning a membrane spanning [y0, y0 + a]; -1 if a cut crosses or touches it (membranes are never
+// split across GPUs: the paper's membrane-preserving partition)
+int membrane_slab(const sem_box_desc& b0, const std::vector<long long>& cuts, double y0, double a) {
+    const double hy = b0.extent[1] / b0.nel[1];
     int slab = 0;
-    for (int r = 1; r < G; ++r) {
-        const double cut = g.origin[1] + hy * (double)(g.nel[1] / G) * r;
+    for (size_t r = 1; r + 1 < cuts.size(); ++r) {
+        const double cut = cut_y(b0, cuts[r]);
         if (y0 <= cut + 1e-9 * hy && y0 + a >= cut - 1e-9 * hy) return -1;
-        if (y0 > cut) slab = r;
+        if (y0 > cut) slab = (int)r;
     }
     return slab;
 }
 
-// cuts must fall on coarse-element boundaries so every 2:1 interface face pair is slab-local
-bool interface_aligned(const sem_box_desc& F, const sem_box_desc& C, int G) {
-    const int R = F.nel[1] / C.nel[1];
-    return R >= 1 && (F.nel[1] / G) % R == 0;
+std::vector<long long> equal_plan(const sem_box_desc& b0, int G) {
+    std::vector<long long> c(G + 1);
+    for (int r = 0; r <= G; ++r) c[r] = (long long)b0.nel[1] * r / G;
+    return c;
+}
+
+bool plan_ok(const sem_box_desc* boxes, int n, const std::vector<long long>& cuts, const sem_pmut_desc* pm) {
+    if (plan_invalid(boxes, n, cuts)) return false;
+    if (pm)
+        for (int k = 0; k < pm->n_pmut; ++k)
+            if (membrane_slab(boxes[0], cuts, pm->center[2 * k + 1] - 0.5 * pm->side, pm->side) < 0) return false;
+    return true;
+}
+
+// equal slabs if admissible, else greedily the admissible cut nearest to each equal cut
+bool auto_plan(const sem_box_desc* boxes, int n, int G, const sem_pmut_desc* pm, std::vector<long long>& cuts) {
+    const long long nel = boxes[0].nel[1];
+    if (G > nel) return false;
+    if (nel % G == 0 && plan_ok(boxes, n, cuts = equal_plan(boxes[0], G), pm)) return true;
+    std::vector<char> adm(nel + 1, 0);
+    const double a = pm ? pm->side : 0.0;
+    for (long long k = 1; k < nel; ++k) {
+        bool ok = true;
+        for (int i = 0; i < n && ok; ++i) ok = cut_in_box(boxes[0], boxes[i], k) >= 0;
+        if (ok && pm)
+            for (int m = 0; m < pm->n_pmut && ok; ++m) {
+                const double y0 = pm->center[2 * m + 1] - 0.5 * a, hy = boxes[0].extent[1] / nel, cy = cut_y(boxes[0], k);
+                ok = !(y0 <= cy + 1e-9 * hy && y0 + a >= cy - 1e-9 * hy);
+            }
+        adm[k] = ok ? 1 : 0;
+    }
+    // admissible boundaries, then the G-slab plan minimising the largest slab (dynamic programme over
+    // the admissible positions; the largest slab bounds the step time of a strong-scaling run)
+    std::vector<long long> P{0};
+    for (long long k = 1; k < nel; ++k)
+        if (adm[k]) P.push_back(k);
+    P.push_back(nel);
+    const int m = (int)P.size();
+    const long long INF = 1LL << 60;
+    std::vector<std::vector<long long>> dp(G + 1, std::vector<long long>(m, INF));
+    std::vector<std::vector<int>> from(G + 1, std::vector<int>(m, -1));
+    dp[0][0] = 0;
+    for (int r = 1; r <= G; ++r)
+        for (int j = 1; j < m; ++j)
+            for (int i = 0; i < j; ++i) {
+                if (dp[r - 1][i] >= INF) continue;
+                const long long v = std::max(dp[r - 1][i], P[j] - P[i]);
+                if (v < dp[r][j]) {
+                    dp[r][j] = v;
+                    from[r][j] = i;
+                }
+            }
+    if (dp[G][m - 1] >= INF) return false;
+    cuts.assign(G + 1, 0);
+    for (int r = G, j = m - 1; r >= 1; --r) {
+        cuts[r] = P[j];
+        j = from[r][j];
+    }
+    return plan_ok(boxes, n, cuts, pm);
 }
 
 // Slab of global box g: elements [ey0, ey0 + nel_loc) along y.  1D tables (coordinates, face masses)
@@ -498,7 +569,8 @@ sem::CutParams cut_params(sem_ctx* ctx, sem::Part& pt, int side, int bi, int cur
     return c;
 }
 
-sem::CurvedParams curved_params(sem_ctx* ctx, Box& b, int cur) {
+sem::CurvedParams curved_params(sem_ctx* ctx, sem::Part& pt, int bi, int cur) {
+    Box& b = pt.boxes[bi];
     sem::CurvedParams p{};
     p.N = b.N;
     p.NX = b.NX;
@@ -527,6 +599,11 @@ sem::CurvedParams curved_params(sem_ctx* ctx, Box& b, int cur) {
     }
     p.c2 = b.d.c * b.d.c;
     p.dt = ctx->dt;
+    if (pt.pm.on && pt.pm.box == bi) {
+        p.F = pt.pm.F;
+        p.fmx = b.mx;
+        p.fmy = b.my;
+    }
     return p;
 }
 
@@ -633,11 +710,18 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
     if (ctx->itf_on) {
         mark(1, true, s);
         for (auto& pt : ctx->parts) {
+            if (pt.itf.general) {   // curved boxes: the face terms go straight into the residuals
+                sem::GIfaceParams gp = pt.itf.gprm;
+                gp.Pf = pt.boxes[pt.itf.fine].P[cur];
+                gp.Pc = pt.boxes[pt.itf.coarse].P[cur];
+                sem::launch_iface_general(gp, s);
+                ++nl;
+                continue;
+            }
             sem::IfaceParams ip = pt.itf.prm;
             ip.Pf = pt.boxes[pt.itf.fine].P[cur];
             ip.Pc = pt.boxes[pt.itf.coarse].P[cur];
-            sem::launch_iface(ip, s);
-            nl += 4;
+            nl += sem::launch_iface(ip, s);
         }
         mark(1, false, s);
     }
@@ -710,9 +794,9 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
         }
         // curved boxes: element-by-element residual + nodal update (no structured volume launch)
         for (auto& pt : ctx->parts)
-            for (auto& bx : pt.boxes)
-                if (bx.curved) {
-                    sem::launch_curved(curved_params(ctx, bx, cur), s);
+            for (int bi = 0; bi < (int)pt.boxes.size(); ++bi)
+                if (pt.boxes[bi].curved) {
+                    sem::launch_curved(curved_params(ctx, pt, bi, cur), s);
                     nl += 2;
                 }
         if (ls.empty()) {
@@ -846,6 +930,159 @@ sem_status setup_part_buffers(sem_ctx* ctx, sem::Part& pt) {
     return SEM_OK;
 }
 
+// host trilinear map of an element: J[i][j] = dX_i / dxi_j at xi (vertex v = i + 2j + 4k at reference
+// corner (2i-1, 2j-1, 2k-1))
+void trilinear_jacobian(const double* V, const double xi[3], double J[3][3]) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) J[i][j] = 0.0;
+    for (int v = 0; v < 8; ++v) {
+        const double s0 = (v & 1) ? 1.0 : -1.0, s1 = (v & 2) ? 1.0 : -1.0, s2 = (v & 4) ? 1.0 : -1.0;
+        const double f0 = 1.0 + s0 * xi[0], f1 = 1.0 + s1 * xi[1], f2 = 1.0 + s2 * xi[2];
+        const double dN[3] = {0.125 * s0 * f1 * f2, 0.125 * s1 * f0 * f2, 0.125 * s2 * f0 * f1};
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) J[i][j] += dN[j] * V[3 * v + i];
+    }
+}
+
+// x = J^-1 b (Cramer's rule; J is a positive-Jacobian element map)
+void solve3(const double J[3][3], const double b[3], double x[3]) {
+    const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) - J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                       J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    for (int c = 0; c < 3; ++c) {
+        double M[3][3];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) M[i][j] = (j == c) ? b[i] : J[i][j];
+        x[c] = (M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) - M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0])) / det;
+    }
+}
+
+// ell_j'(t) of the Lagrange basis on nodes x: sum_m 1/(x_j - x_m) prod_{k != j, m} (t - x_k)/(x_j - x_k)
+std::vector<double> lagrange_deriv_at(const std::vector<double>& x, double t) {
+    const int n = (int)x.size();
+    std::vector<double> d(n, 0.0);
+    for (int j = 0; j < n; ++j)
+        for (int m = 0; m < n; ++m) {
+            if (m == j) continue;
+            double pr = 1.0 / (x[j] - x[m]);
+            for (int k = 0; k < n; ++k)
+                if (k != j && k != m) pr *= (t - x[k]) / (x[j] - x[k]);
+            d[j] += pr;
+        }
+    return d;
+}
+
+// General non-conforming interface between two curved (element-scatter) boxes: Algorithm 3 on the
+// GPU (sem_face_match: fine +z faces vs coarse -z faces) and per quadrature point the fine face
+// weight W_q = w_a w_b |J_s|, the outward unit normal n+, J_F^-1 n+ at the fine node, J_C^-1 n+ and the
+// coarse 1D basis values / derivatives at x_hat^- (reading R9).
+sem_status build_general_interface(sem_ctx* ctx, int fb, int cb, double gamma) {
+    sem::Part& pt = ctx->parts[0];
+    Box& F = pt.boxes[fb];
+    Box& C = pt.boxes[cb];
+    const sem_box_desc& gF = ctx->gdesc[fb];
+    const sem_box_desc& gC = ctx->gdesc[cb];
+    const int Nf = gF.degree, Nc = gC.degree, q1 = Nf + 1, nq = q1 * q1, c1 = Nc + 1;
+    auto verts_of = [](const Box& b, const sem_box_desc& g, int ex, int ey, int ez, double* out) {
+        const long long nx = g.nel[0] + 1, ny = g.nel[1] + 1;
+        for (int v = 0; v < 8; ++v) {
+            const long long vx = ex + (v & 1), vy = ey + ((v >> 1) & 1), vz = ez + (v >> 2);
+            for (int i = 0; i < 3; ++i) out[3 * v + i] = b.vlat_h[3 * (vx + nx * (vy + ny * vz)) + i];
+        }
+    };
+    const int nfF = gF.nel[0] * gF.nel[1], nfC = gC.nel[0] * gC.nel[1];
+    std::vector<double> fv((size_t)24 * nfF), cv((size_t)24 * nfC);
+    std::vector<int> ff(nfF, 5), cf(nfC, 4);
+    for (int ey = 0; ey < gF.nel[1]; ++ey)
+        for (int ex = 0; ex < gF.nel[0]; ++ex) verts_of(F, gF, ex, ey, gF.nel[2] - 1, &fv[(size_t)24 * (ex + gF.nel[0] * ey)]);
+    for (int ey = 0; ey < gC.nel[1]; ++ey)
+        for (int ex = 0; ex < gC.nel[0]; ++ex) verts_of(C, gC, ex, ey, 0, &cv[(size_t)24 * (ex + gC.nel[0] * ey)]);
+    const sem_face_set fs{nfF, fv.data(), ff.data()}, cs{nfC, cv.data(), cf.data()};
+    const long long nqp = (long long)nfF * nq;
+    std::vector<long long> owner((size_t)nqp);
+    std::vector<double> xim((size_t)3 * nqp);
+    CU(cudaStreamSynchronize(ctx->stream));
+    const sem_status ms = sem_face_match(ctx->device, &fs, &cs, Nf, 1e-3, owner.data(), xim.data(), nullptr);
+    if (ms == SEM_E_UNMATCHED) return fail(ctx, SEM_E_UNMATCHED, "orphan interface quadrature point (Algorithm 3)");
+    if (ms != SEM_OK) return fail(ctx, ms, "interface face matching failed");
+    std::vector<double> xf, wf, xc, wc;
+    gll_rule(Nf, xf, wf);
+    gll_rule(Nc, xc, wc);
+    const std::vector<double> Df = deriv_matrix(xf);
+    std::vector<long long> fbase((size_t)nqp), cbase((size_t)nqp);
+    std::vector<double> geo((size_t)7 * nqp), bas((size_t)6 * c1 * nqp);
+    for (int f = 0; f < nfF; ++f) {
+        const int ex = f % gF.nel[0], ey = f / gF.nel[0], ez = gF.nel[2] - 1;
+        for (int q = 0; q < nq; ++q) {
+            const long long i = (long long)f * nq + q;
+            const int a = q % q1, b = q / q1;
+            const double xi[3] = {xf[a], xf[b], 1.0};
+            double J[3][3];
+            trilinear_jacobian(&fv[(size_t)24 * f], xi, J);
+            // n+ |J_s| = J[:,0] x J[:,1] (outward: +zeta for a positive Jacobian)
+            double cr[3] = {J[1][0] * J[2][1] - J[2][0] * J[1][1], J[2][0] * J[0][1] - J[0][0] * J[2][1],
+                            J[0][0] * J[1][1] - J[1][0] * J[0][1]};
+            const double js = std::sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+            for (double& v : cr) v /= js;
+            double gp[3], gm[3];
+            solve3(J, cr, gp);
+            const long long oc = owner[(size_t)i];
+            const int cex = (int)(oc % gC.nel[0]), cey = (int)(oc / gC.nel[0]);
+            const double* xm = &xim[(size_t)3 * i];
+            double JC[3][3];
+            trilinear_jacobian(&cv[(size_t)24 * oc], xm, JC);
+            solve3(JC, cr, gm);
+            double* G = &geo[(size_t)7 * i];
+            G[0] = wf[a] * wf[b] * js;
+            for (int k = 0; k < 3; ++k) {
+                G[1 + k] = gp[k];
+                G[4 + k] = gm[k];
+            }
+            double* Bq = &bas[(size_t)6 * c1 * i];
+            for (int d = 0; d < 3; ++d) {
+                const std::vector<double> l = lagrange_at(xc, xm[d]), dl = lagrange_deriv_at(xc, xm[d]);
+                for (int k = 0; k <= Nc; ++k) {
+                    Bq[(2 * d) * c1 + k] = l[k];
+                    Bq[(2 * d + 1) * c1 + k] = dl[k];
+                }
+            }
+            fbase[(size_t)i] = ((long long)Nf * ez * F.NY + (long long)Nf * ey) * F.PX + (long long)Nf * ex;
+            cbase[(size_t)i] = ((long long)0 * C.NY + (long long)Nc * cey) * C.PX + (long long)Nc * cex;
+        }
+    }
+    sem::GIfaceParams& g = pt.itf.gprm;
+    g = sem::GIfaceParams{};
+    g.Nf = Nf;
+    g.Nc = Nc;
+    g.nqp = nqp;
+    g.resF = F.res;
+    g.resC = C.res;
+    g.PXf = F.PX;
+    g.NYf = F.NY;
+    g.PXc = C.PX;
+    g.NYc = C.NY;
+    long long *dfb = nullptr, *dcb = nullptr;
+    double *dgeo = nullptr, *dbas = nullptr;
+    if (upload(ctx, &dfb, fbase) || upload(ctx, &dcb, cbase) || upload(ctx, &dgeo, geo) || upload(ctx, &dbas, bas))
+        return SEM_E_CUDA;
+    g.fbase = dfb;
+    g.cbase = dcb;
+    g.geo = dgeo;
+    g.bas = dbas;
+    for (int i = 0; i <= Nf; ++i)
+        for (int j = 0; j <= Nf; ++j) g.Df[i][j] = Df[(size_t)i * q1 + j];
+    g.gamma = gamma;
+    g.cf2 = gF.c * gF.c;
+    g.cc2 = gC.c * gC.c;
+    pt.itf.general = true;
+    pt.itf.on = true;
+    pt.itf.fine = fb;
+    pt.itf.coarse = cb;
+    F.iface_side = +1;
+    C.iface_side = -1;
+    return SEM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -863,18 +1100,11 @@ sem_status sem_nccl_unique_id(void* out) {
 sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, const sem_pmut_desc* pm,
                          long long* slab_x0) {
     if (!boxes || n_boxes < 1 || n_boxes > 2 || world < 1) return SEM_E_ARG;
-    if (slabs_divisible(boxes, n_boxes, world)) return SEM_E_PARTITION;
-    if (n_boxes == 2 && boxes[0].bc[5] == SEM_BC_INTERFACE && boxes[1].bc[4] == SEM_BC_INTERFACE &&
-        !interface_aligned(boxes[0], boxes[1], world))
-        return SEM_E_PARTITION;
-    if (pm) {
-        if (pm->box < 0 || pm->box >= n_boxes || !pm->center) return SEM_E_ARG;
-        for (int k = 0; k < pm->n_pmut; ++k)
-            if (membrane_slab(boxes[pm->box], world, pm->center[2 * k + 1] - 0.5 * pm->side, pm->side) < 0)
-                return SEM_E_PARTITION;
-    }
+    if (pm && (pm->box < 0 || pm->box >= n_boxes || !pm->center)) return SEM_E_ARG;
+    std::vector<long long> cuts;
+    if (!auto_plan(boxes, n_boxes, world, pm, cuts)) return SEM_E_PARTITION;
     if (slab_x0)
-        for (int r = 0; r <= world; ++r) slab_x0[r] = (long long)(boxes[0].nel[1] / world) * r;
+        for (int r = 0; r <= world; ++r) slab_x0[r] = cuts[r];
     return SEM_OK;
 }
 
@@ -917,10 +1147,19 @@ sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
         ctx->gNY.push_back((long long)g.degree * g.nel[1] + 1);
         ctx->gNZ.push_back((long long)g.degree * g.nel[2] + 1);
     }
-    // slab decomposition along y: equal element counts per slab, the same slab boundaries for all
-    // boxes (box b's element count must be a multiple of the world size)
+    // slab decomposition along y: the caller's plan (sem_slab_plan) or equal slabs; the same slab
+    // boundaries (in y) for all boxes
     const int G = ctx->world;
-    if (const char* why = slabs_divisible(ctx->gdesc.data(), (int)ctx->gdesc.size(), G)) {
+    if (desc->slab_y0) {
+        ctx->cuts.assign(desc->slab_y0, desc->slab_y0 + G + 1);
+    } else {
+        if (ctx->gdesc[0].nel[1] % G) {
+            ctx->err = "nel_y must be divisible by the number of slabs (or pass slab_y0 from sem_slab_plan)";
+            return bail(SEM_E_PARTITION);
+        }
+        ctx->cuts = equal_plan(ctx->gdesc[0], G);
+    }
+    if (const char* why = plan_invalid(ctx->gdesc.data(), (int)ctx->gdesc.size(), ctx->cuts)) {
         ctx->err = why;
         return bail(SEM_E_PARTITION);
     }
@@ -932,8 +1171,8 @@ sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out) {
         pt.cutL = r > 0;
         pt.cutR = r < G - 1;
         for (auto& g : ctx->gdesc) {
-            const long long nloc = g.nel[1] / G;
-            pt.boxes.push_back(make_slab(g, nloc * r, nloc, pt.cutL, pt.cutR));
+            const long long e0 = cut_in_box(ctx->gdesc[0], g, ctx->cuts[r]), e1 = cut_in_box(ctx->gdesc[0], g, ctx->cuts[r + 1]);
+            pt.boxes.push_back(make_slab(g, e0, e1 - e0, pt.cutL, pt.cutR));
         }
         ctx->parts.push_back(pt);
     }
@@ -975,7 +1214,8 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
     if (pd->box < 0 || pd->box >= (int)ctx->gdesc.size()) return fail(ctx, SEM_E_ARG, "bad box");
     if (pd->face != 4) return fail(ctx, SEM_E_ARG, "PMUTs supported on the -z face only");
     for (auto& pt : ctx->parts)
-        if (pt.boxes[pd->box].curved) return fail(ctx, SEM_E_STATE, "PMUTs on a curved box are not supported");
+        if (pt.boxes[pd->box].verts_set)
+            return fail(ctx, SEM_E_STATE, "PMUTs on a curved (vertex-lattice) box are not supported");
     if (pd->n_pmut < 1 || pd->n_modes < 1 || pd->n_modes > sem::kMaxModes)
         return fail(ctx, SEM_E_ARG, "n_pmut >= 1 and 1 <= n_modes <= 8 required");
     if (!(pd->side > 0) || !pd->center || !pd->mode_mn || !pd->freq_hz || !pd->modal_mass || !pd->damping_ratio ||
@@ -997,7 +1237,7 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
         if (x0 < g.origin[0] - 1e-12 * a || y0 < g.origin[1] - 1e-12 * a ||
             x0 + a > g.origin[0] + g.extent[0] + 1e-12 * a || y0 + a > g.origin[1] + g.extent[1] + 1e-12 * a)
             return fail(ctx, SEM_E_ARG, "membrane off the face");
-        const int slab = membrane_slab(g, G, y0, a);
+        const int slab = membrane_slab(ctx->gdesc[0], ctx->cuts, y0, a);
         if (slab < 0) return fail(ctx, SEM_E_PARTITION, "a slab cut crosses a membrane");
         ctx->pm_lists[slab].push_back(k);
     }
@@ -1034,6 +1274,16 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
                     if (o >= 0) return fail(ctx, SEM_E_ARG, "membranes overlap");
                     o = l;
                 }
+            if (!b.solid_h.empty()) {   // obstacle box: a membrane is a fluid boundary, never under a solid element
+                const int N = b.N;
+                for (long long j : yi[l])
+                    for (long long i : xi[l])
+                        for (long long ey = std::max<long long>(0, (j - 1) / N); ey <= std::min<long long>(b.d.nel[1] - 1, j / N); ++ey)
+                            for (long long ex = std::max<long long>(0, (i - 1) / N); ex <= std::min<long long>(b.d.nel[0] - 1, i / N); ++ex)
+                                if (b.solid_h[(size_t)ex + (size_t)b.d.nel[0] * (size_t)ey] &&
+                                    i >= N * ex && i <= N * (ex + 1) && j >= N * ey && j <= N * (ey + 1))
+                                    return fail(ctx, SEM_E_ARG, "membrane on the face of an obstacle element");
+            }
         }
         std::vector<double> sx((size_t)KL * M * lmax, 0.0), sy((size_t)KL * M * lmax, 0.0), wx((size_t)KL * lmax, 0.0),
             wy((size_t)KL * lmax, 0.0), om2((size_t)KL * M), tzw((size_t)KL * M), im(M), et(M), dl(KL);
@@ -1102,9 +1352,6 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
     const int nb = (int)ctx->gdesc.size();
     if (fine_box < 0 || coarse_box < 0 || fine_box >= nb || coarse_box >= nb || fine_box == coarse_box)
         return fail(ctx, SEM_E_ARG, "bad box indices");
-    for (auto& pt : ctx->parts)
-        if (pt.boxes[fine_box].curved || pt.boxes[coarse_box].curved)
-            return fail(ctx, SEM_E_STATE, "the interface of a curved box is not supported");
     if (!(alpha > 0)) return fail(ctx, SEM_E_ARG, "penalty alpha must be > 0");
     const sem_box_desc& gF = ctx->gdesc[fine_box];
     const sem_box_desc& gC = ctx->gdesc[coarse_box];
@@ -1112,6 +1359,25 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
         return fail(ctx, SEM_E_ARG, "fine +z and coarse -z faces must be tagged SEM_BC_INTERFACE");
     const double hF[3] = {gF.extent[0] / gF.nel[0], gF.extent[1] / gF.nel[1], gF.extent[2] / gF.nel[2]};
     const double hC[3] = {gC.extent[0] / gC.nel[0], gC.extent[1] / gC.nel[1], gC.extent[2] / gC.nel[2]};
+    {
+        const bool cvF = ctx->parts[0].boxes[fine_box].curved, cvC = ctx->parts[0].boxes[coarse_box].curved;
+        if (cvF || cvC) {   // curved boxes: general non-conforming interface (Algorithm 3 matching)
+            if (!(cvF && cvC))
+                return fail(ctx, SEM_E_STATE, "an interface with a curved box needs both boxes curved (set vertices)");
+            if (ctx->world > 1 || ctx->parts.size() != 1)
+                return fail(ctx, SEM_E_PARTITION, "the curved-box interface is implemented for a single slab only");
+            if (quad_rule != 0) return fail(ctx, SEM_E_ARG, "the curved-box interface uses the GLL rule (quad_rule 0)");
+            const double cbar = 2.0 * gF.c * gC.c / (gF.c + gC.c);
+            const double hmin = std::min(std::min(std::min(hF[0], hF[1]), hF[2]), std::min(std::min(hC[0], hC[1]), hC[2]));
+            const int Nm = std::max(gF.degree, gC.degree);
+            st = build_general_interface(ctx, fine_box, coarse_box, alpha * cbar * cbar * Nm * Nm / hmin);
+            if (st) return st;
+            ctx->itf_on = true;
+            drop_graphs(ctx);
+            CU(cudaStreamSynchronize(ctx->stream));
+            return SEM_OK;
+        }
+    }
     const double tol = 1e-9 * std::max(hF[0], hC[0]);
     for (int k = 0; k < 2; ++k) {
         if (std::fabs(gF.origin[k] - gC.origin[k]) > tol || std::fabs(gF.extent[k] - gC.extent[k]) > tol)
@@ -1122,8 +1388,9 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
     if (gF.nel[0] % gC.nel[0] || gF.nel[1] % gC.nel[1] || gF.nel[0] / gC.nel[0] != gF.nel[1] / gC.nel[1])
         return fail(ctx, SEM_E_UNMATCHED, "fine lattice does not nest in the coarse one (need h_c = R h_f)");
     const int R = gF.nel[0] / gC.nel[0];
-    if (!interface_aligned(gF, gC, ctx->world))
-        return fail(ctx, SEM_E_PARTITION, "slab cut not aligned to the coarse elements");
+    for (size_t r = 1; r + 1 < ctx->cuts.size(); ++r)   // (sem_mesh_create checked every box; restated here)
+        if (cut_in_box(ctx->gdesc[0], gC, ctx->cuts[r]) < 0)
+            return fail(ctx, SEM_E_PARTITION, "slab cut not aligned to the coarse elements");
     std::vector<double> xf, wf, xc, wc;
     gll_rule(gF.degree, xf, wf);
     gll_rule(gC.degree, xc, wc);
@@ -1233,6 +1500,7 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
         pt.itf.fine = fine_box;
         pt.itf.coarse = coarse_box;
     }
+    sem::iface_prepare(gF.degree, gC.degree, R);
     ctx->itf_on = true;
     drop_graphs(ctx);
     CU(cudaStreamSynchronize(ctx->stream));
@@ -1327,15 +1595,16 @@ sem_status scatter_box_check(sem_ctx* ctx, int box, const void* data, const char
     if (ctx->world > 1 || ctx->parts.size() != 1)
         return fail(ctx, SEM_E_PARTITION, "curved / obstacle boxes are implemented for a single slab (world 1) only");
     sem::Part& pt = ctx->parts[0];
-    if ((pt.pm.on && pt.pm.box == box) || pt.boxes[box].iface_side != 0 || (pt.pml.on && pt.pml.box == box) ||
-        (ctx->pw.on && ctx->pw.box == box))
-        return fail(ctx, SEM_E_STATE, "curved / obstacle boxes carry no PMUT / interface / PML / plane wave");
+    if (pt.boxes[box].iface_side != 0 || (pt.pml.on && pt.pml.box == box) || (ctx->pw.on && ctx->pw.box == box))
+        return fail(ctx, SEM_E_STATE, "curved / obstacle boxes carry no interface / PML / plane wave");
     return SEM_OK;
 }
 
 sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size_t n_verts) {
     sem_status st = scatter_box_check(ctx, box, verts, "vertices");
     if (st) return st;
+    if (ctx->parts[0].pm.on && ctx->parts[0].pm.box == box)
+        return fail(ctx, SEM_E_STATE, "PMUTs on a curved (vertex-lattice) box are not supported");
     Box& b = ctx->parts[0].boxes[box];
     const sem_box_desc& g = ctx->gdesc[box];
     if (b.verts_set) return fail(ctx, SEM_E_STATE, "vertices already set");
@@ -1352,6 +1621,8 @@ sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size
 sem_status sem_box_set_obstacle(sem_ctx* ctx, int box, const unsigned char* solid, size_t n_el) {
     sem_status st = scatter_box_check(ctx, box, solid, "solid mask");
     if (st) return st;
+    if (ctx->parts[0].pm.on && ctx->parts[0].pm.box == box)
+        return fail(ctx, SEM_E_STATE, "set the obstacle before attaching the PMUTs of its box");
     Box& b = ctx->parts[0].boxes[box];
     const sem_box_desc& g = ctx->gdesc[box];
     if ((long long)n_el != (long long)g.nel[0] * g.nel[1] * g.nel[2])

@@ -238,6 +238,31 @@ struct CurvedParams {
     double D[kMaxN + 1][kMaxN + 1];  // D[i][j] = l_j'(x_i)
     double x[kMaxN + 1], w[kMaxN + 1];
     double c2, dt;
+    // PMUT forcing on the z = 0 face of an affine element-scatter (obstacle) box: the update subtracts
+    // F m_x m_y (F = kappa sum_m qdd S, face weights m_x m_y) from the residual of the face nodes
+    const double* __restrict__ F;    // [NY][NX] or nullptr
+    const double* __restrict__ fmx;  // [NX] face mass factors
+    const double* __restrict__ fmy;  // [NY]
+};
+
+// General non-conforming SIPG interface between two element-scatter boxes (curved vertex lattices):
+// per fine-face quadrature point (the fine face's GLL nodes, reading R9) the owner coarse element and
+// x_hat^- come from Algorithm 3 (sem_face_match) at setup; the kernel adds the face terms of Eq. 7 into
+// both boxes' assembled residuals (atomics).
+struct GIfaceParams {
+    int Nf, Nc;
+    long long nqp;                          // quadrature points (fine faces x (Nf+1)^2)
+    const double* __restrict__ Pf;          // p^{n+1} of the fine / coarse box (pitched)
+    const double* __restrict__ Pc;
+    double* resF;                           // assembled residuals (K p), consumed by the curved update
+    double* resC;
+    long long PXf, NYf, PXc, NYc;           // node (ix, iy, iz) at (iz NY + iy) PX + ix
+    const long long* __restrict__ fbase;    // [nqp] pitched index of the fine element's node (0,0,0)
+    const long long* __restrict__ cbase;    // [nqp] same for the owner coarse element
+    const double* __restrict__ geo;         // [nqp][7]: W_q = w_a w_b |J_s|, J_F^-1 n+, J_C(x_hat^-)^-1 n+
+    const double* __restrict__ bas;         // [nqp][6][Nc+1]: l, l' of the coarse basis at x_hat^- per axis
+    double Df[kMaxN + 1][kMaxN + 1];        // fine GLL differentiation matrix D[i][j] = l_j'(x_i)
+    double gamma, cf2, cc2;
 };
 
 // One side of one slab cut for one box (partial rows before, fix-up after the exchange).
@@ -327,6 +352,8 @@ struct Iface {
     bool on = false;
     int fine = 0, coarse = 1;
     IfaceParams prm{};
+    bool general = false;          // curved boxes: table-driven kernel on Algorithm 3's matching
+    GIfaceParams gprm{};
     std::vector<void*> allocs;
 };
 
@@ -370,6 +397,7 @@ struct sem_ctx {
     std::vector<sem_box_desc> gdesc;               // global boxes as given
     std::vector<long long> gNX, gNY, gNZ;          // global lattice sizes
     std::vector<sem::Part> parts;
+    std::vector<long long> cuts;                   // slab plan: box-0 element y index of each slab start [world+1]
     int n_pmut = 0, n_modes = 0;                   // global PMUT array
     std::vector<std::vector<int>> pm_lists;        // global PMUT indices per slab
     bool itf_on = false;
@@ -403,13 +431,15 @@ void launch_volume(VolLaunch L, cudaStream_t s);
 bool volume_pair_supported(int N0, int N1);
 void volume_pair_prepare(int N0, int N1);
 void launch_modal(const ModalParams& p, cudaStream_t s);
-void launch_iface(const IfaceParams& p, cudaStream_t s);
+int launch_iface(const IfaceParams& p, cudaStream_t s);   // returns the number of kernel launches
+void iface_prepare(int Nf, int Nc, int R);
 void launch_fill_random(double* p, double* w, double* pn, long long NX, long long PX, long long NY, long long NZ,
                         long long gy0, long long NYg, unsigned long long seed, int box, double ps, double vs,
                         double dt, cudaStream_t s);
 void launch_cut_partial(const CutBatch& B, cudaStream_t s);
 void launch_pml_elements(const PmlParams& p, cudaStream_t s);
 void launch_curved(const CurvedParams& p, cudaStream_t s);
+void launch_iface_general(const GIfaceParams& p, cudaStream_t s);
 int curved_grid(int N, int nel);   // resident blocks of the curved residual kernel on this device
 void launch_step_bump(long long* step, cudaStream_t s);
 void launch_pml_fixup(const PmlParams& p, cudaStream_t s);

@@ -43,7 +43,8 @@ class MeshDesc(C.Structure):
     _fields_ = [("n_boxes", C.c_int), ("boxes", C.POINTER(BoxDesc)), ("dt", C.c_double),
                 ("device", C.c_int), ("stream", C.c_void_p), ("rank", C.c_int), ("world", C.c_int),
                 ("nccl_unique_id", C.c_void_p), ("flags", C.c_int),
-                ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_user", C.c_void_p)]
+                ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_user", C.c_void_p),
+                ("slab_y0", C.POINTER(C.c_longlong))]
 
 
 def torch_allocator(device=0):
@@ -161,13 +162,17 @@ def sem_slab_plan(boxes, world, pm=None):
 
 
 def sem_mesh_create(boxes, dt, device=0, stream=None, rank=0, world=1, nccl_unique_id=None, flags=0,
-                    allocator=None):
-    """allocator: optional (dev_alloc, dev_free) pair of ctypes callbacks (see torch_allocator)."""
+                    allocator=None, slab_y0=None):
+    """allocator: optional (dev_alloc, dev_free) pair of ctypes callbacks (see torch_allocator);
+    slab_y0: optional slab plan [world + 1] (sem_slab_plan)."""
     arr = _box_array(boxes)
     d = MeshDesc(len(boxes), arr, float(dt), int(device), C.c_void_p(stream) if stream else None, int(rank),
                  int(world), C.cast(C.c_char_p(nccl_unique_id), C.c_void_p) if nccl_unique_id else None, int(flags))
     if allocator is not None:
         d.dev_alloc, d.dev_free = allocator
+    if slab_y0 is not None:
+        plan = (C.c_longlong * len(slab_y0))(*[int(v) for v in slab_y0])
+        d.slab_y0 = C.cast(plan, C.POINTER(C.c_longlong))
     out = C.c_void_p()
     st = LIB.sem_mesh_create(C.byref(d), C.byref(out))
     if st != 0:
@@ -336,14 +341,16 @@ class Simulation:
     """One context built from a ``sem_inputs`` workload record (boxes, PMUTs, interface, source)."""
 
     def __init__(self, rec, device=0, stream=None, flags=0, rank=0, world=1, nccl_unique_id=None,
-                 torch_memory=False):
+                 torch_memory=False, slab_y0=None):
         self.rec = rec
         if rec.get("coupling", "predicted") == "literal":
             flags |= SEM_F_COUPLING_LITERAL
         # torch_memory: the context's device arrays come from torch's caching allocator
         self._allocator = torch_allocator(device) if torch_memory else None
+        if slab_y0 is None and world > 1:   # equal slabs when admissible, else the uneven plan
+            slab_y0 = sem_slab_plan(rec["boxes"], world, rec.get("pmut"))
         self.ctx = sem_mesh_create(rec["boxes"], rec["dt"], device, stream, rank, world, nccl_unique_id, flags,
-                                   self._allocator)
+                                   self._allocator, slab_y0)
         self.nn = [tuple(b["degree"] * n + 1 for n in b["nel"]) for b in rec["boxes"]]
         self.ndof = [a * b * c for a, b, c in self.nn]
         try:

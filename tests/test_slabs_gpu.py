@@ -114,3 +114,28 @@ def test_fullsize_cfg3_eight_slabs_crops():
         k = info["pmut_full_index"]
         assert rel_l2(q2[k[ok]], nm.q[ok]) < TOL
         assert rel_l2(qd2[k[ok]], nm.qd[ok]) < TOL
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_config1_uneven_membrane_preserving_slabs(world):
+    """Config 1 at 4 / 8 slabs: equal cuts would split membranes, so sem_slab_plan picks uneven cuts in
+    the membrane gaps; the emulated decomposition at full size vs the oracle."""
+    from paper_2603_06267_b200.sem import sem_slab_plan
+    rec = config(1)
+    plan = sem_slab_plan(rec["boxes"], world, rec["pmut"])
+    assert len(set(np.diff(plan))) > 1                    # really uneven
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        nm = oracle_run(rec, 200)
+    sim = _sim(rec, world, steps=200)
+    for k, v in compare(sim, nm).items():
+        assert v < TOL, (world, k, v)
+    sim.close()
+
+
+def test_config0_two_uneven_slabs():
+    rec = config(0)
+    nm = oracle_run(rec, rec["n_steps"])
+    sim = _sim(rec, 2, steps=rec["n_steps"])
+    for k, v in compare(sim, nm).items():
+        assert v < TOL, (k, v)
