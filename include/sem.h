@@ -120,10 +120,12 @@ sem_status sem_nccl_unique_id(void* out128);
  * in [0, n_cycles/f0] (reading R10) for t <= t_switch; (1/C) sum_m eta_m q_m after (Eq. 3).
  * Arrays: center [n_pmut*2] (x, y), mode_mn [n_modes*2], freq_hz [n_pmut*n_modes] (k-major),
  * modal_mass / damping_ratio / eta [n_modes], delay_s [n_pmut].  n_modes <= 8.
- * The box may be a structured box or an affine obstacle box (sem_box_set_obstacle, called first);
- * curved (vertex-lattice) boxes carry no PMUT (SEM_E_STATE).
+ * The box may be a structured box, an affine obstacle box (sem_box_set_obstacle, called first) or a
+ * curved box (sem_box_set_vertices, called first): there the coupling is tabulated per membrane node,
+ * B_{k,m,j} = sum_F w_a w_b |J_s| S_{k,m}(x_j) with the trilinear face's |J_s| and physical node
+ * positions (not separable), and the force enters the box's assembled residual.
  * Errors: SEM_E_ARG (membranes overlapping or off the face, zero-node membrane, membrane on a solid
- * element's face, rx with C <= 0), SEM_E_STATE (already attached, curved box). */
+ * element's face, rx with C <= 0), SEM_E_STATE (already attached). */
 typedef struct {
     int box, face;
     int n_pmut, n_modes;
@@ -178,9 +180,9 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
  * metric terms w_q c^2 |J| J^-1 J^-T recomputed from the 8 vertices at every GLL point (nothing
  * stored per quadrature point), FP64 atomics into an assembled residual, and a nodal kick-drift with
  * the assembled lumped mass and ABC diagonal (computed here on the host).  Call right after
- * sem_mesh_create: curved boxes carry no PMUT / PML / plane wave (SEM_E_STATE); an interface between
- * two curved boxes is the general one of sem_dg_interface_build (call that afterwards); world 1 only
- * (SEM_E_PARTITION).  Caller owns `verts` (copied).  Errors: SEM_E_ARG (size, non-positive
+ * sem_mesh_create: curved boxes carry no PML / plane wave (SEM_E_STATE); PMUTs (tabulated coupling) and
+ * an interface between two curved boxes (the general one of sem_dg_interface_build) are attached
+ * afterwards; world 1 only (SEM_E_PARTITION).  Caller owns `verts` (copied).  Errors: SEM_E_ARG (size, non-positive
  * Jacobian at a GLL point), SEM_E_STATE, SEM_E_OOM. */
 sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size_t n_verts);
 

@@ -54,8 +54,30 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the phase completes (or the
+// hint elapses) instead of re-issuing the test (SEM_WAIT_HINT = 0: plain polling)
+#ifndef SEM_XSPLIT
+#define SEM_XSPLIT 0
+#endif
+#ifndef SEM_WAIT_HINT
+#define SEM_WAIT_HINT 0
+#endif
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"((uint32_t)SEM_WAIT_HINT)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
+    if (SEM_WAIT_HINT) {
+        while (!mbar_try_wait_hint(bar, parity)) {
+        }
+    } else {
+        while (!mbar_try_wait(bar, parity)) {
+        }
     }
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint32_t bar) {
@@ -165,12 +187,27 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
     double v[N + 1];
 #pragma unroll
     for (int b = 0; b <= N; ++b) v[b] = sP[t.xb + b];
+#if SEM_XSPLIT   // two accumulation chains per x row (shorter dependent DFMA chains)
+    double xr0 = 0.0, xr1 = 0.0, xl0 = 0.0, xl1 = 0.0;
+#pragma unroll
+    for (int b = 0; b <= N; b += 2) {
+        xr0 = fma(t.cR[b], v[b], xr0);
+        xl0 = fma(RT.L[b], v[b], xl0);
+    }
+#pragma unroll
+    for (int b = 1; b <= N; b += 2) {
+        xr1 = fma(t.cR[b], v[b], xr1);
+        xl1 = fma(RT.L[b], v[b], xl1);
+    }
+    const double xr = xr0 + xr1, xl = xl0 + xl1;
+#else
     double xr = 0.0, xl = 0.0;
 #pragma unroll
     for (int b = 0; b <= N; ++b) {
         xr = fma(t.cR[b], v[b], xr);
         xl = fma(RT.L[b], v[b], xl);
     }
+#endif
     const double xlr = __shfl_sync(0xffffffffu, xl, (threadIdx.x + 31) & 31);
     // ---- y: per-warp row (registers, scaled); left row of a shared node: row L
     double y0 = 0.0, y1 = 0.0;
@@ -657,10 +694,58 @@ __device__ __forceinline__ double drive_tx(const ModalParams& p, double tp) {
     return p.amp * sin(p.om0 * tp) * 0.5 * (1.0 - cos(p.om0 * tp / p.ncyc));
 }
 
+// One block of kModalWarps warps per PMUT (see modal_kernel).
+constexpr int kModalWarps = 4;
+
+// Modal ODE of PMUT k (warp 0, lane m = mode m): predictor / solve / corrector with the
+// projection G_m = sum over the block's partial sums red[w][m]; q'' of every mode into qv_s.
+__device__ __forceinline__ void modal_ode(const ModalParams& p, int k, const double (*red)[kMaxModes], double* qv_s,
+                                          int lane) {
+    const unsigned FULL = 0xffffffffu;
+    const int M = p.n_modes;
+    const double dt = p.dt;
+    {
+        const long long n = __ldcg(p.step);
+        const double t1 = (double)(n + 1) * dt, t0 = (double)n * dt;
+        double G = 0.0;
+        if (lane < kMaxModes)
+#pragma unroll
+            for (int w = 0; w < kModalWarps; ++w) G += red[w][lane];
+        const bool act = lane < M;
+        const size_t km = (size_t)k * M + lane;
+        double q = 0, qd = 0, qdd = 0;
+        if (act) { q = p.q[km]; qd = p.qd[km]; qdd = p.qdd[km]; }
+        const double q1 = q + dt * qd + 0.5 * dt * dt * qdd;   // P:L615
+        double qd1 = qd + 0.5 * dt * qdd;                       // P:L617
+        const double etam = act ? p.eta[lane] : 0.0;
+        // phi at the coupling time level (R2): predicted -> (t^{n+1}, q^{n+1}); literal -> (t^n, q^n)
+        const double tu = p.literal ? t0 : t1;
+        double s = etam * (p.literal ? q : q1);
+        double s1 = etam * q1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s += __shfl_xor_sync(FULL, s, o);
+            s1 += __shfl_xor_sync(FULL, s1, o);
+        }
+        const double tp_delay = p.delay[k];
+        const double phi = (p.rx && tu > p.t_switch) ? s * p.invC : drive_tx(p, tu - tp_delay);
+        const double phi1 = (p.rx && t1 > p.t_switch) ? s1 * p.invC : drive_tx(p, t1 - tp_delay);
+        double qdd1 = 0.0;
+        if (act) {
+            qdd1 = -p.omega2[km] * q1 - p.twozw[km] * qd1 + (-G + etam * phi) * p.invmass[lane];  // P:L619
+            qd1 = qd1 + 0.5 * dt * qdd1;                                                           // P:L621
+            p.q[km] = q1;
+            p.qd[km] = qd1;
+            p.qdd[km] = qdd1;
+        }
+        if (lane == 0) p.phi[k] = phi1;
+        if (lane < kMaxModes) qv_s[lane] = qdd1;
+    }
+}
+
 // One block of kModalWarps warps per PMUT: the warps share the membrane's rows (projection and force
 // plane), warp 0 advances the modes.  (One warp per PMUT left the grid at < 1 block per SM for the
 // 512 PMUTs of a cfg-3 slab: latency-bound.)
-constexpr int kModalWarps = 4;
 
 __global__ void __launch_bounds__(32 * kModalWarps) modal_kernel(const __grid_constant__ ModalParams p) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -705,43 +790,7 @@ __global__ void __launch_bounds__(32 * kModalWarps) modal_kernel(const __grid_co
         for (int m = 0; m < kMaxModes; ++m) red[warp][m] = acc[m];
     __syncthreads();
 
-    if (warp == 0) {   // modal predictor / solve / corrector (lane m = mode m)
-        const long long n = __ldcg(p.step);
-        const double t1 = (double)(n + 1) * dt, t0 = (double)n * dt;
-        double G = 0.0;
-        if (lane < kMaxModes)
-#pragma unroll
-            for (int w = 0; w < kModalWarps; ++w) G += red[w][lane];
-        const bool act = lane < M;
-        const size_t km = (size_t)k * M + lane;
-        double q = 0, qd = 0, qdd = 0;
-        if (act) { q = p.q[km]; qd = p.qd[km]; qdd = p.qdd[km]; }
-        const double q1 = q + dt * qd + 0.5 * dt * dt * qdd;   // P:L615
-        double qd1 = qd + 0.5 * dt * qdd;                       // P:L617
-        const double etam = act ? p.eta[lane] : 0.0;
-        // phi at the coupling time level (R2): predicted -> (t^{n+1}, q^{n+1}); literal -> (t^n, q^n)
-        const double tu = p.literal ? t0 : t1;
-        double s = etam * (p.literal ? q : q1);
-        double s1 = etam * q1;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            s += __shfl_xor_sync(FULL, s, o);
-            s1 += __shfl_xor_sync(FULL, s1, o);
-        }
-        const double tp_delay = p.delay[k];
-        const double phi = (p.rx && tu > p.t_switch) ? s * p.invC : drive_tx(p, tu - tp_delay);
-        const double phi1 = (p.rx && t1 > p.t_switch) ? s1 * p.invC : drive_tx(p, t1 - tp_delay);
-        double qdd1 = 0.0;
-        if (act) {
-            qdd1 = -p.omega2[km] * q1 - p.twozw[km] * qd1 + (-G + etam * phi) * p.invmass[lane];  // P:L619
-            qd1 = qd1 + 0.5 * dt * qdd1;                                                           // P:L621
-            p.q[km] = q1;
-            p.qd[km] = qd1;
-            p.qdd[km] = qdd1;
-        }
-        if (lane == 0) p.phi[k] = phi1;
-        if (lane < kMaxModes) qv_s[lane] = qdd1;
-    }
+    if (warp == 0) modal_ode(p, k, red, qv_s, lane);
     __syncthreads();
     double qv[kMaxModes];
 #pragma unroll
@@ -762,8 +811,48 @@ __global__ void __launch_bounds__(32 * kModalWarps) modal_kernel(const __grid_co
     }
 }
 
+// Tabulated coupling (curved boxes): one block per PMUT over its face-node list; projection
+// G_m = sum_j B[j][m] p_j (Eq. 12), the same modal ODE, then r_j -= kappa sum_m qdd_m B[j][m] (Eq. 11)
+// into the box's assembled residual (membranes are disjoint: no two blocks touch a node).
+__global__ void __launch_bounds__(32 * kModalWarps) modal_table_kernel(const __grid_constant__ ModalParams p) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k = blockIdx.x, M = p.n_modes;
+    const int j0 = p.toff[k], j1 = p.toff[k + 1];
+    __shared__ double red[kModalWarps][kMaxModes];
+    __shared__ double qv_s[kMaxModes];
+    double acc[kMaxModes];
+#pragma unroll
+    for (int m = 0; m < kMaxModes; ++m) acc[m] = 0.0;
+    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+        const double v = p.P[p.tidx[j]];
+#pragma unroll
+        for (int m = 0; m < kMaxModes; ++m)
+            if (m < M) acc[m] = fma(p.tB[(long long)j * M + m], v, acc[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < kMaxModes; ++m) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[m] += __shfl_xor_sync(0xffffffffu, acc[m], o);
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int m = 0; m < kMaxModes; ++m) red[warp][m] = acc[m];
+    __syncthreads();
+    if (warp == 0) modal_ode(p, k, red, qv_s, lane);
+    __syncthreads();
+    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+        double f = 0.0;
+#pragma unroll
+        for (int m = 0; m < kMaxModes; ++m)
+            if (m < M) f = fma(qv_s[m], p.tB[(long long)j * M + m], f);
+        atomicAdd(p.res + p.tidx[j], -p.kappa * f);   // (other kernels may add to the residual concurrently)
+    }
+}
+
 void launch_modal(const ModalParams& p, cudaStream_t s) {
-    if (p.n_pmut > 0) modal_kernel<<<p.n_pmut, 32 * kModalWarps, 0, s>>>(p);
+    if (p.n_pmut <= 0) return;
+    if (p.toff) modal_table_kernel<<<p.n_pmut, 32 * kModalWarps, 0, s>>>(p);
+    else modal_kernel<<<p.n_pmut, 32 * kModalWarps, 0, s>>>(p);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1355,6 +1444,8 @@ __global__ void cut_partial_kernel(const __grid_constant__ CutBatch B) {
         double s = 0.0;
         for (int b = 0; b <= c.N; ++b) s = fma(c.row[b], col[(long long)b * c.PX], s);
         c.out[i] = s;
+        if (c.pda)   // PML acceleration of this slab's elements at the cut node
+            c.out[n + 2 * c.NXt + i] = c.pda[(iz * c.NY + (c.side ? c.NY - 1 : 0)) * c.PX + ix];
     } else if (i < n + c.NXt) {   // coarse SIPG partial sums at the cut row of the face lattice
         const long long jx = i - n;
         const long long jy = c.side ? c.NYt - 1 : 0;
@@ -1372,6 +1463,7 @@ __global__ void cut_fixup_kernel(const __grid_constant__ CutBatch B) {
     double da = -c.in[i];
     if (c.NXt > 0 && iz <= c.N)   // coarse-side SIPG layer terms of the neighbour's fine points
         da -= c.in[n + ix] * c.ktau[iz] + c.in[n + c.NXt + ix] * c.ksig[iz];
+    if (c.pda) da += c.in[n + 2 * c.NXt + i];   // the neighbour's PML acceleration
     const long long d = (iz * c.NY + (c.side ? c.NY - 1 : 0)) * c.PX + ix;
     const double dw = c.dt * da;
     c.W[d] += dw;
@@ -1445,7 +1537,10 @@ __global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1), pm
     // per-axis tables
     const double pv = p.P[g];
     const double so = p.psi_old[g];
-    const bool own = (a < N || ex == p.nelx - 1) && (b < N || ey == p.nely - 1) && (c < N || ez == p.nelz - 1);
+    // (a y-slab with a lower cut leaves its cut-plane nodes' nodal terms to the slab below, whose last
+    //  element owns them: the exchanged PML accelerations then count them once)
+    const bool own = (a < N || ex == p.nelx - 1) && (b < N || ey == p.nely - 1) && (c < N || ez == p.nelz - 1) &&
+                     !(p.cutL && gy == 0);
     const double wv = own ? p.W[g] : 0.0;
     double* ph = p.phi + (size_t)k * 3 * nl;
     const double phold[3] = {ph[t], ph[nl + t], ph[2 * nl + t]};
@@ -1537,8 +1632,35 @@ void launch_pml_elements(const PmlParams& p, cudaStream_t s) {
     }
 }
 
+// Row-segment sweep of the PML region (one warp per segment, coalesced): w += dt da, p += dt^2 da,
+// da = 0.  Each region node lies in exactly one segment, so no atomics are needed.
+__global__ void __launch_bounds__(256) pml_fixup_rows_kernel(const __grid_constant__ PmlParams p) {
+    const int lane = threadIdx.x & 31;
+    const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long sg = wid; sg < p.n_seg; sg += nw) {
+        const long long g0 = p.seg_start[sg];
+        const int len = p.seg_len[sg];
+        for (int i = lane; i < len; i += 32) {
+            const long long g = g0 + i;
+            const double v = p.da[g];
+            if (v != 0.0) {
+                const double dw = p.dt * v;
+                p.Wn[g] += dw;
+                p.Pn[g] = fma(p.dt, dw, p.Pn[g]);
+                p.da[g] = 0.0;
+            }
+        }
+    }
+}
+
 void launch_pml_fixup(const PmlParams& p, cudaStream_t s) {
     if (p.n_el <= 0) return;
+    if (p.n_seg > 0) {
+        const long long warps = p.n_seg < 148LL * 64 ? p.n_seg : 148LL * 64;
+        pml_fixup_rows_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(p);
+        return;
+    }
     switch (p.N) {
 #define SEM_PML_CASE(n) case n: pml_fixup_kernel<n><<<(p.n_el + pml_epb<n>() - 1) / pml_epb<n>(), pml_epb<n>() * (n + 1) * (n + 1) * (n + 1), 0, s>>>(p); break;
         SEM_PML_CASE(1) SEM_PML_CASE(2) SEM_PML_CASE(3) SEM_PML_CASE(4)

@@ -535,6 +535,12 @@ sem::ModalParams modal_params(sem_ctx* ctx, sem::Part& pt, int cur) {
     p.phi = pm.phi;
     p.F = pm.F;
     p.step = ctx->d_step;
+    if (pm.toff) {
+        p.toff = pm.toff;
+        p.tidx = pm.tidx;
+        p.tB = pm.tB;
+        p.res = b.res;
+    }
     return p;
 }
 
@@ -564,6 +570,7 @@ sem::CutParams cut_params(sem_ctx* ctx, sem::Part& pt, int side, int bi, int cur
             c.ksig[k] = b.tab.ksig[k];
         }
     }
+    if (pt.pml.on && pt.pml.box == bi) c.pda = pt.pml.da;
     c.out = pt.send[side] + pt.xoff[bi];
     c.in = pt.recv[side] + pt.xoff[bi];
     return c;
@@ -599,7 +606,7 @@ sem::CurvedParams curved_params(sem_ctx* ctx, sem::Part& pt, int bi, int cur) {
     }
     p.c2 = b.d.c * b.d.c;
     p.dt = ctx->dt;
-    if (pt.pm.on && pt.pm.box == bi) {
+    if (pt.pm.on && pt.pm.box == bi && !pt.pm.toff) {   // affine obstacle box: separable coupling
         p.F = pt.pm.F;
         p.fmx = b.mx;
         p.fmy = b.my;
@@ -648,6 +655,10 @@ sem::PmlParams pml_params(sem_ctx* ctx, sem::Part& pt, int cur) {
     p.jac = 0.125 * b.h[0] * b.h[1] * b.h[2];
     p.c2 = b.d.c * b.d.c;
     p.dt = ctx->dt;
+    p.cutL = b.cutL ? 1 : 0;
+    p.seg_start = m.seg_start;
+    p.seg_len = m.seg_len;
+    p.n_seg = m.n_seg;
     return p;
 }
 
@@ -896,6 +907,25 @@ cudaError_t copy_slab(double* host, double* dev, const Box& b, long long NYg, lo
     return cudaMemcpy3DAsync(&m, s);
 }
 
+// exchange buffers: per box one NX x NZ cut plane + 2 NX for the coarse SIPG row (sized always) + one
+// NX x NZ plane of PML acceleration for the PML box (after sem_pml_attach)
+sem_status setup_exchange(sem_ctx* ctx, sem::Part& pt) {
+    pt.xoff.clear();
+    long long off = 0;
+    for (int bi = 0; bi < (int)pt.boxes.size(); ++bi) {
+        const Box& b = pt.boxes[bi];
+        pt.xoff.push_back(off);
+        off += b.NX * b.NZ + 2 * b.NX + ((pt.pml.on && pt.pml.box == bi) ? b.NX * b.NZ : 0);
+    }
+    pt.xcount = off;
+    for (int s = 0; s < 2; ++s) {   // (buffers of an earlier layout stay allocated until sem_destroy)
+        if (dalloc(ctx, &pt.send[s], (size_t)off) || dalloc(ctx, &pt.recv[s], (size_t)off)) return SEM_E_OOM;
+        CU(cudaMemsetAsync(pt.send[s], 0, (size_t)off * 8, ctx->stream));
+        CU(cudaMemsetAsync(pt.recv[s], 0, (size_t)off * 8, ctx->stream));
+    }
+    return SEM_OK;
+}
+
 sem_status setup_part_buffers(sem_ctx* ctx, sem::Part& pt) {
     for (auto& b : pt.boxes) {
         const size_t n = (size_t)b.nalloc();
@@ -914,20 +944,7 @@ sem_status setup_part_buffers(sem_ctx* ctx, sem::Part& pt) {
             !make_map(&b.tmW, b.W, b, sem::vol_wbox_w(b.N), TY))
             return fail(ctx, SEM_E_CUDA, "cuTensorMapEncodeTiled failed");
     }
-    // exchange buffers: per box one NX x NZ cut plane (+ 2 NX for the coarse SIPG row, sized always)
-    pt.xoff.clear();
-    long long off = 0;
-    for (auto& b : pt.boxes) {
-        pt.xoff.push_back(off);
-        off += b.NX * b.NZ + 2 * b.NX;
-    }
-    pt.xcount = off;
-    for (int s = 0; s < 2; ++s) {
-        if (dalloc(ctx, &pt.send[s], (size_t)off) || dalloc(ctx, &pt.recv[s], (size_t)off)) return SEM_E_OOM;
-        CU(cudaMemsetAsync(pt.send[s], 0, (size_t)off * 8, ctx->stream));
-        CU(cudaMemsetAsync(pt.recv[s], 0, (size_t)off * 8, ctx->stream));
-    }
-    return SEM_OK;
+    return setup_exchange(ctx, pt);
 }
 
 // host trilinear map of an element: J[i][j] = dX_i / dxi_j at xi (vertex v = i + 2j + 4k at reference
@@ -1083,6 +1100,74 @@ sem_status build_general_interface(sem_ctx* ctx, int fb, int cb, double gamma) {
     return SEM_OK;
 }
 
+// Coupling table of a curved box (reading R4, Eqs. 11-12): B_{k,m,j} = sum over the -z faces of the
+// face quadrature weight w_a w_b |J_s| (J_s of the trilinear map at zeta = -1) times S_{k,m} at the
+// node's physical position (reading R19), for every face node of every PMUT with some S != 0.
+sem_status pmut_tables(sem_ctx* ctx, sem::Part& pt, Box& b, const sem_pmut_desc& pd, const std::vector<int>& ks) {
+    const sem_box_desc& g = b.d;
+    const int N = b.N, M = pd.n_modes, KL = (int)ks.size();
+    std::vector<double> x, w;
+    gll_rule(N, x, w);
+    const long long nx = g.nel[0] + 1, ny = g.nel[1] + 1;
+    // assembled face weight and position of every z = 0 lattice node
+    std::vector<double> fw((size_t)b.NX * b.NY, 0.0), fx((size_t)b.NX * b.NY), fy((size_t)b.NX * b.NY);
+    for (int ey = 0; ey < g.nel[1]; ++ey)
+        for (int ex = 0; ex < g.nel[0]; ++ex) {
+            double V[24];
+            for (int v = 0; v < 8; ++v) {
+                const long long vx = ex + (v & 1), vy = ey + ((v >> 1) & 1), vz = (v >> 2);
+                for (int i = 0; i < 3; ++i) V[3 * v + i] = b.vlat_h[3 * (vx + nx * (vy + ny * vz)) + i];
+            }
+            for (int bb = 0; bb <= N; ++bb)
+                for (int a = 0; a <= N; ++a) {
+                    const double xi[3] = {x[a], x[bb], -1.0};
+                    double J[3][3];
+                    trilinear_jacobian(V, xi, J);
+                    const double cx = J[1][0] * J[2][1] - J[2][0] * J[1][1], cy = J[2][0] * J[0][1] - J[0][0] * J[2][1],
+                                 cz = J[0][0] * J[1][1] - J[1][0] * J[0][1];
+                    double X[3] = {0, 0, 0};
+                    for (int v = 0; v < 8; ++v) {
+                        const double sh = 0.125 * (1.0 + ((v & 1) ? 1 : -1) * xi[0]) * (1.0 + ((v & 2) ? 1 : -1) * xi[1]) *
+                                          (1.0 + ((v & 4) ? 1 : -1) * xi[2]);
+                        for (int i = 0; i < 3; ++i) X[i] += sh * V[3 * v + i];
+                    }
+                    const size_t j = (size_t)(N * ey + bb) * b.NX + (N * ex + a);
+                    fw[j] += w[a] * w[bb] * std::sqrt(cx * cx + cy * cy + cz * cz);
+                    fx[j] = X[0];
+                    fy[j] = X[1];
+                }
+        }
+    std::vector<int> off(KL + 1, 0);
+    std::vector<long long> idx;
+    std::vector<double> B;
+    std::vector<int> used((size_t)b.NX * b.NY, -1);
+    const double a = pd.side;
+    for (int l = 0; l < KL; ++l) {
+        const int k = ks[l];
+        const double x0 = pd.center[2 * k] - 0.5 * a, y0 = pd.center[2 * k + 1] - 0.5 * a;
+        for (size_t j = 0; j < fw.size(); ++j) {
+            const double xl = fx[j] - x0, yl = fy[j] - y0;
+            if (!(xl >= 0 && xl <= a && yl >= 0 && yl <= a)) continue;
+            std::vector<double> row(M);
+            bool nz = false;
+            for (int m = 0; m < M; ++m) {
+                const double S = std::sin(pd.mode_mn[2 * m] * M_PI * xl / a) * std::sin(pd.mode_mn[2 * m + 1] * M_PI * yl / a);
+                row[m] = fw[j] * S;
+                nz = nz || S != 0.0;
+            }
+            if (!nz) continue;
+            if (used[j] >= 0) return fail(ctx, SEM_E_ARG, "membranes overlap");
+            used[j] = l;
+            idx.push_back((long long)(j / b.NX) * b.PX + (long long)(j % b.NX));   // pitched, plane z = 0
+            B.insert(B.end(), row.begin(), row.end());
+        }
+        off[l + 1] = (int)idx.size();
+        if (off[l + 1] == off[l]) return fail(ctx, SEM_E_ARG, "membrane with no face node");
+    }
+    if (upload(ctx, &pt.pm.toff, off) || upload(ctx, &pt.pm.tidx, idx) || upload(ctx, &pt.pm.tB, B)) return SEM_E_CUDA;
+    return SEM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1213,9 +1298,7 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
     if (ctx->n_pmut) return fail(ctx, SEM_E_STATE, "PMUT array already attached");
     if (pd->box < 0 || pd->box >= (int)ctx->gdesc.size()) return fail(ctx, SEM_E_ARG, "bad box");
     if (pd->face != 4) return fail(ctx, SEM_E_ARG, "PMUTs supported on the -z face only");
-    for (auto& pt : ctx->parts)
-        if (pt.boxes[pd->box].verts_set)
-            return fail(ctx, SEM_E_STATE, "PMUTs on a curved (vertex-lattice) box are not supported");
+
     if (pd->n_pmut < 1 || pd->n_modes < 1 || pd->n_modes > sem::kMaxModes)
         return fail(ctx, SEM_E_ARG, "n_pmut >= 1 and 1 <= n_modes <= 8 required");
     if (!(pd->side > 0) || !pd->center || !pd->mode_mn || !pd->freq_hz || !pd->modal_mass || !pd->damping_ratio ||
@@ -1284,6 +1367,10 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
                                     i >= N * ex && i <= N * (ex + 1) && j >= N * ey && j <= N * (ey + 1))
                                     return fail(ctx, SEM_E_ARG, "membrane on the face of an obstacle element");
             }
+        }
+        if (b.verts_set) {   // curved box: tabulated coupling
+            st = pmut_tables(ctx, pt, b, *pd, ks);
+            if (st) return st;
         }
         std::vector<double> sx((size_t)KL * M * lmax, 0.0), sy((size_t)KL * M * lmax, 0.0), wx((size_t)KL * lmax, 0.0),
             wy((size_t)KL * lmax, 0.0), om2((size_t)KL * M), tzw((size_t)KL * M), im(M), et(M), dl(KL);
@@ -1604,7 +1691,7 @@ sem_status sem_box_set_vertices(sem_ctx* ctx, int box, const double* verts, size
     sem_status st = scatter_box_check(ctx, box, verts, "vertices");
     if (st) return st;
     if (ctx->parts[0].pm.on && ctx->parts[0].pm.box == box)
-        return fail(ctx, SEM_E_STATE, "PMUTs on a curved (vertex-lattice) box are not supported");
+        return fail(ctx, SEM_E_STATE, "set the vertices before attaching the PMUTs of their box");
     Box& b = ctx->parts[0].boxes[box];
     const sem_box_desc& g = ctx->gdesc[box];
     if (b.verts_set) return fail(ctx, SEM_E_STATE, "vertices already set");
@@ -1655,34 +1742,29 @@ sem_status sem_pml_attach(sem_ctx* ctx, int box, const double* thickness, double
     if (st) return st;
     if (box < 0 || box >= (int)ctx->gdesc.size() || !thickness) return fail(ctx, SEM_E_ARG, "bad box / thickness");
     if (!(R > 0.0 && R < 1.0)) return fail(ctx, SEM_E_ARG, "PML reflection coefficient must be in (0, 1)");
-    if (ctx->world > 1 || ctx->parts.size() != 1)
-        return fail(ctx, SEM_E_PARTITION, "the PML is implemented for a single slab (world 1) only");
-    sem::Part& pt = ctx->parts[0];
-    if (pt.pml.on) return fail(ctx, SEM_E_STATE, "PML already attached");
-    if (pt.boxes[box].curved) return fail(ctx, SEM_E_STATE, "PML on a curved box is not supported");
-    Box& b = pt.boxes[box];
+    for (auto& pt : ctx->parts) {
+        if (pt.pml.on) return fail(ctx, SEM_E_STATE, "PML already attached");
+        if (pt.boxes[box].curved) return fail(ctx, SEM_E_STATE, "PML on a curved box is not supported");
+    }
     const sem_box_desc& g = ctx->gdesc[box];
     for (int f = 0; f < 6; ++f)
         if (!(thickness[f] >= 0.0) || !std::isfinite(thickness[f])) return fail(ctx, SEM_E_ARG, "thickness must be >= 0");
     for (int d = 0; d < 3; ++d)
         if (thickness[2 * d] + thickness[2 * d + 1] > g.extent[d] * (1.0 + 1e-12))
             return fail(ctx, SEM_E_ARG, "PML layers of opposite faces overlap");
-    const int N = b.N;
+    const int N = g.degree;
     std::vector<double> x, w;
     gll_rule(N, x, w);
-    sem::PmlBox& m = pt.pml;
-    m.box = box;
-    m.D = deriv_matrix(x);
-    m.w = w;
-    // 1D damping profiles z_d at the lattice nodes (reading R23)
-    const long long nn[3] = {b.NX, b.NY, b.NZ};
+    // 1D damping profiles z_d at the GLOBAL lattice nodes (reading R23): a y-slab takes its
+    // rows of the y profile, so the layers sit at the global box faces, never at a slab cut
+    const long long ng[3] = {(long long)N * g.nel[0] + 1, (long long)N * g.nel[1] + 1, (long long)N * g.nel[2] + 1};
     std::vector<double> zt[3];
     std::vector<char> epml[3];
     for (int d = 0; d < 3; ++d) {
         const int nel = g.nel[d];
         const double hd = g.extent[d] / nel;
-        zt[d].assign(nn[d], 0.0);
-        for (long long i = 0; i < nn[d]; ++i) {
+        zt[d].assign(ng[d], 0.0);
+        for (long long i = 0; i < ng[d]; ++i) {
             long long e = i / N;
             if (e > nel - 1) e = nel - 1;
             const int a = (int)(i - e * N);
@@ -1703,25 +1785,32 @@ sem_status sem_pml_attach(sem_ctx* ctx, int box, const double* thickness, double
             for (int a = 0; a <= N; ++a)
                 if (zt[d][(size_t)e * N + a] > 0.0) epml[d][e] = 1;
     }
-    // PML elements: every element with a node where some z_d > 0
-    std::vector<int> el;
-    for (int ez = 0; ez < g.nel[2]; ++ez)
-        for (int ey = 0; ey < g.nel[1]; ++ey)
-            for (int ex = 0; ex < g.nel[0]; ++ex)
-                if (epml[0][ex] || epml[1][ey] || epml[2][ez]) {
-                    el.push_back(ex);
-                    el.push_back(ey);
-                    el.push_back(ez);
-                }
-    m.n_el = (int)(el.size() / 3);
-    const size_t nl = (size_t)(N + 1) * (N + 1) * (N + 1);
-    if (m.n_el > 0) {
-        // per-axis node tables: z, CN factors, inverse assembled 1D mass (PmlParams::tx)
+    for (auto& pt : ctx->parts) {
+        Box& b = pt.boxes[box];
+        sem::PmlBox& m = pt.pml;
+        m.box = box;
+        m.D = deriv_matrix(x);
+        m.w = w;
+        const long long ey0 = b.gy0 / N, nely = b.d.nel[1];
+        // PML elements of this slab: every element with a node where some z_d > 0 (slab-local y index)
+        std::vector<int> el;
+        for (int ez = 0; ez < g.nel[2]; ++ez)
+            for (long long ey = 0; ey < nely; ++ey)
+                for (int ex = 0; ex < g.nel[0]; ++ex)
+                    if (epml[0][ex] || epml[1][ey + ey0] || epml[2][ez]) {
+                        el.push_back(ex);
+                        el.push_back((int)ey);
+                        el.push_back(ez);
+                    }
+        m.n_el = (int)(el.size() / 3);
+        const size_t nl = (size_t)(N + 1) * (N + 1) * (N + 1);
+        // per-axis node tables: z, CN factors, inverse assembled 1D mass (PmlParams::tx); slab rows in y
+        const long long nn[3] = {b.NX, b.NY, b.NZ}, i0[3] = {0, b.gy0, 0};
         const std::vector<double>* m1[3] = {&b.mxh, &b.myh, &b.mzh};
         for (int d = 0; d < 3; ++d) {
             std::vector<double> t4((size_t)nn[d] * 4);
             for (long long i = 0; i < nn[d]; ++i) {
-                const double zz = zt[d][i], den = 1.0 + 0.5 * ctx->dt * zz;
+                const double zz = zt[d][i + i0[d]], den = 1.0 + 0.5 * ctx->dt * zz;
                 t4[4 * i] = zz;
                 t4[4 * i + 1] = (1.0 - 0.5 * ctx->dt * zz) / den;
                 t4[4 * i + 2] = ctx->dt / den;
@@ -1729,11 +1818,50 @@ sem_status sem_pml_attach(sem_ctx* ctx, int box, const double* thickness, double
             }
             if (upload(ctx, &m.tab[d], t4)) return SEM_E_CUDA;
         }
-        if (upload(ctx, &m.elems, el)) return SEM_E_CUDA;
-        if (dalloc(ctx, &m.phi, (size_t)m.n_el * 3 * nl) || dalloc(ctx, &m.psi[0], (size_t)b.nalloc()) ||
+        if (m.n_el > 0 && upload(ctx, &m.elems, el)) return SEM_E_CUDA;
+        if (dalloc(ctx, &m.phi, (size_t)std::max(m.n_el, 1) * 3 * nl) || dalloc(ctx, &m.psi[0], (size_t)b.nalloc()) ||
             dalloc(ctx, &m.psi[1], (size_t)b.nalloc()) || dalloc(ctx, &m.da, (size_t)b.nalloc()))
             return SEM_E_OOM;
+        // the region (nodes of PML elements) as x-row segments: node (ix, iy, iz) belongs to a PML element
+        // iff some element containing it along some axis d has a damped node (element masks per axis)
+        if (m.n_el > 0) {
+            auto node_mask = [&](int d, long long n, long long off) {
+                std::vector<char> nm((size_t)n, 0);
+                for (long long i = 0; i < n; ++i) {
+                    const long long ig = i + off;
+                    const long long e1 = std::min<long long>(ig / N, g.nel[d] - 1), e0 = (ig % N == 0 && ig > 0) ? ig / N - 1 : e1;
+                    nm[(size_t)i] = (epml[d][e0] || epml[d][e1]) ? 1 : 0;
+                }
+                return nm;
+            };
+            const std::vector<char> mx = node_mask(0, b.NX, 0), my = node_mask(1, b.NY, b.gy0), mz = node_mask(2, b.NZ, 0);
+            std::vector<long long> ss;
+            std::vector<int> sl;
+            for (long long iz = 0; iz < b.NZ; ++iz)
+                for (long long iy = 0; iy < b.NY; ++iy) {
+                    const long long row = (iz * b.NY + iy) * b.PX;
+                    if (my[(size_t)iy] || mz[(size_t)iz]) {
+                        ss.push_back(row);
+                        sl.push_back((int)b.NX);
+                        continue;
+                    }
+                    for (long long ix = 0; ix < b.NX;) {
+                        if (!mx[(size_t)ix]) {
+                            ++ix;
+                            continue;
+                        }
+                        long long e = ix;
+                        while (e < b.NX && mx[(size_t)e]) ++e;
+                        ss.push_back(row + ix);
+                        sl.push_back((int)(e - ix));
+                        ix = e;
+                    }
+                }
+            if (upload(ctx, &m.seg_start, ss) || upload(ctx, &m.seg_len, sl)) return SEM_E_CUDA;
+            m.n_seg = (long long)ss.size();
+        }
         m.on = true;
+        if (ctx->world > 1 && setup_exchange(ctx, pt) != SEM_OK) return SEM_E_OOM;   // + the PML da plane
     }
     drop_graphs(ctx);
     st = reset_dynamic(ctx);

@@ -155,6 +155,13 @@ struct ModalParams {
     double* __restrict__ phi;       // phi_k(t^{n+1}, q^{n+1}) for readout
     double* __restrict__ F;         // force plane [NX*NY]
     const long long* step;
+    // tabulated coupling (curved boxes: B_{k,m,j} = sum_F w_a w_b |J_s| S_{k,m}(x_j), not separable):
+    // PMUT k's face nodes tidx[toff[k] .. toff[k+1]) (pitched indices into P's plane z = 0) with B[j][m];
+    // the force f = kappa B^T qdd goes straight into the box's assembled residual res (r -= f)
+    const int* __restrict__ toff;
+    const long long* __restrict__ tidx;
+    const double* __restrict__ tB;
+    double* res;
 };
 
 struct IfaceParams {
@@ -218,6 +225,12 @@ struct PmlParams {
     double s2h[3];                      // 2 / h_d
     double jac;                         // |J| = h_x h_y h_z / 8
     double c2, dt;
+    int cutL;                           // y-slab with a lower cut (multi-GPU): its row 0 is the cut plane
+    // the PML region (nodes of PML elements) as contiguous lattice-row segments [start, start + len)
+    // of the pitched layout, each node once (the fix-up sweeps them coalesced, no atomics)
+    const long long* __restrict__ seg_start;
+    const int* __restrict__ seg_len;
+    long long n_seg;
 };
 
 // Curved box: element-by-element K p with the geometric factors recomputed from
@@ -280,7 +293,10 @@ struct CutParams {
     const double* tau;
     const double* sig;
     double ktau[kMaxN + 1], ksig[kMaxN + 1];
-    double* out;                    // send buffer: [NX*NZ plane][NXt tau][NXt sigma]
+    // PML box: its acceleration da at the cut plane travels with the message (the neighbour's PML
+    // elements touching the shared nodes), applied by the fix-up like the partial rows
+    const double* pda;              // PML da of this box (pitched) or nullptr
+    double* out;                    // send buffer: [NX*NZ plane][NXt tau][NXt sigma][NX*NZ PML da]
     const double* in;               // receive buffer, same layout
 };
 
@@ -334,6 +350,9 @@ struct PmlBox {
     double* psi[2] = {nullptr, nullptr};
     double* da = nullptr;
     double* tab[3] = {nullptr, nullptr, nullptr};   // per-axis node tables (PmlParams::tx)
+    long long* seg_start = nullptr;                  // PML region row segments (PmlParams::seg_start)
+    int* seg_len = nullptr;
+    long long n_seg = 0;
     std::vector<double> D, w;
 };
 
@@ -346,6 +365,9 @@ struct Pmut {
     double *q = nullptr, *qd = nullptr, *qdd = nullptr, *phi = nullptr, *F = nullptr;
     double amp = 0, om0 = 0, ncyc = 1, t_end = 0, t_switch = 0, invC = 0, kappa = 0;
     int rx = 0;
+    int* toff = nullptr;             // tabulated coupling of a curved box (ModalParams::toff)
+    long long* tidx = nullptr;
+    double* tB = nullptr;
 };
 
 struct Iface {

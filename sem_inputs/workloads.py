@@ -472,3 +472,25 @@ def curved_interface_config(nf=(6, 6, 2), nc=(4, 4, 2), degree_f=4, degree_c=3, 
            "interface": {"fine_box": 0, "coarse_box": 1, "alpha": alpha}}
     rec["dt"] = cfl_dt(rec["boxes"], cfl)
     return _finish(rec)
+
+
+def curved_pmut_config(nel=(6, 6, 4), degree=4, h=25e-6, amp=0.12, floor_jitter=0.12, seed=9, rx=False,
+                       n_steps=300, cfl=0.25):
+    """A PMUT on a curved box (SURVEY 8(f) item 3 with the PMUT coupling of Eqs. 11-12): curved_config's
+    bulged, jittered vertex lattice whose z = 0 layer (the membrane face) also moves in-plane by
+    U(-floor_jitter, floor_jitter) x h (interior vertices; the face stays planar), so the face weights
+    |J_s| and the node positions the mode shapes are evaluated at are not those of the affine lattice.
+    One config-0 membrane (100 um square, 3 modes) centred on the floor; TX burst, or RX from t = 0."""
+    extent = tuple(h * n for n in nel)
+    rec = curved_config(nel=nel, degree=degree, extent=extent, amp=amp, bc_top=BC_ABSORBING, n_steps=n_steps,
+                        cfl=cfl, seed=seed)
+    rec["name"] = "curved_pmut"
+    v = rec["boxes"][0]["vertices"].reshape(nel[2] + 1, nel[1] + 1, nel[0] + 1, 3)
+    J = np.random.default_rng(seed + 1).uniform(-floor_jitter, floor_jitter, size=(nel[1] + 1, nel[0] + 1, 2)) * h
+    J[0, :, :] = J[-1, :, :] = 0.0
+    J[:, 0, :] = J[:, -1, :] = 0.0
+    v[0, :, :, :2] += J
+    rec["boxes"][0]["vertices"] = v.reshape(-1, 3)
+    cx, cy = extent[0] / 2, extent[1] / 2
+    rec["pmut"] = _pmut([[cx, cy]], MODES_3, FREQS_3, None, [0.0], rx=rx)
+    return rec

@@ -25,9 +25,9 @@ def oracle_run(rec, n_steps, state=None, coupling=None):
     return nm.run(n_steps)
 
 
-def gpu_run(rec, n_steps, state=None, flags=0, chunks=None):
+def gpu_run(rec, n_steps, state=None, flags=0, chunks=None, world=1):
     from paper_2603_06267_b200 import Simulation
-    sim = Simulation(rec, flags=flags)
+    sim = Simulation(rec, flags=flags, world=world)
     if state is not None:
         for b, (p, v) in enumerate(state):
             sim.write_state(b, p, v)

@@ -75,3 +75,40 @@ def test_pml_with_pmut_array():
     assert np.abs(nm.q).max() > 1e-12
     for k, v in r.items():
         assert v < TOL, (k, v, r)
+
+
+@pytest.mark.parametrize("world,layers,nel", [
+    (2, (1, 1, 1, 1, 0, 1), (4, 6, 4)),        # lateral + top layers, both slabs carry PML elements
+    (3, (0, 0, 1, 1, 0, 0), (3, 9, 3)),        # y layers only: the middle slab has none
+    (4, (1, 0, 1, 0, 1, 1), (3, 8, 4)),        # corners and a layer ending at a cut
+])
+def test_pml_under_y_slabs(world, layers, nel):
+    """PML under the y-slab decomposition (emulated ranks on one GPU): the profiles come from the global
+    box, each slab's PML acceleration at the cut plane travels with the exchange and the nodal terms of a
+    cut node are counted by the slab below only."""
+    from paper_2603_06267_b200 import SEM_F_EMULATE_SLABS
+    rec = pml_config(nel=nel, degree=4, extent=(1e-4 * nel[0], 0.9e-4 * nel[1], 1.1e-4 * nel[2]),
+                     layers=layers, layer_el=1)
+    st = random_state(rec, seed=5 + world)
+    for n in (1, 4, 20):
+        nm = oracle_run(rec, n, state=st)
+        sim = gpu_run(rec, n, state=st, flags=SEM_F_EMULATE_SLABS, world=world)
+        d_gpu = sim.pressure(0) - st[0][0]
+        d_orc = nm.sys.split(nm.p)[0] - st[0][0]
+        assert rel_l2(d_gpu, d_orc) < 1e-10, (n, rel_l2(d_gpu, d_orc))
+        for k, v in compare(sim, nm).items():
+            assert v < TOL, (n, k, v)
+        sim.close()
+
+
+def test_pml_config0_pmut_two_slabs():
+    from paper_2603_06267_b200 import SEM_F_EMULATE_SLABS
+    rec = config(0)
+    b = rec["boxes"][0]
+    h = b["extent"][0] / b["nel"][0]
+    rec["pml"] = {"box": 0, "thickness": [h, h, h, h, 0.0, h], "R": 1e-4}
+    rec["boxes"][0]["bc"] = [1, 1, 1, 1, 0, 1]
+    nm = oracle_run(rec, rec["n_steps"])
+    sim = gpu_run(rec, rec["n_steps"], flags=SEM_F_EMULATE_SLABS, world=2)
+    for k, v in compare(sim, nm).items():
+        assert v < TOL, (k, v)

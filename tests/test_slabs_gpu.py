@@ -64,8 +64,11 @@ def test_random_state_interface_slabs(world):
 
 def test_partition_errors():
     from paper_2603_06267_b200 import SemError
-    with pytest.raises(SemError, match="PARTITION"):
-        _sim(config(0), 2)                     # the cut at y = 300 um crosses the membrane
+    from paper_2603_06267_b200 import SEM_F_EMULATE_SLABS, Simulation
+    with pytest.raises(SemError, match="PARTITION"):   # an explicit equal plan: y = 300 um crosses the membrane
+        Simulation(config(0), world=2, flags=SEM_F_EMULATE_SLABS, slab_y0=[0, 2, 4])
+    with pytest.raises(SemError, match="PARTITION"):   # a cut that is not a coarse element boundary
+        Simulation(small_config("cfg2s"), world=2, flags=SEM_F_EMULATE_SLABS, slab_y0=[0, 5, 12])
     with pytest.raises(SemError, match="PARTITION"):
         _sim(small_config("cfg2s"), 5)         # 12 elements are not divisible by 5
     with pytest.raises(SemError, match="PARTITION"):
