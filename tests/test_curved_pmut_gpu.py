@@ -38,7 +38,7 @@ def test_curved_pmut_rx_random_state():
         nm = oracle_run(rec, n, state=st)
         sim = gpu_run(rec, n, state=st)
         r = compare(sim, nm)
-        assert np.abs(nm.q).max() > 0.0
+        assert n == 1 or np.abs(nm.q).max() > 0.0      # q^1 = 0 (pdd^0 = qdd^0 = 0), driven after
         for k, v in r.items():
             assert v < TOL, (n, k, v, r)
         sim.close()

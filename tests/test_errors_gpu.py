@@ -63,10 +63,11 @@ def test_pml_layers_overlap_rejected():
     assert _status(lambda: Simulation(rec)) == SEM_E_ARG
 
 
-def test_curved_box_refuses_pmut():
+def test_curved_box_refuses_pml():
+    """Curved boxes carry PMUTs (tabulated coupling) and the general interface, not a PML."""
     from paper_2603_06267_b200 import Simulation
     rec = curved_config(nel=(4, 4, 4), degree=4, extent=(0.6e-3,) * 3, bc_top=BC_ABSORBING)
-    rec["pmut"] = config(0)["pmut"]
+    rec["pml"] = {"box": 0, "thickness": [0.15e-3, 0, 0, 0, 0, 0], "R": 1e-4}
     assert _status(lambda: Simulation(rec)) == SEM_E_STATE
 
 
