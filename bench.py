@@ -11,9 +11,10 @@ largest config and the one the north-star's roofline / scaling targets name), sy
 Prints ONE JSON line on rank 0.  For N > 1 the ranks run the y-slab decomposition: under torchrun, or
 spawned by this script itself (torch.distributed.run on 127.0.0.1) when WORLD_SIZE is unset.
 
-Timing: the CUDA-graph path users get (profiling off), K steps per repeat, median of 5 repeats (each
-bracketed by barrier + synchronize, max over ranks); per-kernel times for the roofline come from a
-separate profiling pass over K more steps (direct launches with CUDA events on the launching stream).
+Timing: the CUDA-graph path users get (profiling off): exactly K steps, timed as 5 repeats of ~K/5 steps
+(each bracketed by barrier + synchronize, max over ranks), median ms per step; per-kernel times for the
+roofline come from a separate profiling pass over K more steps (direct launches with CUDA events on the
+launching stream).
 """
 from __future__ import annotations
 
@@ -246,24 +247,25 @@ def main():
                      flags=flags)
     ndof_total = sum(sim.ndof)      # global node count (every rank holds one y-slab of it)
 
-    # ---- device-resident timed region: the CUDA-graph path users get (profiling off), K steps per
-    #      repeat, N_REPEATS repeats, each bracketed by barrier + synchronize; max over ranks per repeat,
-    #      median over repeats
+    # ---- device-resident timed region: the CUDA-graph path users get (profiling off); exactly K steps,
+    #      timed as N_REPEATS repeats of ~K/N_REPEATS steps, each bracketed by barrier + synchronize;
+    #      max over ranks per repeat; the step time is the median over repeats of ms per step
     sim.step(args.warmup)
     sim.sync()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = []
-    launches = 0
-    for _ in range(N_REPEATS):
+    nrep = max(1, min(N_REPEATS, args.steps))
+    chunks = [args.steps // nrep + (1 if r < args.steps % nrep else 0) for r in range(nrep)]
+    reps, launches = [], 0
+    for n in chunks:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        sim.step(args.steps)
-        launches = sem_last_launch_count(sim.ctx)
+        sim.step(n)
+        launches += sem_last_launch_count(sim.ctx)
         e1.record(stream)
         torch.cuda.synchronize()
         r = e0.elapsed_time(e1)
@@ -273,7 +275,7 @@ def main():
             r = float(t.item())
         reps.append(r)
     clk = clocks.stop()
-    ms = statistics.median(reps)
+    ms = statistics.median([r / n for r, n in zip(reps, chunks)]) * args.steps
     # ---- per-kernel pass (same K steps, direct launches with CUDA events around each kernel group on
     #      the launching stream): the roofline's kernel time and the step shares
     sem_set_profiling(sim.ctx, 1)
@@ -361,7 +363,8 @@ def main():
                      "interface_ms_per_step": ifc_ms / max(ifc_n, 1), "modal_ms_per_step": mod_ms / max(mod_n, 1)},
         "gpu_launches": launches,
         "repeats_ms": reps,
-        "timed_path": f"CUDA graph (sem_step), median of {N_REPEATS} repeats of K steps",
+        "repeat_steps": chunks,
+        "timed_path": f"CUDA graph (sem_step): the K steps timed in {nrep} repeats, median ms per step",
         "clocks": clk,
         "e2e": e2e,
     }

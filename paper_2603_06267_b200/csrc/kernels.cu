@@ -1410,7 +1410,10 @@ struct IfFused {
     static constexpr int FW = (kIfTC + 1) * NFR + 1;   // fine footprint nodes per direction
     static constexpr int CW = (kIfTC + 1) * NC + 1;    // coarse footprint nodes per direction
     static constexpr int CO = kIfTC * NC + 1;          // owned coarse rows (the last tile: + the box's last)
-    static constexpr int SMEM = 8 * (2 * CW * CW + 2 * FW * FW + 2 * CO * FW);
+    // shared memory: coarse trace [2][CW][CW] | weighted fine terms [2][FW][FW] | a union of the
+    // x-interpolated coarse trace [2][CW][FW] (phase 2) and the y-gathered terms [2][CO][FW] (phases 3-4)
+    static constexpr int UNION = (CW > CO ? CW : CO) * FW;
+    static constexpr int SMEM = 8 * (2 * CW * CW + 2 * FW * FW + 2 * UNION);
 };
 
 template <int NF, int NC, int R>
@@ -1423,7 +1426,9 @@ __global__ void __launch_bounds__(256) iface_fused(const __grid_constant__ Iface
     double* const g1 = sd + CW * CW;        // [FW][FW] weighted fine terms (row = y)
     double* const g2 = g1 + FW * FW;
     double* const h1 = g2 + FW * FW;        // [CO][FW] after the y pass
-    double* const h2 = h1 + CO * FW;
+    double* const h2 = h1 + G::UNION;
+    double* const xt = h1;                  // [CW][FW] coarse trace interpolated along x (phase 2 only)
+    double* const xd = h2;
     const int tid = threadIdx.x, nth = blockDim.x;
     const int ex0 = (int)blockIdx.x * TC - 1, ey0 = (int)blockIdx.y * TC - 1;   // footprint's first element
     const long long NXf = p.NXf, NYf = p.NYf, NXc = p.NXc, NYc = p.NYc;
@@ -1444,6 +1449,22 @@ __global__ void __launch_bounds__(256) iface_fused(const __grid_constant__ Iface
         sd[k] = d;
     }
     __syncthreads();
+    // (1b) the coarse trace interpolated along x at every fine column of the footprint (separable: the
+    //      fine flux then needs N_c + 1 values per node instead of (N_c + 1)^2)
+    for (int k = tid; k < CW * FW; k += nth) {
+        const int i = k % FW, j = k / FW;
+        const int elx = i / NFR < TC ? i / NFR : TC, qx = i - elx * NFR;
+        double rt = 0.0, rd = 0.0;
+#pragma unroll
+        for (int a = 0; a <= NC; ++a) {
+            const double wx = __ldg(p.I + qx * (NC + 1) + a);
+            rt = fma(wx, st[j * CW + elx * NC + a], rt);
+            rd = fma(wx, sd[j * CW + elx * NC + a], rd);
+        }
+        xt[k] = rt;
+        xd[k] = rd;
+    }
+    __syncthreads();
     // (2) fine flux
     const long long Sf = p.PXf * NYf;
     const double* top = p.Pf + (p.NZf - 1) * Sf;
@@ -1459,23 +1480,14 @@ __global__ void __launch_bounds__(256) iface_fused(const __grid_constant__ Iface
             double dpp = 0.0;
 #pragma unroll
             for (int c = 0; c <= NF; ++c) dpp = fma(p.dfT[c], __ldg(node - (long long)(NF - c) * Sf), dpp);
-            // coarse element (footprint-local) and local fine index of this node in it
-            const int elx = i / NFR < TC ? i / NFR : TC, ely = j / NFR < TC ? j / NFR : TC;
-            const int qx = i - elx * NFR, qy = j - ely * NFR;
+            // coarse element row (footprint-local) and local fine index of this node in it along y
+            const int ely = j / NFR < TC ? j / NFR : TC, qy = j - ely * NFR;
             double pm = 0.0, dpm = 0.0;
 #pragma unroll
             for (int b = 0; b <= NC; ++b) {
                 const double wy = __ldg(p.I + qy * (NC + 1) + b);
-                const int row = (ely * NC + b) * CW + elx * NC;
-                double rt = 0.0, rd = 0.0;
-#pragma unroll
-                for (int a = 0; a <= NC; ++a) {
-                    const double wx = __ldg(p.I + qx * (NC + 1) + a);
-                    rt = fma(wx, st[row + a], rt);
-                    rd = fma(wx, sd[row + a], rd);
-                }
-                pm = fma(wy, rt, pm);
-                dpm = fma(wy, rd, dpm);
+                pm = fma(wy, xt[(ely * NC + b) * FW + i], pm);
+                dpm = fma(wy, xd[(ely * NC + b) * FW + i], dpm);
             }
             const double J = pp - pm;
             const double A = 0.5 * (p.cf2 * dpp + p.cc2 * dpm);
