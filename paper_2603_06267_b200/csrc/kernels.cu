@@ -54,33 +54,8 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-// try_wait with a suspend-time hint: the thread sleeps in hardware until the phase completes (or the
-// hint elapses) instead of re-issuing the test (SEM_WAIT_HINT = 0: plain polling)
-#ifndef SEM_ZSMEM
-#define SEM_ZSMEM 0
-#endif
-#ifndef SEM_XSPLIT
-#define SEM_XSPLIT 0
-#endif
-#ifndef SEM_WAIT_HINT
-#define SEM_WAIT_HINT 0
-#endif
-__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity), "r"((uint32_t)SEM_WAIT_HINT)
-        : "memory");
-    return ok != 0;
-}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    if (SEM_WAIT_HINT) {
-        while (!mbar_try_wait_hint(bar, parity)) {
-        }
-    } else {
-        while (!mbar_try_wait(bar, parity)) {
-        }
+    while (!mbar_try_wait(bar, parity)) {
     }
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint32_t bar) {
@@ -190,27 +165,12 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
     double v[N + 1];
 #pragma unroll
     for (int b = 0; b <= N; ++b) v[b] = sP[t.xb + b];
-#if SEM_XSPLIT   // two accumulation chains per x row (shorter dependent DFMA chains)
-    double xr0 = 0.0, xr1 = 0.0, xl0 = 0.0, xl1 = 0.0;
-#pragma unroll
-    for (int b = 0; b <= N; b += 2) {
-        xr0 = fma(t.cR[b], v[b], xr0);
-        xl0 = fma(RT.L[b], v[b], xl0);
-    }
-#pragma unroll
-    for (int b = 1; b <= N; b += 2) {
-        xr1 = fma(t.cR[b], v[b], xr1);
-        xl1 = fma(RT.L[b], v[b], xl1);
-    }
-    const double xr = xr0 + xr1, xl = xl0 + xl1;
-#else
     double xr = 0.0, xl = 0.0;
 #pragma unroll
     for (int b = 0; b <= N; ++b) {
         xr = fma(t.cR[b], v[b], xr);
         xl = fma(RT.L[b], v[b], xl);
     }
-#endif
     const double xlr = __shfl_sync(0xffffffffu, xl, (threadIdx.x + 31) & 31);
     // ---- y: per-warp row (registers, scaled); left row of a shared node: row L
     double y0 = 0.0, y1 = 0.0;
@@ -379,214 +339,6 @@ __device__ __forceinline__ void vol_layer(const VolParams& p, const VolThread<N>
     }
 }
 
-#if SEM_ZSMEM
-// ---- Variant: z taps read from the ring (no register window).  A plane's slot is released N planes
-//      after the plane itself (the last plane whose z row reaches back to it), the layer's planes
-//      z0 .. z0 + N are waited for at the layer's start.  Frees the 2N+1-double register window, so
-//      more consumer rows (SEM_KTY) fit the register file.
-template <class RG>
-__device__ __forceinline__ double ring_val(const unsigned char* ring, int slot, int own) {
-    return reinterpret_cast<const double*>(ring + slot * RG::SLOT)[own];
-}
-template <class RG>
-__device__ __forceinline__ int slot_add(int s, int j) {   // (s + j) mod D for |j| < D
-    int r = s + j;
-    if (r < 0) r += RG::D;
-    if (r >= RG::D) r -= RG::D;
-    return r;
-}
-
-template <int N, int TY, int C, int F, class RG>
-__device__ __forceinline__ void vol_plane_z(const VolParams& p, const VolThread<N>& t, const unsigned char* ring,
-                                            int s_cur, int s0, int ez, double& wn_out, double& pn_out) {
-    using G = VolGeo<N, TY>;
-    const BoxTables& T = p.tab;
-    const double* __restrict__ sP = reinterpret_cast<const double*>(ring + s_cur * RG::SLOT);
-    const double* __restrict__ sW = reinterpret_cast<const double*>(ring + s_cur * RG::SLOT + G::POFF);
-    const auto& RT = kRef<N>;
-    double v[N + 1];
-#pragma unroll
-    for (int b = 0; b <= N; ++b) v[b] = sP[t.xb + b];
-    double xr = 0.0, xl = 0.0;
-#pragma unroll
-    for (int b = 0; b <= N; ++b) {
-        xr = fma(t.cR[b], v[b], xr);
-        xl = fma(RT.L[b], v[b], xl);
-    }
-    const double xlr = __shfl_sync(0xffffffffu, xl, (threadIdx.x + 31) & 31);
-    double y0 = 0.0, y1 = 0.0;
-#pragma unroll
-    for (int b = 0; b <= N; b += 2) y0 = fma(t.cyR[b], sP[t.yb + b * G::SW], y0);
-#pragma unroll
-    for (int b = 1; b <= N; b += 2) y1 = fma(t.cyR[b], sP[t.yb + b * G::SW], y1);
-    double acc = fma(t.fL, xlr, xr) + (y0 + y1);
-    if (t.yLs != 0.0) {
-        double yl = 0.0;
-#pragma unroll
-        for (int b = 0; b <= N; ++b) yl = fma(RT.L[b], sP[t.yl + b * G::SW], yl);
-        acc = fma(t.yLs, yl, acc);
-    }
-    // z taps from the layer's planes z0 - N .. z0 + N (slot s0 = plane z0)
-    double z0 = 0.0, z1 = 0.0;
-    if constexpr (C == N) {
-#pragma unroll
-        for (int b = 0; b <= N; b += 2) z0 = fma(2.0 * RT.L[b], ring_val<RG>(ring, slot_add<RG>(s0, b), t.own), z0);
-#pragma unroll
-        for (int b = 1; b <= N; b += 2) z1 = fma(2.0 * RT.L[b], ring_val<RG>(ring, slot_add<RG>(s0, b), t.own), z1);
-    } else if constexpr (C == 0 && (F & kFirst)) {
-#pragma unroll
-        for (int b = 0; b <= N; b += 2) z0 = fma(2.0 * RT.R[0][b], ring_val<RG>(ring, slot_add<RG>(s0, b), t.own), z0);
-#pragma unroll
-        for (int b = 1; b <= N; b += 2) z1 = fma(2.0 * RT.R[0][b], ring_val<RG>(ring, slot_add<RG>(s0, b), t.own), z1);
-    } else if constexpr (C == 0) {
-#pragma unroll
-        for (int b = 0; b <= N; ++b) z0 = fma(RT.R[0][b], ring_val<RG>(ring, slot_add<RG>(s0, b), t.own), z0);
-#pragma unroll
-        for (int b = 0; b <= N; ++b) z1 = fma(RT.L[b], ring_val<RG>(ring, slot_add<RG>(s0, b - N), t.own), z1);
-    } else {
-#pragma unroll
-        for (int b = 0; b <= N; b += 2) z0 = fma(RT.R[C][b], ring_val<RG>(ring, slot_add<RG>(s0, b), t.own), z0);
-#pragma unroll
-        for (int b = 1; b <= N; b += 2) z1 = fma(RT.R[C][b], ring_val<RG>(ring, slot_add<RG>(s0, b), t.own), z1);
-    }
-    acc = fma(p.sdir[2], z0 + z1, acc);
-    double a = -acc;
-    const double wv = sW[t.wown];
-    const double pv = sP[t.own];
-    double damp = t.dxy;
-    if constexpr ((F & kFirst) && C == 0) {
-        damp += p.damp[4];
-        if (p.F && t.valid) a = fma(p.kF, __ldg(p.F + t.fc), a);
-    }
-    if constexpr ((F & kLast) && C == N) {
-        damp += p.damp[5];
-        if (p.pw_on && t.valid) {
-            const int ixp = t.fc % (int)p.NX, iyp = t.fc / (int)p.NX;
-            const double t1 = (double)(__ldcg(p.step) + 1) * p.dt;
-            const double tau = t1 - (p.pw_k[0] * (__ldg(p.xc + ixp) - p.pw_xref[0]) +
-                                     p.pw_k[1] * (__ldg(p.yc + iyp) - p.pw_xref[1]) +
-                                     p.pw_k[2] * (p.pw_ztop - p.pw_xref[2])) / p.pw_c;
-            const double u = tau - p.pw_t0;
-            const double is2 = 1.0 / (p.pw_sigma * p.pw_sigma);
-            double sn, cs;
-            sincos(p.pw_om * u, &sn, &cs);
-            a += p.pw_fac * (exp(-0.5 * u * u * is2) * (-u * is2 * sn + p.pw_om * cs));
-        }
-    }
-    if constexpr (F & kLast) {
-        if (p.iface_side > 0 && t.valid) {
-            a -= __ldg(p.sig + t.fc) * T.ksig[C];
-            if constexpr (C == N) a -= __ldg(p.tau + t.fc) * T.ktau[N];
-        }
-    }
-    if constexpr (F & kFirst) {
-        if (p.iface_side < 0 && t.valid) {
-            a -= __ldg(p.sig + t.fc) * T.ksig[C];
-            if constexpr (C == 0) a -= __ldg(p.tau + t.fc) * T.ktau[0];
-        }
-    } else if constexpr (C == 0) {
-        if (p.iface_side < 0 && ez == 1 && t.valid) a -= __ldg(p.sig + t.fc) * T.ksig[N];
-    }
-    a = fma(-damp, wv, a);
-    wn_out = fma(p.dt, a, wv);
-    pn_out = fma(p.dt, wn_out, pv);
-}
-
-// planes of one layer (compile-time C); after plane z the slot of plane z - N is released (rel)
-template <int N, int TY, class RG, int F, int C>
-__device__ __forceinline__ void vol_layer_step_z(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
-                                                 uint32_t bars, int ez, int s0, double*& outP, double*& outW,
-                                                 int& s_cur, RingPos& rel, int& zc) {
-    constexpr int NP = (F & kLast) ? N + 1 : N;
-    if constexpr (C < NP) {
-        const long long PS = p.PX * p.NY;
-        if constexpr (SEM_PAIR && C + 1 < NP) {
-            const int s1 = slot_add<RG>(s_cur, 1);
-            double w0, p0, w1, p1;
-            vol_plane_z<N, TY, C, F, RG>(p, t, ring, s_cur, s0, ez, w0, p0);
-            vol_plane_z<N, TY, C + 1, F, RG>(p, t, ring, s1, s0, ez, w1, p1);
-            if (t.valid) {
-                st_out(outW, w0);
-                st_out(outP, p0);
-                st_out(outW + PS, w1);
-                st_out(outP + PS, p1);
-            }
-            outP += 2 * PS;
-            outW += 2 * PS;
-            __syncwarp();
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                if (zc + k >= N) {
-                    if (threadIdx.x == 0) mbar_arrive(bars + 8u * (RG::D + rel.slot));
-                    rel.template advance<RG::D>();
-                }
-            }
-            zc += 2;
-            s_cur = slot_add<RG>(s1, 1);
-            vol_layer_step_z<N, TY, RG, F, C + 2>(p, t, ring, bars, ez, s0, outP, outW, s_cur, rel, zc);
-        } else {
-            double w0, p0;
-            vol_plane_z<N, TY, C, F, RG>(p, t, ring, s_cur, s0, ez, w0, p0);
-            if (t.valid) {
-                st_out(outW, w0);
-                st_out(outP, p0);
-            }
-            outP += PS;
-            outW += PS;
-            __syncwarp();
-            if (zc >= N) {
-                if (threadIdx.x == 0) mbar_arrive(bars + 8u * (RG::D + rel.slot));
-                rel.template advance<RG::D>();
-            }
-            ++zc;
-            s_cur = slot_add<RG>(s_cur, 1);
-            vol_layer_step_z<N, TY, RG, F, C + 1>(p, t, ring, bars, ez, s0, outP, outW, s_cur, rel, zc);
-        }
-    }
-}
-
-// one layer: wait for its planes z0 .. z0 + N, then run them
-template <int N, int TY, class RG, int F>
-__device__ __forceinline__ void vol_layer_z(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
-                                            uint32_t bars, int ez, double*& outP, double*& outW, RingPos& lay,
-                                            RingPos& rel, int& zc) {
-    const int NZ = (int)p.NZ;
-    RingPos w = lay;
-#pragma unroll
-    for (int k = 0; k <= N; ++k) {
-        if (N * ez + k < NZ) mbar_wait(bars + 8u * w.slot, w.par);
-        w.template advance<RG::D>();
-    }
-    int s_cur = lay.slot;
-    vol_layer_step_z<N, TY, RG, F, 0>(p, t, ring, bars, ez, lay.slot, outP, outW, s_cur, rel, zc);
-#pragma unroll
-    for (int k = 0; k < N; ++k) lay.template advance<RG::D>();
-}
-
-template <int N, int TY, class RG>
-__device__ __forceinline__ void vol_run_z(const VolParams& p, const VolThread<N>& t, unsigned char* ring, uint32_t bars,
-                                          unsigned g0, double* outP, double* outW) {
-    const int nelz = p.nelz, NZ = (int)p.NZ;
-    RingPos lay = RingPos::at<RG::D>(g0), rel = RingPos::at<RG::D>(g0);
-    int zc = 0;
-    if (nelz == 1) {
-        vol_layer_z<N, TY, RG, kFirst | kLast>(p, t, ring, bars, 0, outP, outW, lay, rel, zc);
-    } else {
-        vol_layer_z<N, TY, RG, kFirst>(p, t, ring, bars, 0, outP, outW, lay, rel, zc);
-        for (int ez = 1; ez < nelz - 1; ++ez) vol_layer_z<N, TY, RG, 0>(p, t, ring, bars, ez, outP, outW, lay, rel, zc);
-        vol_layer_z<N, TY, RG, kLast>(p, t, ring, bars, nelz - 1, outP, outW, lay, rel, zc);
-    }
-    // the tile's last N planes
-    for (int z = NZ - N; z < NZ; ++z) {
-        if (z >= 0) {
-            __syncwarp();
-            if (threadIdx.x == 0) mbar_arrive(bars + 8u * (RG::D + rel.slot));
-            rel.template advance<RG::D>();
-        }
-    }
-}
-#endif
-
 // Consumer side of one tile (TXE x TY node column, all z): planes g0 .. g0 + NZ - 1 of the ring.
 template <int N, int TY, class RG>
 __device__ __forceinline__ void vol_tile(const VolParams& p, unsigned char* ring, uint32_t bars, int tx0, int ty0,
@@ -647,10 +399,6 @@ __device__ __forceinline__ void vol_tile(const VolParams& p, unsigned char* ring
     double* outP = p.Pn + off;
     double* outW = p.W + off;
 
-#if SEM_ZSMEM
-    vol_run_z<N, TY, RG>(p, t, ring, bars, g0, outP, outW);
-    return;
-#endif
     // ---- register window zw[k] = p(-N + k), k = 0..2N: planes 0..N from the ring
     double zw[2 * N + 1];
 #pragma unroll
