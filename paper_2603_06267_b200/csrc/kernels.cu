@@ -1165,7 +1165,10 @@ struct IfFused {
 };
 
 template <int NF, int NC, int R>
-__global__ void __launch_bounds__(256) iface_fused(const __grid_constant__ IfaceParams p) {
+#ifndef SEM_IF_THREADS
+#define SEM_IF_THREADS 512
+#endif
+__global__ void __launch_bounds__(SEM_IF_THREADS) iface_fused(const __grid_constant__ IfaceParams p) {
     using G = IfFused<NF, NC, R>;
     constexpr int NFR = G::NFR, FW = G::FW, CW = G::CW, CO = G::CO, TC = kIfTC;
     extern __shared__ double ifs[];
@@ -1326,7 +1329,7 @@ template <int NF, int NC, int R>
 static int launch_iface_fused(const IfaceParams& p, cudaStream_t s) {
     using G = IfFused<NF, NC, R>;
     const dim3 grid((unsigned)((p.nelcx + kIfTC - 1) / kIfTC), (unsigned)((p.nelcy + kIfTC - 1) / kIfTC));
-    iface_fused<NF, NC, R><<<grid, 256, G::SMEM, s>>>(p);
+    iface_fused<NF, NC, R><<<grid, SEM_IF_THREADS, G::SMEM, s>>>(p);
     return 1;
 }
 
