@@ -715,33 +715,41 @@ __global__ void __launch_bounds__(32 * kModalWarps) modal_kernel(const __grid_co
     const int k = blockIdx.x;
     const unsigned FULL = 0xffffffffu;
     const int M = p.n_modes;
-    const double dt = p.dt;
     const int i0 = p.rect[4 * k], j0 = p.rect[4 * k + 1], ni = p.rect[4 * k + 2], nj = p.rect[4 * k + 3];
-    const int L = p.lmax;
-    const double* sxk = p.sx + (size_t)k * M * L;
-    const double* syk = p.sy + (size_t)k * M * L;
-    const double* wxk = p.wx + (size_t)k * L;
-    const double* wyk = p.wy + (size_t)k * L;
+    const int L = p.lmax, nn = ni * nj;
     __shared__ double red[kModalWarps][kMaxModes];
     __shared__ double qv_s[kMaxModes];
-
-    // pressure projection G_m = sum_ij m_x(i) S_x(i) m_y(j) S_y(j) p_ij   (Eq. 12: int p U.n = -G)
+    // this PMUT's separable tables, staged once: sx[m][i], sy[m][j] and the face mass factors wx, wy
+    extern __shared__ double mtab[];
+    double* const tsx = mtab;
+    double* const tsy = tsx + M * L;
+    double* const twx = tsy + M * L;
+    double* const twy = twx + L;
+    {
+        const double* sxk = p.sx + (size_t)k * M * L;
+        const double* syk = p.sy + (size_t)k * M * L;
+        for (int q = threadIdx.x; q < M * L; q += blockDim.x) {
+            tsx[q] = __ldg(sxk + q);
+            tsy[q] = __ldg(syk + q);
+        }
+        for (int q = threadIdx.x; q < L; q += blockDim.x) {
+            twx[q] = __ldg(p.wx + (size_t)k * L + q);
+            twy[q] = __ldg(p.wy + (size_t)k * L + q);
+        }
+    }
+    __syncthreads();
+    // pressure projection G_m = sum_ij m_x(i) S_x(i) m_y(j) S_y(j) p_ij   (Eq. 12: int p U.n = -G); the
+    // membrane's nodes are spread over the block, several loads in flight per thread
     double acc[kMaxModes];
 #pragma unroll
     for (int m = 0; m < kMaxModes; ++m) acc[m] = 0.0;
-    for (int ib = 0; ib < ni; ib += 32) {
-        const int i = ib + lane;
-        const bool on = i < ni;
-        double bx[kMaxModes];
+#pragma unroll 4
+    for (int q = threadIdx.x; q < nn; q += blockDim.x) {
+        const int j = q / ni, i = q - j * ni;
+        const double val = p.P[(long long)(j0 + j) * p.PX + i0 + i] * twx[i] * twy[j];
 #pragma unroll
-        for (int m = 0; m < kMaxModes; ++m) bx[m] = (on && m < M) ? wxk[i] * sxk[m * L + i] : 0.0;
-        for (int j = warp; j < nj; j += kModalWarps) {
-            const double val = on ? p.P[(long long)(j0 + j) * p.PX + i0 + i] : 0.0;
-            const double wj = wyk[j];
-#pragma unroll
-            for (int m = 0; m < kMaxModes; ++m)
-                if (m < M) acc[m] = fma(bx[m] * val, wj * syk[m * L + j], acc[m]);
-        }
+        for (int m = 0; m < kMaxModes; ++m)
+            if (m < M) acc[m] = fma(tsx[m * L + i] * tsy[m * L + j], val, acc[m]);
     }
 #pragma unroll
     for (int m = 0; m < kMaxModes; ++m) {
@@ -759,18 +767,14 @@ __global__ void __launch_bounds__(32 * kModalWarps) modal_kernel(const __grid_co
 #pragma unroll
     for (int m = 0; m < kMaxModes; ++m) qv[m] = qv_s[m];
     // force plane F = kappa sum_m qdd_m S_m  (Eq. 11; the 1/M factor is applied in vol_kernel)
-    for (int j = warp; j < nj; j += kModalWarps) {
-        for (int ib = 0; ib < ni; ib += 32) {
-            const int i = ib + lane;
-            if (i < ni) {
-                double f = 0.0;
+    for (int q = threadIdx.x; q < nn; q += blockDim.x) {
+        const int j = q / ni, i = q - j * ni;
+        double f = 0.0;
 #pragma unroll
-                for (int m = 0; m < kMaxModes; ++m)
-                    if (m < M) f = fma(qv[m], sxk[m * L + i] * syk[m * L + j], f);
-                SEM_CHECK(i0 + i < p.NX);
-                p.F[(long long)(j0 + j) * p.NX + i0 + i] = p.kappa * f;
-            }
-        }
+        for (int m = 0; m < kMaxModes; ++m)
+            if (m < M) f = fma(qv[m], tsx[m * L + i] * tsy[m * L + j], f);
+        SEM_CHECK(i0 + i < p.NX);
+        p.F[(long long)(j0 + j) * p.NX + i0 + i] = p.kappa * f;
     }
 }
 
@@ -815,7 +819,7 @@ __global__ void __launch_bounds__(32 * kModalWarps) modal_table_kernel(const __g
 void launch_modal(const ModalParams& p, cudaStream_t s) {
     if (p.n_pmut <= 0) return;
     if (p.toff) modal_table_kernel<<<p.n_pmut, 32 * kModalWarps, 0, s>>>(p);
-    else modal_kernel<<<p.n_pmut, 32 * kModalWarps, 0, s>>>(p);
+    else modal_kernel<<<p.n_pmut, 32 * kModalWarps, (size_t)8 * (2 * p.n_modes * p.lmax + 2 * p.lmax), s>>>(p);
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -1019,7 +1019,9 @@ sem_status build_general_interface(sem_ctx* ctx, int fb, int cb, double gamma) {
     std::vector<long long> owner((size_t)nqp);
     std::vector<double> xim((size_t)3 * nqp);
     CU(cudaStreamSynchronize(ctx->stream));
-    const sem_status ms = sem_face_match(ctx->device, &fs, &cs, Nf, 1e-3, owner.data(), xim.data(), nullptr);
+    // normal filter |n+ + n-| < 0.25 (opposite up to ~14 degrees: a curved interface's matching faces
+    // need not have parallel centre normals; Newton containment decides)
+    const sem_status ms = sem_face_match(ctx->device, &fs, &cs, Nf, 0.25, owner.data(), xim.data(), nullptr);
     if (ms == SEM_E_UNMATCHED) return fail(ctx, SEM_E_UNMATCHED, "orphan interface quadrature point (Algorithm 3)");
     if (ms != SEM_OK) return fail(ctx, ms, "interface face matching failed");
     std::vector<double> xf, wf, xc, wc;
