@@ -159,3 +159,22 @@ def test_two_material_interface_random_state(ratio, nh):
         for k, v in compare(sim, nm).items():
             assert v < TOL, (n, k, v)
         sim.close()
+
+
+def test_state_rewrite_mid_run():
+    """The volume kernel hands the next step's interface its face traces; a state written between steps
+    (sem_write_state) invalidates them, and the next step reads the planes again."""
+    rec = conforming_cut_config(nel_xy=6, nz_lo=2, nz_hi=3, degree=5, degree_hi=3, ratio=2, h=25e-6, bc_top=1)
+    from paper_2603_06267_b200 import Simulation
+    sim = Simulation(rec)
+    for b, (p, v) in enumerate(random_state(rec, seed=22)):
+        sim.write_state(b, p, v)
+    sim.step(17)
+    st = random_state(rec, seed=23)
+    for b, (p, v) in enumerate(st):
+        sim.write_state(b, p, v)
+    sim.step(11)
+    nm = oracle_run(rec, 11, state=st)
+    for k, v in compare(sim, nm).items():
+        assert v < TOL, (k, v)
+    sim.close()
