@@ -161,7 +161,10 @@ sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, cons
  * quad_rule 1 = their (N+ + 1)^2 Gauss-Legendre points (R9's flag, Fig. 7's "LG" nodes):
  * the fine trace is interpolated to the points and the fine side's terms projected back onto the
  * fine face nodes; single slab only (world 1, no emulation: SEM_E_PARTITION otherwise).
- * Requires matching lateral extents and h_coarse = R h_fine for an integer R >= 1.
+ * Requires matching lateral extents; h_coarse = R h_fine for an integer R >= 1 gives the lattice kernel,
+ * otherwise (lattices that do not nest, e.g. 6 : 4 elements) both boxes move to the element-scatter
+ * path with their affine vertex lattices and take the general interface below (single slab, GLL rule,
+ * no PML / plane wave on them: SEM_E_UNMATCHED otherwise).
  * Curved boxes (sem_box_set_vertices / sem_box_set_obstacle on BOTH boxes, before this call): the
  * general non-conforming interface -- any trilinear face sets that tile the same surface, lattices that
  * need not nest.  Algorithm 3 (sem_face_match) gives every

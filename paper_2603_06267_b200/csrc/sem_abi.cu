@@ -947,6 +947,20 @@ sem_status setup_part_buffers(sem_ctx* ctx, sem::Part& pt) {
     return setup_exchange(ctx, pt);
 }
 
+// the affine vertex lattice of a structured box (element-scatter path without set vertices)
+void affine_lattice(Box& b, const sem_box_desc& g) {
+    const int nx = g.nel[0] + 1, ny = g.nel[1] + 1, nz = g.nel[2] + 1;
+    b.vlat_h.resize((size_t)3 * nx * ny * nz);
+    for (int k = 0; k < nz; ++k)
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i) {
+                const int ijk[3] = {i, j, k};
+                for (int d = 0; d < 3; ++d)
+                    b.vlat_h[3 * ((size_t)i + (size_t)nx * ((size_t)j + (size_t)ny * k)) + d] =
+                        g.origin[d] + g.extent[d] * ijk[d] / g.nel[d];
+            }
+}
+
 // host trilinear map of an element: J[i][j] = dX_i / dxi_j at xi (vertex v = i + 2j + 4k at reference
 // corner (2i-1, 2j-1, 2k-1))
 void trilinear_jacobian(const double* V, const double xi[3], double J[3][3]) {
@@ -1430,6 +1444,8 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
     return SEM_OK;
 }
 
+sem_status curved_setup(sem_ctx* ctx, Box& b, const sem_box_desc& g);   // below
+
 sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, double alpha, int quad_rule) {
     sem_status st = check_ctx(ctx);
     if (st) return st;
@@ -1474,8 +1490,33 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
     }
     if (std::fabs(gF.origin[2] + gF.extent[2] - gC.origin[2]) > tol)
         return fail(ctx, SEM_E_UNMATCHED, "boxes do not touch in z");
-    if (gF.nel[0] % gC.nel[0] || gF.nel[1] % gC.nel[1] || gF.nel[0] / gC.nel[0] != gF.nel[1] / gC.nel[1])
-        return fail(ctx, SEM_E_UNMATCHED, "fine lattice does not nest in the coarse one (need h_c = R h_f)");
+    if (gF.nel[0] % gC.nel[0] || gF.nel[1] % gC.nel[1] || gF.nel[0] / gC.nel[0] != gF.nel[1] / gC.nel[1]) {
+        // lattices that do not nest: both boxes move to the element-scatter path (their affine vertex
+        // lattices) and take the general interface (Algorithm 3 matching, section 5.2e of DESIGN.md)
+        sem::Part& pt0 = ctx->parts[0];
+        if (ctx->world > 1 || ctx->parts.size() != 1 || quad_rule != 0 ||
+            (pt0.pml.on && (pt0.pml.box == fine_box || pt0.pml.box == coarse_box)) ||
+            (ctx->pw.on && (ctx->pw.box == fine_box || ctx->pw.box == coarse_box)))
+            return fail(ctx, SEM_E_UNMATCHED,
+                        "fine lattice does not nest in the coarse one (need h_c = R h_f; the general interface of "
+                        "non-nested lattices is single-slab, GLL rule, without PML / plane wave on its boxes)");
+        for (int bi : {fine_box, coarse_box}) {
+            Box& b = pt0.boxes[bi];
+            if (b.curved) continue;
+            affine_lattice(b, ctx->gdesc[bi]);
+            st = curved_setup(ctx, b, ctx->gdesc[bi]);
+            if (st) return st;
+        }
+        const double cbar = 2.0 * gF.c * gC.c / (gF.c + gC.c);
+        const double hmin = std::min(std::min(std::min(hF[0], hF[1]), hF[2]), std::min(std::min(hC[0], hC[1]), hC[2]));
+        const int Nm = std::max(gF.degree, gC.degree);
+        st = build_general_interface(ctx, fine_box, coarse_box, alpha * cbar * cbar * Nm * Nm / hmin);
+        if (st) return st;
+        ctx->itf_on = true;
+        drop_graphs(ctx);
+        CU(cudaStreamSynchronize(ctx->stream));
+        return SEM_OK;
+    }
     const int R = gF.nel[0] / gC.nel[0];
     for (size_t r = 1; r + 1 < ctx->cuts.size(); ++r)   // (sem_mesh_create checked every box; restated here)
         if (cut_in_box(ctx->gdesc[0], gC, ctx->cuts[r]) < 0)
@@ -1720,18 +1761,7 @@ sem_status sem_box_set_obstacle(sem_ctx* ctx, int box, const unsigned char* soli
     size_t n_fluid = 0;
     for (size_t e = 0; e < n_el; ++e) n_fluid += solid[e] ? 0 : 1;
     if (n_fluid == 0) return fail(ctx, SEM_E_ARG, "every element is solid");
-    if (b.vlat_h.empty()) {   // affine box: its own vertex lattice
-        const int nx = g.nel[0] + 1, ny = g.nel[1] + 1, nz = g.nel[2] + 1;
-        b.vlat_h.resize((size_t)3 * nx * ny * nz);
-        for (int k = 0; k < nz; ++k)
-            for (int j = 0; j < ny; ++j)
-                for (int i = 0; i < nx; ++i) {
-                    const int ijk[3] = {i, j, k};
-                    for (int d = 0; d < 3; ++d)
-                        b.vlat_h[3 * ((size_t)i + (size_t)nx * ((size_t)j + (size_t)ny * k)) + d] =
-                            g.origin[d] + g.extent[d] * ijk[d] / g.nel[d];
-                }
-    }
+    if (b.vlat_h.empty()) affine_lattice(b, g);   // affine box: its own vertex lattice
     b.solid_h.assign(solid, solid + n_el);
     for (auto& v : b.solid_h) v = v ? 1 : 0;
     st = curved_setup(ctx, b, g);

@@ -423,7 +423,7 @@ def obstacle_pmut_config(n_cycles=1, n_steps=2160, with_obstacle=True):
 
 def curved_interface_config(nf=(6, 6, 2), nc=(4, 4, 2), degree_f=4, degree_c=3, hf=25e-6, jitter=0.15, seed=0,
                             bc_top=BC_RIGID, c_f=C_WATER, c_c=C_WATER, alpha=PENALTY_ALPHA, n_steps=100, cfl=0.25,
-                            coarse_height=75e-6, nested_jitter=False):
+                            coarse_height=75e-6, nested_jitter=False, pmut=False):
     """Two curved (vertex-lattice) boxes stacked in z, joined by a general non-conforming DG interface
     (the interface quadrature of P:L912-938 with Algorithm 3's matching,
     P:L1062-1080, on trilinear faces).  The fine box has nf elements of degree degree_f and edge hf, the
@@ -433,7 +433,7 @@ def curved_interface_config(nf=(6, 6, 2), nc=(4, 4, 2), degree_f=4, degree_c=3, 
     tile the same plane without matching; every other vertex stays on the affine lattice.  With
     nested_jitter (nf a multiple of nc) only the coarse vertices are drawn and the fine interface
     vertices are the coarse faces' bilinear maps at the sub-lattice points: curved faces that nest.  Faces rigid
-    except the coarse top (bc_top)."""
+    except the coarse top (bc_top).  pmut: one config-0 membrane (TX) centred on the fine box's floor."""
     rng = np.random.default_rng(seed)
     L = nf[0] * hf
     hc = L / nc[0]
@@ -470,6 +470,8 @@ def curved_interface_config(nf=(6, 6, 2), nc=(4, 4, 2), degree_f=4, degree_c=3, 
         fine["vertices"] = fv.reshape(-1, 3)
     rec = {"name": "curved_iface", "boxes": [fine, coarse], "n_steps": n_steps, "seed": seed,
            "interface": {"fine_box": 0, "coarse_box": 1, "alpha": alpha}}
+    if pmut:   # one config-0 membrane centred on the fine box's floor (TX burst)
+        rec["pmut"] = _pmut([[L / 2, L / 2]], MODES_3, FREQS_3, None, [0.0])
     rec["dt"] = cfl_dt(rec["boxes"], cfl)
     return _finish(rec)
 

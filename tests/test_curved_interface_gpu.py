@@ -64,3 +64,32 @@ def test_general_interface_pulse_long_run():
     assert np.abs(nm.sys.split(nm.p)[1]).max() > 1e-3      # the pulse crossed the interface
     for k, v in compare(sim, nm).items():
         assert v < TOL, (k, v)
+
+
+def _structured(rec):
+    """The same boxes without vertex lattices: structured boxes whose lattices do not nest (6 : 4) --
+    sem_dg_interface_build moves them to the element-scatter path and the general interface."""
+    for b in rec["boxes"]:
+        b.pop("vertices", None)
+    return rec
+
+
+def test_non_nested_structured_boxes_random_state():
+    rec = _structured(curved_interface_config(jitter=0.0, seed=3))
+    st = random_state(rec, seed=17)
+    for n in (1, 4, 25):
+        nm = oracle_run(rec, n, state=st)
+        sim = gpu_run(rec, n, state=st)
+        for k, v in compare(sim, nm).items():
+            assert v < TOL, (n, k, v)
+        sim.close()
+
+
+def test_non_nested_structured_boxes_with_pmut():
+    """A PMUT transmitting on the fine box of a non-nested (6 : 4) two-box mesh, 300 steps."""
+    rec = _structured(curved_interface_config(jitter=0.0, pmut=True, bc_top=BC_ABSORBING))
+    nm = oracle_run(rec, 300)
+    sim = gpu_run(rec, 300)
+    assert np.abs(nm.q).max() > 1e-13 and np.abs(nm.sys.split(nm.p)[1]).max() > 1e-3
+    for k, v in compare(sim, nm).items():
+        assert v < TOL, (k, v)

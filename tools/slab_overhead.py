@@ -13,10 +13,13 @@ from paper_2603_06267_b200 import SEM_F_EMULATE_SLABS, SEM_F_NO_GRAPH, Simulatio
 from sem_inputs import config  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-rec = config(3)
-out = {"what": "cfg3 y-slab decomposition emulated on one GPU", "steps": steps}
+ci = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+rec = config(ci)
+from paper_2603_06267_b200.sem import sem_slab_plan  # noqa: E402
+out = {"what": f"cfg{ci} y-slab decomposition emulated on one GPU", "steps": steps}
 base = None
 for G in (1, 2, 4, 8):
+    out.setdefault("plans", {})[f"G{G}"] = sem_slab_plan(rec["boxes"], G, rec.get("pmut"))
     flags = SEM_F_EMULATE_SLABS if G > 1 else 0
     sim = Simulation(rec, world=G, flags=flags)
     sim.step(3)
