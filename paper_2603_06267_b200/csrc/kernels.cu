@@ -790,7 +790,9 @@ __global__ void __launch_bounds__(32 * kModalWarps) modal_table_kernel(const __g
     double acc[kMaxModes];
 #pragma unroll
     for (int m = 0; m < kMaxModes; ++m) acc[m] = 0.0;
+    SEM_CHECK(j0 >= 0 && j1 >= j0);
     for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+        SEM_CHECK(p.tidx[j] >= 0 && p.tidx[j] < p.PX * p.NY_dbg);
         const double v = p.P[p.tidx[j]];
 #pragma unroll
         for (int m = 0; m < kMaxModes; ++m)
@@ -1250,6 +1252,7 @@ __global__ void __launch_bounds__(SEM_IF_THREADS) iface_fused(const __grid_const
             const bool own = ix >= ox && (ix < ox + TC * NFR || ix == NXf - 1) && iy >= oy &&
                              (iy < oy + TC * NFR || iy == NYf - 1);
             if (own) {
+                SEM_CHECK(ix < NXf && iy < NYf);
                 p.tauf[iy * NXf + ix] = tau;
                 p.sigf[iy * NXf + ix] = sig;
             }
@@ -1323,6 +1326,7 @@ __global__ void __launch_bounds__(SEM_IF_THREADS) iface_fused(const __grid_const
                 s2 = fma(w, h2[jr * FW + (el - 1) * NFR + q], s2);
             }
         }
+        SEM_CHECK(jx >= 0 && jx < NXc && jy >= 0 && jy < NYc);
         const double inv = 1.0 / (__ldg(p.mxc + jx) * __ldg(p.myc + jy));
         p.tauc[jy * NXc + jx] = s1 * inv;
         p.sigc[jy * NXc + jx] = s2 * inv;
@@ -1623,6 +1627,7 @@ __global__ void __launch_bounds__(256) pml_fixup_rows_kernel(const __grid_consta
     for (long long sg = wid; sg < p.n_seg; sg += nw) {
         const long long g0 = p.seg_start[sg];
         const int len = p.seg_len[sg];
+        SEM_CHECK(g0 >= 0 && len > 0 && len <= p.NX && g0 + len <= p.PX * p.NY * p.NZ);
         for (int i = lane; i < len; i += 32) {
             const long long g = g0 + i;
             const double v = p.da[g];
@@ -1940,6 +1945,7 @@ __global__ void __launch_bounds__(128) iface_general_kernel(const __grid_constan
     const int q = (int)(qp % (q1 * q1)), a = q % q1, b = q / q1;
     const long long SF = p.PXf * p.NYf, SC = p.PXc * p.NYc;
     const long long fb = p.fbase[qp] + a + b * p.PXf + Nf * SF;   // fine node (a, b, Nf)
+    SEM_CHECK(p.fbase[qp] >= 0 && fb < SF * (p.NZf_dbg > 0 ? p.NZf_dbg : 1) && p.cbase[qp] >= 0);
     const double pp = __ldg(p.Pf + fb);
     double dxi = 0.0, deta = 0.0, dzeta = 0.0;
     for (int j = 0; j <= Nf; ++j) {

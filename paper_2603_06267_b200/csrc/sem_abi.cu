@@ -540,6 +540,7 @@ sem::ModalParams modal_params(sem_ctx* ctx, sem::Part& pt, int cur) {
         p.tidx = pm.tidx;
         p.tB = pm.tB;
         p.res = b.res;
+        p.NY_dbg = b.NY;
     }
     return p;
 }
@@ -1105,6 +1106,7 @@ sem_status build_general_interface(sem_ctx* ctx, int fb, int cb, double gamma) {
     for (int i = 0; i <= Nf; ++i)
         for (int j = 0; j <= Nf; ++j) g.Df[i][j] = Df[(size_t)i * q1 + j];
     g.gamma = gamma;
+    g.NZf_dbg = F.NZ;
     g.cf2 = gF.c * gF.c;
     g.cc2 = gC.c * gC.c;
     pt.itf.general = true;

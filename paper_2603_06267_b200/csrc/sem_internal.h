@@ -162,6 +162,7 @@ struct ModalParams {
     const long long* __restrict__ tidx;
     const double* __restrict__ tB;
     double* res;
+    long long NY_dbg;                   // node rows of the PMUT box (debug-build bounds checks)
 };
 
 struct IfaceParams {
@@ -276,6 +277,7 @@ struct GIfaceParams {
     const double* __restrict__ bas;         // [nqp][6][Nc+1]: l, l' of the coarse basis at x_hat^- per axis
     double Df[kMaxN + 1][kMaxN + 1];        // fine GLL differentiation matrix D[i][j] = l_j'(x_i)
     double gamma, cf2, cc2;
+    long long NZf_dbg;                      // fine box node count along z (debug-build bounds checks)
 };
 
 // One side of one slab cut for one box (partial rows before, fix-up after the exchange).
