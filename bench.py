@@ -32,7 +32,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "acoustic GDOF-updates/s per leapfrog step (FP64)"
 UNIT = "GDOF/s"
-BYTES_PER_DOF = 32.0          # algorithmic: read p, w; write p, w (FP64) -- DESIGN.md "Byte budget"
+BYTES_PER_DOF = 32.0          # SURVEY 8(d)'s algorithmic bytes: read p, w; write p, w (FP64) -- the roofline's unit
+KERNEL_BYTES_PER_DOF = 24.0   # what the two-level volume kernel moves: read p^{n+1}, p^n; write p^{n+2} (DESIGN 1)
 
 
 def _peaks():
@@ -356,6 +357,12 @@ def main():
                      "bytes_per_step_algorithmic": BYTES_PER_DOF * ndof_total,
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                      "frac_spec_8tbs": achieved / SPEC_HBM_GBS,
+                     "bytes_per_dof_algorithmic": BYTES_PER_DOF,
+                     "bytes_per_dof_kernel": KERNEL_BYTES_PER_DOF,
+                     "frac_kernel_bytes": achieved * KERNEL_BYTES_PER_DOF / BYTES_PER_DOF / peak,
+                     "bytes_note": "achieved uses SURVEY 8(d)'s 32 B/DOF (read p, w; write p, w); the two-level "
+                                   "kernel recomputes w = (p^{n+1} - p^n)/dt and moves 24 B/DOF, so its own "
+                                   "bandwidth fraction is frac_kernel_bytes (DESIGN.md section 1)",
                      "step_frac": BYTES_PER_DOF * ndof_total / world / (ms_step / 1e3) / 1e9 / peak,
                      "share_of_step": vol_ms / ms_prof if ms_prof > 0 else None,
                      "timing": "kernel times from a separate profiling pass of the same K steps (direct "

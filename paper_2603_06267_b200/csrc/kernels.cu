@@ -210,8 +210,12 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
     }
     acc = fma(p.sdir[2], z0 + z1, acc);
     double a = -acc;
-    const double wv = sW[t.wown];
     const double pv = zw[N + C];
+#if SEM_TWO_LEVEL   // w^n = (p^{n+1} - p^n) / dt from the p^n tile
+    const double wv = (pv - sW[t.wown]) * p.inv_dt;
+#else
+    const double wv = sW[t.wown];
+#endif
     double damp = t.dxy;
     if constexpr ((F & kFirst) && C == 0) {      // z = 0 face: ABC and PMUT forcing (Eq. 11)
         damp += p.damp[4];
@@ -280,9 +284,9 @@ __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThre
             vol_plane<N, TY, C + 1, F>(p, t, reinterpret_cast<const double*>(s1),
                                        reinterpret_cast<const double*>(s1 + G::POFF), zw, ez, w1, p1);
             if (t.valid) {
-                st_out(outW, w0);
+                if (!SEM_TWO_LEVEL) st_out(outW, w0);
                 st_out(outP, p0);
-                st_out(outW + PS, w1);
+                if (!SEM_TWO_LEVEL) st_out(outW + PS, w1);
                 st_out(outP + PS, p1);
             }
             outP += 2 * PS;
@@ -301,7 +305,7 @@ __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThre
             vol_plane<N, TY, C, F>(p, t, reinterpret_cast<const double*>(s0),
                                    reinterpret_cast<const double*>(s0 + G::POFF), zw, ez, w0, p0);
             if (t.valid) {
-                st_out(outW, w0);
+                if (!SEM_TWO_LEVEL) st_out(outW, w0);
                 st_out(outP, p0);
             }
             outP += PS;
@@ -1452,7 +1456,7 @@ __global__ void cut_fixup_kernel(const __grid_constant__ CutBatch B) {
     if (c.pda) da += c.in[n + 2 * c.NXt + i];   // the neighbour's PML acceleration
     const long long d = (iz * c.NY + (c.side ? c.NY - 1 : 0)) * c.PX + ix;
     const double dw = c.dt * da;
-    c.W[d] += dw;
+    if (!SEM_TWO_LEVEL) c.W[d] += dw;
     c.Pn[d] = fma(c.dt, dw, c.Pn[d]);
 }
 
@@ -1527,7 +1531,11 @@ __global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1), pm
     //  element owns them: the exchanged PML accelerations then count them once)
     const bool own = (a < N || ex == p.nelx - 1) && (b < N || ey == p.nely - 1) && (c < N || ez == p.nelz - 1) &&
                      !(p.cutL && gy == 0);
+#if SEM_TWO_LEVEL   // predictor velocity w^n = (p^{n+1} - p^n) / dt (p^n still in Pn before the volume kernel)
+    const double wv = own ? (pv - p.Pn[g]) * p.inv_dt : 0.0;
+#else
     const double wv = own ? p.W[g] : 0.0;
+#endif
     double* ph = p.phi + (size_t)k * 3 * nl;
     const double phold[3] = {ph[t], ph[nl + t], ph[2 * nl + t]};
     const double* __restrict__ Tx = p.tx + 4 * gx;
@@ -1602,7 +1610,7 @@ __global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1)) pm
     if (bits) {
         const double v = __longlong_as_double((long long)bits);
         const double dw = p.dt * v;
-        p.Wn[g] += dw;
+        if (!SEM_TWO_LEVEL) p.Wn[g] += dw;
         p.Pn[g] = fma(p.dt, dw, p.Pn[g]);
     }
 }
@@ -1633,7 +1641,7 @@ __global__ void __launch_bounds__(256) pml_fixup_rows_kernel(const __grid_consta
             const double v = p.da[g];
             if (v != 0.0) {
                 const double dw = p.dt * v;
-                p.Wn[g] += dw;
+                if (!SEM_TWO_LEVEL) p.Wn[g] += dw;
                 p.Pn[g] = fma(p.dt, dw, p.Pn[g]);
                 p.da[g] = 0.0;
             }

@@ -452,7 +452,7 @@ sem::VolParams vol_params(sem_ctx* ctx, sem::Part& pt, int bi, int cur) {
     Box& b = pt.boxes[bi];
     sem::VolParams p{};
     p.tmP = b.tmP[cur];
-    p.tmW = b.tmW;
+    p.tmW = SEM_TWO_LEVEL ? b.tmPw[1 - cur] : b.tmW;   // two-level: the p^n tile instead of w^n
     p.tab = b.tab;
     p.Pn = b.P[1 - cur];
     p.W = b.W;
@@ -464,6 +464,7 @@ sem::VolParams vol_params(sem_ctx* ctx, sem::Part& pt, int bi, int cur) {
     for (int d = 0; d < 3; ++d) p.sdir[d] = b.d.c * b.d.c * (2.0 / b.h[d]) * (2.0 / b.h[d]);
     p.nelz = b.d.nel[2];
     p.dt = ctx->dt;
+    p.inv_dt = 1.0 / ctx->dt;
     std::vector<double> x, w;
     gll_rule(b.N, x, w);
     for (int f = 0; f < 6; ++f) {
@@ -656,6 +657,7 @@ sem::PmlParams pml_params(sem_ctx* ctx, sem::Part& pt, int cur) {
     p.jac = 0.125 * b.h[0] * b.h[1] * b.h[2];
     p.c2 = b.d.c * b.d.c;
     p.dt = ctx->dt;
+    p.inv_dt = 1.0 / ctx->dt;
     p.cutL = b.cutL ? 1 : 0;
     p.seg_start = m.seg_start;
     p.seg_len = m.seg_len;
@@ -942,7 +944,9 @@ sem_status setup_part_buffers(sem_ctx* ctx, sem::Part& pt) {
         const int TY = sem::volume_tile_y();
         if (!make_map(&b.tmP[0], b.P[0], b, sem::vol_pbox_w(b.N), TY + 2 * b.N) ||
             !make_map(&b.tmP[1], b.P[1], b, sem::vol_pbox_w(b.N), TY + 2 * b.N) ||
-            !make_map(&b.tmW, b.W, b, sem::vol_wbox_w(b.N), TY))
+            !make_map(&b.tmW, b.W, b, sem::vol_wbox_w(b.N), TY) ||
+            !make_map(&b.tmPw[0], b.P[0], b, sem::vol_wbox_w(b.N), TY) ||
+            !make_map(&b.tmPw[1], b.P[1], b, sem::vol_wbox_w(b.N), TY))
             return fail(ctx, SEM_E_CUDA, "cuTensorMapEncodeTiled failed");
     }
     return setup_exchange(ctx, pt);

@@ -28,6 +28,14 @@
 
 namespace sem {
 
+// Two-level time stepping of the structured volume kernel: the state is p^{n+1},
+// p^n; the half-step velocity w^n = (p^{n+1} - p^n) / dt is recomputed per node instead of stored, so a
+// step reads p^{n+1} (with the stencil halo) and p^n and writes p^{n+2} over p^n: 24 B per DOF-step
+// instead of 32 (p, w read and written).  Curved / obstacle boxes keep the stored w.
+#ifndef SEM_TWO_LEVEL
+#define SEM_TWO_LEVEL 1
+#endif
+
 constexpr int kMaxN = 8;          // supported GLL degrees 1..8
 constexpr int kRows = kMaxN + 3;  // row classes per direction: R[0..N-1], L, B0, BN
 constexpr int kMaxModes = 8;
@@ -84,7 +92,7 @@ struct BoxTables {
 
 struct VolParams {
     CUtensorMap tmP;                // TMA map of p^{n+1} (3D: NX, NY, NZ; row pitch PX)
-    CUtensorMap tmW;                // TMA map of w^n
+    CUtensorMap tmW;                // TMA map of w^n (two-level: of p^n, the same box shape)
     BoxTables tab;
     double* __restrict__ Pn;        // p^{n+2} (output)
     double* __restrict__ W;         // w^n in, w^{n+1} out (in place)
@@ -94,6 +102,7 @@ struct VolParams {
     double sdir[3];                 // s_d = c^2 (2/h_d)^2: scale of the compile-time reference rows
     int nelz;
     double dt;
+    double inv_dt;
     // lumped ABC: C_ii / M_ii at boundary nodes of absorbing faces (0 if rigid)
     double damp[6];
     // PMUT forcing plane on z = 0 (F = kappa sum_m qdd S), scaled by kF = 1 / m_z(0)
@@ -225,7 +234,7 @@ struct PmlParams {
     double w[kMaxN + 1];                // GLL weights
     double s2h[3];                      // 2 / h_d
     double jac;                         // |J| = h_x h_y h_z / 8
-    double c2, dt;
+    double c2, dt, inv_dt;
     int cutL;                           // y-slab with a lower cut (multi-GPU): its row 0 is the cut plane
     // the PML region (nodes of PML elements) as contiguous lattice-row segments [start, start + len)
     // of the pitched layout, each node once (the fix-up sweeps them coalesced, no atomics)
@@ -315,6 +324,7 @@ struct Box {
     long long PX = 0;       // device row pitch (doubles): NX rounded up to 8 (TMA needs 16 B strides)
     double h[3] = {0, 0, 0};
     CUtensorMap tmP[2], tmW;
+    CUtensorMap tmPw[2];            // p levels with the W tile's box shape (two-level: p^n tile)
     double* P[2] = {nullptr, nullptr};
     double* W = nullptr;
     double* xc = nullptr;
