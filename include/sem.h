@@ -101,11 +101,14 @@ typedef struct {
 
 /* Create the context: validates boxes, builds the 1D GLL tables and allocates p (two time
  * levels), w = p' + dt/2 p'' (one level) per box (this rank's y-slab), zero-initialised
- * (P:L609-610).  With world > 1 (and no SEM_F_EMULATE_SLABS) every rank calls it with the same
- * global boxes and the ncclUniqueId from sem_nccl_unique_id on rank 0; each step then exchanges
- * one cut plane per box with each y-neighbour.
- * Errors: SEM_E_ARG (bad descriptor), SEM_E_PARTITION (nel_y not divisible by world),
- * SEM_E_NCCL, SEM_E_CUDA / SEM_E_OOM.  *out is NULL on error. */
+ * (P:L609-610).  The structured step keeps only the two p levels current (w^n = (p^{n+1} - p^n)/dt
+ * is recomputed); w serves the element-scatter boxes.  With world > 1 (and no
+ * SEM_F_EMULATE_SLABS) every rank calls it with the same global boxes, the same slab plan and the
+ * ncclUniqueId from sem_nccl_unique_id on rank 0; each step then exchanges one cut plane per box with
+ * each y-neighbour.
+ * Errors: SEM_E_ARG (bad descriptor), SEM_E_PARTITION (no slab_y0 and nel_y not divisible by world,
+ * or a slab_y0 cut that is not an element boundary of every box), SEM_E_NCCL, SEM_E_CUDA /
+ * SEM_E_OOM.  *out is NULL on error. */
 sem_status sem_mesh_create(const sem_mesh_desc* desc, sem_ctx** out);
 
 /* 128-byte ncclUniqueId for world > 1 (rank 0 calls it and broadcasts the bytes).
@@ -214,9 +217,11 @@ sem_status sem_box_set_obstacle(sem_ctx* ctx, int box, const unsigned char* soli
  * boundary condition (the paper's Gamma_ABC behind the layer: tag them SEM_BC_ABSORBING).
  * Discretisation (readings R23-R25): psi continuous nodal, Phi element-local, div Phi in weak
  * form, psi/Phi at half steps (Crank-Nicolson on Z1), PML terms at the predictor velocity.
- * Caller owns `thickness` (copied).  Single slab only (world 1, no emulation): SEM_E_PARTITION
- * otherwise.  Errors: SEM_E_ARG (negative thickness, overlapping layers, R outside (0, 1)),
- * SEM_E_STATE (already attached), SEM_E_OOM.  Resets the dynamic state like sem_pmut_attach. */
+ * Under y-slabs (world > 1, NCCL or emulated) the profiles come from the global box and the PML
+ * accelerations of the cut-plane nodes travel with the cut exchange (reading R31).
+ * Caller owns `thickness` (copied).  Errors: SEM_E_ARG (negative thickness, overlapping layers, R
+ * outside (0, 1)), SEM_E_STATE (already attached, curved box), SEM_E_OOM.  Resets the dynamic state
+ * like sem_pmut_attach. */
 sem_status sem_pml_attach(sem_ctx* ctx, int box, const double* thickness, double R);
 
 /* Algorithm 3 (face matching on the non-conforming interface) on GPU `device`: for every
