@@ -1901,7 +1901,14 @@ __global__ void __launch_bounds__(256, 8) curved_update_kernel(const __grid_cons
 #pragma unroll 1
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
         // read-only (non-coherent) loads: each element is read once, before this thread overwrites it
+#if SEM_TWO_LEVEL   // w^n = (p^{n+1} - p^n) / dt; p^n is read here and overwritten by p^{n+2} below
+        const double2 mi = __ldg(M2 + i), cd = __ldg(C2 + i), pv = __ldg(P2 + i);
+        const double2 po = reinterpret_cast<const double2*>(p.Pn)[i];
+        const double2 wv = make_double2((pv.x - po.x) * p.inv_dt, (pv.y - po.y) * p.inv_dt);
+        (void)W2;
+#else
         const double2 wv = __ldg(W2 + i), mi = __ldg(M2 + i), cd = __ldg(C2 + i), pv = __ldg(P2 + i);
+#endif
         double2 r = __ldg(R2 + i);
         if (p.F && 2 * i < p.PX * p.NY) {   // z = 0 plane: PMUT forcing f = kappa B^T qdd (Eq. 11)
             const long long d = 2 * i, ix = d % p.PX, iy = d / p.PX;   // PX even: both nodes on one row
@@ -1917,7 +1924,7 @@ __global__ void __launch_bounds__(256, 8) curved_update_kernel(const __grid_cons
         if (mi.x == 0.0) wn.x = pn.x = 0.0;
         if (mi.y == 0.0) wn.y = pn.y = 0.0;
         reinterpret_cast<double2*>(p.res)[i] = make_double2(0.0, 0.0);
-        reinterpret_cast<double2*>(p.W)[i] = wn;
+        if (!SEM_TWO_LEVEL) reinterpret_cast<double2*>(p.W)[i] = wn;
         reinterpret_cast<double2*>(p.Pn)[i] = pn;
     }
 }

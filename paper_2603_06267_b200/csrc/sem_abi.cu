@@ -608,6 +608,7 @@ sem::CurvedParams curved_params(sem_ctx* ctx, sem::Part& pt, int bi, int cur) {
     }
     p.c2 = b.d.c * b.d.c;
     p.dt = ctx->dt;
+    p.inv_dt = 1.0 / ctx->dt;
     if (pt.pm.on && pt.pm.box == bi && !pt.pm.toff) {   // affine obstacle box: separable coupling
         p.F = pt.pm.F;
         p.fmx = b.mx;

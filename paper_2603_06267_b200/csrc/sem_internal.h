@@ -31,7 +31,8 @@ namespace sem {
 // Two-level time stepping of the structured volume kernel: the state is p^{n+1},
 // p^n; the half-step velocity w^n = (p^{n+1} - p^n) / dt is recomputed per node instead of stored, so a
 // step reads p^{n+1} (with the stencil halo) and p^n and writes p^{n+2} over p^n: 24 B per DOF-step
-// instead of 32 (p, w read and written).  Curved / obstacle boxes keep the stored w.
+// instead of 32 (p, w read and written).  The element-scatter (curved / obstacle) update does the same
+// (56 instead of 64 B per node).
 #ifndef SEM_TWO_LEVEL
 #define SEM_TWO_LEVEL 1
 #endif
@@ -260,7 +261,7 @@ struct CurvedParams {
     const double* __restrict__ cdamp;
     double D[kMaxN + 1][kMaxN + 1];  // D[i][j] = l_j'(x_i)
     double x[kMaxN + 1], w[kMaxN + 1];
-    double c2, dt;
+    double c2, dt, inv_dt;
     // PMUT forcing on the z = 0 face of an affine element-scatter (obstacle) box: the update subtracts
     // F m_x m_y (F = kappa sum_m qdd S, face weights m_x m_y) from the residual of the face nodes
     const double* __restrict__ F;    // [NY][NX] or nullptr
