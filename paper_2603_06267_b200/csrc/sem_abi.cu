@@ -1165,25 +1165,37 @@ sem_status pmut_tables(sem_ctx* ctx, sem::Part& pt, Box& b, const sem_pmut_desc&
     std::vector<double> B;
     std::vector<int> used((size_t)b.NX * b.NY, -1);
     const double a = pd.side;
+    // candidate nodes of a membrane: its square on the affine lattice widened by two elements (a vertex
+    // lattice moves the nodes by less than an element)
+    const double hx = g.extent[0] / g.nel[0], hy = g.extent[1] / g.nel[1];
+    auto lat_range = [](double lo, double hi, double org, double h, int N, long long n, long long& i0, long long& i1) {
+        i0 = std::max<long long>(0, (long long)std::floor((lo - org) / h - 2.0) * N);
+        i1 = std::min<long long>(n - 1, (long long)std::ceil((hi - org) / h + 2.0) * N);
+    };
     for (int l = 0; l < KL; ++l) {
         const int k = ks[l];
         const double x0 = pd.center[2 * k] - 0.5 * a, y0 = pd.center[2 * k + 1] - 0.5 * a;
-        for (size_t j = 0; j < fw.size(); ++j) {
-            const double xl = fx[j] - x0, yl = fy[j] - y0;
-            if (!(xl >= 0 && xl <= a && yl >= 0 && yl <= a)) continue;
-            std::vector<double> row(M);
-            bool nz = false;
-            for (int m = 0; m < M; ++m) {
-                const double S = std::sin(pd.mode_mn[2 * m] * M_PI * xl / a) * std::sin(pd.mode_mn[2 * m + 1] * M_PI * yl / a);
-                row[m] = fw[j] * S;
-                nz = nz || S != 0.0;
+        long long ix0, ix1, iy0, iy1;
+        lat_range(x0, x0 + a, g.origin[0], hx, N, b.NX, ix0, ix1);
+        lat_range(y0, y0 + a, g.origin[1], hy, N, b.NY, iy0, iy1);
+        for (long long jy = iy0; jy <= iy1; ++jy)
+            for (long long jx = ix0; jx <= ix1; ++jx) {
+                const size_t j = (size_t)jy * b.NX + (size_t)jx;
+                const double xl = fx[j] - x0, yl = fy[j] - y0;
+                if (!(xl >= 0 && xl <= a && yl >= 0 && yl <= a)) continue;
+                std::vector<double> row(M);
+                bool nz = false;
+                for (int m = 0; m < M; ++m) {
+                    const double S = std::sin(pd.mode_mn[2 * m] * M_PI * xl / a) * std::sin(pd.mode_mn[2 * m + 1] * M_PI * yl / a);
+                    row[m] = fw[j] * S;
+                    nz = nz || S != 0.0;
+                }
+                if (!nz) continue;
+                if (used[j] >= 0) return fail(ctx, SEM_E_ARG, "membranes overlap");
+                used[j] = l;
+                idx.push_back((long long)(j / b.NX) * b.PX + (long long)(j % b.NX));   // pitched, plane z = 0
+                B.insert(B.end(), row.begin(), row.end());
             }
-            if (!nz) continue;
-            if (used[j] >= 0) return fail(ctx, SEM_E_ARG, "membranes overlap");
-            used[j] = l;
-            idx.push_back((long long)(j / b.NX) * b.PX + (long long)(j % b.NX));   // pitched, plane z = 0
-            B.insert(B.end(), row.begin(), row.end());
-        }
         off[l + 1] = (int)idx.size();
         if (off[l + 1] == off[l]) return fail(ctx, SEM_E_ARG, "membrane with no face node");
     }
