@@ -2051,12 +2051,21 @@ sem_status sem_read_pressure(sem_ctx* ctx, int box, double* host, size_t n) {
         return SEM_OK;
     }
     CU(copy_slab(host, mine.P[1 - ctx->cur], mine, NYg, mine.gy0, 0, true, ctx->stream));
-    double* tmp = nullptr;
-    CU(cudaMallocAsync(&tmp, (size_t)mine.nalloc() * 8, ctx->stream));
+    // the other ranks' slabs (the plan may be uneven): their geometry from the plan, largest buffer once
+    const sem_box_desc& g = ctx->gdesc[box];
+    std::vector<Box> slabs;
+    size_t most = 0;
     for (int r = 1; r < ctx->world; ++r) {
-        const long long gy0 = (mine.NY - 1) * (long long)r;   // equal slabs
-        NC(api.recv(tmp, (size_t)mine.nalloc(), kNcclDouble, r, ctx->nccl, ctx->stream));
-        CU(copy_slab(host, tmp, mine, NYg, gy0, 1, true, ctx->stream));
+        const long long e0 = cut_in_box(ctx->gdesc[0], g, ctx->cuts[r]), e1 = cut_in_box(ctx->gdesc[0], g, ctx->cuts[r + 1]);
+        slabs.push_back(make_slab(g, e0, e1 - e0, true, r < ctx->world - 1));
+        most = std::max(most, (size_t)slabs.back().nalloc());
+    }
+    double* tmp = nullptr;
+    CU(cudaMallocAsync(&tmp, most * 8, ctx->stream));
+    for (int r = 1; r < ctx->world; ++r) {
+        const Box& rb = slabs[r - 1];
+        NC(api.recv(tmp, (size_t)rb.nalloc(), kNcclDouble, r, ctx->nccl, ctx->stream));
+        CU(copy_slab(host, tmp, rb, NYg, rb.gy0, 1, true, ctx->stream));
     }
     CU(cudaFreeAsync(tmp, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));

@@ -31,12 +31,11 @@ def _rank_main(rank, world, port, out_dir, name, graph):
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     from paper_2603_06267_b200 import SEM_F_NO_GRAPH, Simulation
     from paper_2603_06267_b200.sem import sem_nccl_unique_id
-    from sem_inputs import small_config
     idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
     if rank == 0:
         idt.copy_(torch.frombuffer(bytearray(sem_nccl_unique_id()), dtype=torch.uint8))
     dist.broadcast(idt, 0)
-    rec = small_config(name)
+    rec = _record(name)
     sim = Simulation(rec, device=rank, rank=rank, world=world, nccl_unique_id=bytes(idt.cpu().numpy().tobytes()),
                      flags=0 if graph else SEM_F_NO_GRAPH)
     sim.step(STEPS)
@@ -48,20 +47,24 @@ def _rank_main(rank, world, port, out_dir, name, graph):
     dist.destroy_process_group()
 
 
+def _record(name):
+    from sem_inputs import config, small_config
+    return config(0) if name == "cfg0" else small_config(name)
+
+
 @pytest.mark.parametrize("graph", [True, False])
-@pytest.mark.parametrize("name", ["cfg2s", "cfg4s"])
+@pytest.mark.parametrize("name", ["cfg2s", "cfg4s", "cfg0"])   # cfg0: an uneven plan [0, 1, 4] (R30)
 def test_nccl_two_ranks_bitwise_equals_emulation(tmp_path, name, graph):
     _need_two()
     import torch.multiprocessing as mp
     from paper_2603_06267_b200 import SEM_F_EMULATE_SLABS, Simulation
-    from sem_inputs import small_config
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
         port = so.getsockname()[1]
     mp.start_processes(_rank_main, args=(2, port, str(tmp_path), name, graph), nprocs=2, join=True,
                        start_method="spawn")
     got = np.load(tmp_path / "nccl.npz")
-    rec = small_config(name)
+    rec = _record(name)
     emu = Simulation(rec, world=2, flags=SEM_F_EMULATE_SLABS)
     emu.step(STEPS)
     for b in range(len(rec["boxes"])):
