@@ -26,6 +26,12 @@
 #ifndef SEM_MINB
 #define SEM_MINB 1
 #endif
+#ifndef SEM_BATCH_WAIT
+#define SEM_BATCH_WAIT 1   // window slide: the N full-barrier tests issued back to back
+#endif
+#ifndef SEM_BW_TEST
+#define SEM_BW_TEST mbar_test_wait
+#endif
 #define SEM_VOL_BOUNDS(TY) __launch_bounds__(32 * (TY + 1), SEM_MINB)
 
 namespace sem {
@@ -49,6 +55,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// non-blocking test of a phase (no suspension: several tests can be in flight back to back)
+__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
         : "r"(bar), "r"(parity)
         : "memory");
@@ -147,7 +163,7 @@ constexpr int kFirst = 1, kLast = 2;
 // Returns the new (w, p) of this thread's node; the caller stores them.
 template <int N, int TY, int C, int F>
 __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>& t, const double* __restrict__ sP,
-                                          const double* __restrict__ sW, const double (&zw)[2 * N + 1], int ez,
+                                          const double* __restrict__ sW, const double (&zw)[N + 2], int ez,
                                           double& wn_out, double& pn_out) {
     using G = VolGeo<N, TY>;
     const BoxTables& T = p.tab;
@@ -155,7 +171,7 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
     {
         const double wv = sW[t.wown];
         wn_out = wv;
-        pn_out = fma(p.dt, wv, zw[N + C]);
+        pn_out = fma(p.dt, wv, zw[C]);
         return;
     }
 #endif
@@ -185,32 +201,33 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
         for (int b = 0; b <= N; ++b) yl = fma(RT.L[b], sP[t.yl + b * G::SW], yl);
         acc = fma(t.yLs, yl, acc);
     }
-    // ---- z: register window zw[k] = p(z0 - N + k), rows by compile-time plane class
+    // ---- z: register window zw[b] = p(z0 + b), b = 0..N (this element's planes); zw[N + 1] = the
+    //      previous element's L row applied to its planes (the left part of the shared plane z0),
+    //      accumulated when that element's window slid out (vol_layer); rows by compile-time plane class
     double z0 = 0.0, z1 = 0.0;
     if constexpr (C == N) {   // top boundary plane: left element only, BN = 2 L
 #pragma unroll
-        for (int b = 0; b <= N; b += 2) z0 = fma(2.0 * RT.L[b], zw[N + b], z0);
+        for (int b = 0; b <= N; b += 2) z0 = fma(2.0 * RT.L[b], zw[b], z0);
 #pragma unroll
-        for (int b = 1; b <= N; b += 2) z1 = fma(2.0 * RT.L[b], zw[N + b], z1);
+        for (int b = 1; b <= N; b += 2) z1 = fma(2.0 * RT.L[b], zw[b], z1);
     } else if constexpr (C == 0 && (F & kFirst)) {   // bottom boundary plane: B0 = 2 R0
 #pragma unroll
-        for (int b = 0; b <= N; b += 2) z0 = fma(2.0 * RT.R[0][b], zw[N + b], z0);
+        for (int b = 0; b <= N; b += 2) z0 = fma(2.0 * RT.R[0][b], zw[b], z0);
 #pragma unroll
-        for (int b = 1; b <= N; b += 2) z1 = fma(2.0 * RT.R[0][b], zw[N + b], z1);
+        for (int b = 1; b <= N; b += 2) z1 = fma(2.0 * RT.R[0][b], zw[b], z1);
     } else if constexpr (C == 0) {
 #pragma unroll
-        for (int b = 0; b <= N; ++b) z0 = fma(RT.R[0][b], zw[N + b], z0);
-#pragma unroll
-        for (int b = 0; b <= N; ++b) z1 = fma(RT.L[b], zw[b], z1);
+        for (int b = 0; b <= N; ++b) z0 = fma(RT.R[0][b], zw[b], z0);
+        z1 = zw[N + 1];
     } else {
 #pragma unroll
-        for (int b = 0; b <= N; b += 2) z0 = fma(RT.R[C][b], zw[N + b], z0);
+        for (int b = 0; b <= N; b += 2) z0 = fma(RT.R[C][b], zw[b], z0);
 #pragma unroll
-        for (int b = 1; b <= N; b += 2) z1 = fma(RT.R[C][b], zw[N + b], z1);
+        for (int b = 1; b <= N; b += 2) z1 = fma(RT.R[C][b], zw[b], z1);
     }
     acc = fma(p.sdir[2], z0 + z1, acc);
     double a = -acc;
-    const double pv = zw[N + C];
+    const double pv = zw[C];
 #if SEM_TWO_LEVEL   // w^n = (p^{n+1} - p^n) / dt from the p^n tile
     const double wv = (pv - sW[t.wown]) * p.inv_dt;
 #else
@@ -267,7 +284,7 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
 #endif
 template <int N, int TY, class RG, int F, int C>
 __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
-                                               uint32_t bars, int ez, const double (&zw)[2 * N + 1],
+                                               uint32_t bars, int ez, const double (&zw)[N + 2],
                                                double*& outP, double*& outW, RingPos& cur) {
     constexpr int NP = (F & kLast) ? N + 1 : N;   // planes of this layer
     if constexpr (C < NP) {
@@ -320,26 +337,47 @@ __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThre
     }
 }
 
-// Layer, then slide the window: zw <- planes z0 .. z0 + 2N (read from the ring; plane z0+N+1+j is
-// resident because slots are only refilled after their own plane has been processed).
+// Layer, then slide the window to the next element: zw[N + 1] <- L row of this element (the left part of
+// the next shared plane), zw[0] <- plane z0 + N, zw[1..N] <- planes z0 + N + 1 .. z0 + 2N (read from the
+// ring; plane z0+N+1+j is resident because slots are only refilled after their own plane has been
+// processed).  N + 2 window registers instead of 2N + 1.
 template <int N, int TY, class RG, int F>
 __device__ __forceinline__ void vol_layer(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
-                                          uint32_t bars, int ez, double (&zw)[2 * N + 1],
+                                          uint32_t bars, int ez, double (&zw)[N + 2],
                                           double*& outP, double*& outW, RingPos& cur, RingPos& nx) {
     vol_layer_step<N, TY, RG, F, 0>(p, t, ring, bars, ez, zw, outP, outW, cur);
     if constexpr (!(F & kLast)) {
+        const auto& RT = kRef<N>;
+        double zl = 0.0;
 #pragma unroll
-        for (int k = 0; k <= N; ++k) zw[k] = zw[k + N];
-        const int NZ = (int)p.NZ;
+        for (int b = 0; b <= N; ++b) zl = fma(RT.L[b], zw[b], zl);
+        zw[N + 1] = zl;
+        zw[0] = zw[N];
+        // planes z0 + N + 1 .. z0 + 2N exist (this is not the last layer: N ez + 2N <= NZ - 1).  The N
+        // full-barrier tests are issued back to back so that their latencies overlap (a try_wait on a
+        // completed phase still takes ~90 cycles), then the laggards are waited for, then the loads.
+#if SEM_BATCH_WAIT
+        RingPos q = nx;
+        uint32_t ok = 0;
 #pragma unroll
         for (int j = 0; j < N; ++j) {
-            zw[N + 1 + j] = 0.0;
-            if (N * ez + N + 1 + j < NZ) {
-                mbar_wait(bars + 8u * nx.slot, nx.par);
-                zw[N + 1 + j] = reinterpret_cast<const double*>(ring + nx.slot * RG::SLOT)[t.own];
-            }
+            ok |= (uint32_t)SEM_BW_TEST(bars + 8u * q.slot, q.par) << j;
+            q.template advance<RG::D>();
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (!((ok >> j) & 1u)) mbar_wait(bars + 8u * nx.slot, nx.par);
+            zw[1 + j] = reinterpret_cast<const double*>(ring + nx.slot * RG::SLOT)[t.own];
             nx.template advance<RG::D>();
         }
+#else
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            mbar_wait(bars + 8u * nx.slot, nx.par);
+            zw[1 + j] = reinterpret_cast<const double*>(ring + nx.slot * RG::SLOT)[t.own];
+            nx.template advance<RG::D>();
+        }
+#endif
     }
 }
 
@@ -403,17 +441,17 @@ __device__ __forceinline__ void vol_tile(const VolParams& p, unsigned char* ring
     double* outP = p.Pn + off;
     double* outW = p.W + off;
 
-    // ---- register window zw[k] = p(-N + k), k = 0..2N: planes 0..N from the ring
-    double zw[2 * N + 1];
-#pragma unroll
-    for (int k = 0; k < N; ++k) zw[k] = 0.0;
+    // ---- register window zw[b] = p(b), b = 0..N: planes 0..N from the ring (zw[N + 1] is not read on
+    //      the first layer: its bottom plane is a box face)
+    double zw[N + 2];
+    zw[N + 1] = 0.0;
     RingPos w = RingPos::at<RG::D>(g0);
 #pragma unroll
     for (int k = 0; k <= N; ++k) {
-        zw[N + k] = 0.0;
+        zw[k] = 0.0;
         if (k < NZ) {
             mbar_wait(bars + 8u * w.slot, w.par);
-            zw[N + k] = reinterpret_cast<const double*>(ring + w.slot * RG::SLOT)[t.own];
+            zw[k] = reinterpret_cast<const double*>(ring + w.slot * RG::SLOT)[t.own];
         }
         w.template advance<RG::D>();
     }
