@@ -285,7 +285,7 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
 template <int N, int TY, class RG, int F, int C>
 __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
                                                uint32_t bars, int ez, const double (&zw)[N + 2],
-                                               double*& outP, double*& outW, RingPos& cur) {
+                                               double*& outP, double*& outW, RingPos& cur, double& dz) {
     constexpr int NP = (F & kLast) ? N + 1 : N;   // planes of this layer
     if constexpr (C < NP) {
         using G = VolGeo<N, TY>;
@@ -306,6 +306,14 @@ __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThre
                 if (!SEM_TWO_LEVEL) st_out(outW + PS, w1);
                 st_out(outP + PS, p1);
             }
+            if constexpr (F & kLast) {   // d_z p^{n+2} at the top face for the next step's interface
+                if (p.dzf) {
+                    dz = fma(p.dzc[C], p0, dz);
+                    dz = fma(p.dzc[C + 1], p1, dz);
+                    if constexpr (C + 1 == N)
+                        if (t.valid) p.dzf[t.fc] = dz;
+                }
+            }
             outP += 2 * PS;
             outW += 2 * PS;
             __syncwarp();
@@ -315,7 +323,7 @@ __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThre
             }
             nxt.template advance<RG::D>();
             cur = nxt;
-            vol_layer_step<N, TY, RG, F, C + 2>(p, t, ring, bars, ez, zw, outP, outW, cur);
+            vol_layer_step<N, TY, RG, F, C + 2>(p, t, ring, bars, ez, zw, outP, outW, cur, dz);
         } else {
             const unsigned char* s0 = ring + cur.slot * RG::SLOT;
             double w0, p0;
@@ -325,6 +333,13 @@ __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThre
                 if (!SEM_TWO_LEVEL) st_out(outW, w0);
                 st_out(outP, p0);
             }
+            if constexpr (F & kLast) {
+                if (p.dzf) {
+                    dz = fma(p.dzc[C], p0, dz);
+                    if constexpr (C == N)
+                        if (t.valid) p.dzf[t.fc] = dz;
+                }
+            }
             outP += PS;
             outW += PS;
             // release the slot: one arrival per consumer warp on its "empty" barrier (no block-wide
@@ -332,7 +347,7 @@ __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThre
             __syncwarp();
             if (threadIdx.x == 0) mbar_arrive(bars + 8u * (RG::D + cur.slot));
             cur.template advance<RG::D>();
-            vol_layer_step<N, TY, RG, F, C + 1>(p, t, ring, bars, ez, zw, outP, outW, cur);
+            vol_layer_step<N, TY, RG, F, C + 1>(p, t, ring, bars, ez, zw, outP, outW, cur, dz);
         }
     }
 }
@@ -345,7 +360,8 @@ template <int N, int TY, class RG, int F>
 __device__ __forceinline__ void vol_layer(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
                                           uint32_t bars, int ez, double (&zw)[N + 2],
                                           double*& outP, double*& outW, RingPos& cur, RingPos& nx) {
-    vol_layer_step<N, TY, RG, F, 0>(p, t, ring, bars, ez, zw, outP, outW, cur);
+    double dz = 0.0;   // top layer: d_z p^{n+2} at the top face (same fma order as the interface's)
+    vol_layer_step<N, TY, RG, F, 0>(p, t, ring, bars, ez, zw, outP, outW, cur, dz);
     if constexpr (!(F & kLast)) {
         const auto& RT = kRef<N>;
         double zl = 0.0;
@@ -1277,8 +1293,12 @@ __global__ void __launch_bounds__(SEM_IF_THREADS) iface_fused(const __grid_const
             const double* node = top + iy * p.PXf + ix;
             const double pp = __ldg(node);
             double dpp = 0.0;
+            if (p.dzf) {   // written by the previous volume launch (the same sum in the same order)
+                dpp = __ldg(p.dzf + iy * NXf + ix);
+            } else {
 #pragma unroll
-            for (int c = 0; c <= NF; ++c) dpp = fma(p.dfT[c], __ldg(node - (long long)(NF - c) * Sf), dpp);
+                for (int c = 0; c <= NF; ++c) dpp = fma(p.dfT[c], __ldg(node - (long long)(NF - c) * Sf), dpp);
+            }
             // coarse element row (footprint-local) and local fine index of this node in it along y
             const int ely = j / NFR < TC ? j / NFR : TC, qy = j - ely * NFR;
             double pm = 0.0, dpm = 0.0;
@@ -1396,6 +1416,27 @@ static void launch_iface_t(const IfaceParams& p, cudaStream_t s) {
 #ifndef SEM_IFACE_FUSED
 #define SEM_IFACE_FUSED 1
 #endif
+// d_z p at the fine face from the current state (after sem_write_state / sem_fill_random_state / the
+// interface build): the value the volume kernel keeps up to date from then on (VolParams::dzf)
+__global__ void iface_dz_init(const __grid_constant__ IfaceParams p, double* dzf) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= p.NXf * p.NYf) return;
+    const long long ix = k % p.NXf, iy = k / p.NXf;
+    const long long Sf = p.PXf * p.NYf;
+    const double* node = p.Pf + (p.NZf - 1) * Sf + iy * p.PXf + ix;
+    double d = 0.0;
+    for (int c = 0; c <= p.Nf; ++c) d = fma(p.dfT[c], node[-(long long)(p.Nf - c) * Sf], d);
+    dzf[k] = d;
+}
+
+void launch_iface_dz_init(const IfaceParams& p, double* dzf, cudaStream_t s) {
+    const long long n = p.NXf * p.NYf;
+    iface_dz_init<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, dzf);
+}
+
+bool iface_uses_dzf(int Nf, int Nc, int R, int lg) { return SEM_IFACE_FUSED && !lg && Nf == 5 && Nc == 3 && R == 2; }
+
+
 void iface_prepare(int Nf, int Nc, int R) {   // outside any stream capture (function attributes)
     if (SEM_IFACE_FUSED && Nf == 5 && Nc == 3 && R == 2)
         cudaFuncSetAttribute(iface_fused<5, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, IfFused<5, 3, 2>::SMEM);

@@ -448,6 +448,26 @@ Box make_slab(const sem_box_desc& g, long long ey0, long long nel_loc, bool cutL
     return b;
 }
 
+// The fine face's d_z p hand-off (VolParams::dzf / IfaceParams::dzf): the structured fused interface on
+// one GPU (no slabs: the cut fix-up would change p^{n+2} after the volume kernel) and no PML on the fine
+// box (the PML fix-up would, too).
+bool dzf_active(const sem_ctx* ctx, const sem::Part& pt) {
+    if (!pt.itf.on || pt.itf.general || !pt.itf.dzf || ctx->world > 1 || ctx->parts.size() != 1) return false;
+    if (pt.pml.on && pt.pml.box == pt.itf.fine) return false;
+    if (pt.boxes[pt.itf.fine].curved || pt.boxes[pt.itf.coarse].curved) return false;
+    return true;
+}
+
+// (re)compute d_z p at the fine face from the current state P[cur]
+void dzf_refresh(sem_ctx* ctx) {
+    for (auto& pt : ctx->parts)
+        if (dzf_active(ctx, pt)) {
+            sem::IfaceParams ip = pt.itf.prm;
+            ip.Pf = pt.boxes[pt.itf.fine].P[ctx->cur];
+            sem::launch_iface_dz_init(ip, pt.itf.dzf, ctx->stream);
+        }
+}
+
 sem::VolParams vol_params(sem_ctx* ctx, sem::Part& pt, int bi, int cur) {
     Box& b = pt.boxes[bi];
     sem::VolParams p{};
@@ -497,6 +517,10 @@ sem::VolParams vol_params(sem_ctx* ctx, sem::Part& pt, int bi, int cur) {
         p.yc = b.yc;
     }
     p.step = ctx->d_step;
+    if (pt.itf.on && bi == pt.itf.fine && dzf_active(ctx, pt)) {
+        p.dzf = pt.itf.dzf;
+        for (int c = 0; c <= b.N; ++c) p.dzc[c] = pt.itf.prm.dfT[c];
+    }
     return p;
 }
 
@@ -736,6 +760,7 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
             sem::IfaceParams ip = pt.itf.prm;
             ip.Pf = pt.boxes[pt.itf.fine].P[cur];
             ip.Pc = pt.boxes[pt.itf.coarse].P[cur];
+            ip.dzf = dzf_active(ctx, pt) ? pt.itf.dzf : nullptr;
             nl += sem::launch_iface(ip, s);
         }
         mark(1, false, s);
@@ -859,6 +884,7 @@ sem_status reset_dynamic(sem_ctx* ctx) {
         CU(cudaMemsetAsync(m.da, 0, (size_t)b.nalloc() * sizeof(double), ctx->stream));
     }
     ctx->step = 0;
+    dzf_refresh(ctx);   // the state changed: the fine face's d_z p follows it
     return SEM_OK;
 }
 
@@ -1648,8 +1674,10 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
         pt.itf.on = true;
         pt.itf.fine = fine_box;
         pt.itf.coarse = coarse_box;
+        if (sem::iface_uses_dzf(Nf, Nc, R, quad_rule == 1 ? 1 : 0) && dalloc(ctx, &pt.itf.dzf, nf)) return SEM_E_OOM;
     }
     sem::iface_prepare(gF.degree, gC.degree, R);
+    dzf_refresh(ctx);
     ctx->itf_on = true;
     drop_graphs(ctx);
     CU(cudaStreamSynchronize(ctx->stream));

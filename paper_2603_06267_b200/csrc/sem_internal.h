@@ -124,6 +124,11 @@ struct VolParams {
     const double* __restrict__ yc; // node y coordinates [NY]
     // device step counter: t^{n+1} = (step + 1) dt (read by the plane-wave source)
     const long long* step;
+    // fine side of the structured interface (iface_side > 0), one GPU, no PML on the box: the kernel also
+    // writes d_z p^{n+2} at the top face, dzf[iy NX + ix] = sum_c dzc[c] p^{n+2}(top - N + c) (the
+    // next step's interface reads it instead of the top element's N + 1 planes); nullptr otherwise
+    double* dzf;
+    double dzc[kMaxN + 1];
 };
 
 // One persistent volume launch: one or two boxes (box[1] of degree N1 != N0 shares the launch so
@@ -194,6 +199,8 @@ struct IfaceParams {
     double* h1; double* h2;         // [NYc][NXf] after the y gather
     double* tauc; double* sigc;     // coarse outputs [NXc*NYc]
     int skip_iy0;                   // slab with a lower cut: the shared fine cut line belongs to the lower slab
+    const double* __restrict__ dzf; // d_z p+ at the fine face [NXf*NYf] written by the previous volume launch
+                                    // (or iface_dz_init), or nullptr: the fused kernel reads the N_f + 1 planes
     // Gauss-Legendre quadrature on the fine faces (quad_rule 1, R9's flag): nq = Nf + 1 points per
     // direction and fine face, none shared; the fine side's terms are projected back onto the fine
     // face nodes (collocated-equivalent tau / sigma, so vol_kernel is unchanged)
@@ -390,6 +397,7 @@ struct Iface {
     bool general = false;          // curved boxes: table-driven kernel on Algorithm 3's matching
     GIfaceParams gprm{};
     std::vector<void*> allocs;
+    double* dzf = nullptr;         // d_z p at the fine face, kept by the volume kernel (dzf_active)
 };
 
 struct PlaneWave {
@@ -467,6 +475,8 @@ bool volume_pair_supported(int N0, int N1);
 void volume_pair_prepare(int N0, int N1);
 void launch_modal(const ModalParams& p, cudaStream_t s);
 int launch_iface(const IfaceParams& p, cudaStream_t s);   // returns the number of kernel launches
+bool iface_uses_dzf(int Nf, int Nc, int R, int lg);       // the interface path that reads IfaceParams::dzf
+void launch_iface_dz_init(const IfaceParams& p, double* dzf, cudaStream_t s);
 void iface_prepare(int Nf, int Nc, int R);
 void launch_fill_random(double* p, double* w, double* pn, long long NX, long long PX, long long NY, long long NZ,
                         long long gy0, long long NYg, unsigned long long seed, int box, double ps, double vs,

@@ -86,9 +86,14 @@ def test_literal_coupling_flag():
 
 
 @pytest.mark.parametrize("N,nel", [(1, (3, 5, 2)), (2, (2, 3, 4)), (3, (11, 3, 2)), (6, (2, 1, 3)),
-                                   (7, (1, 2, 1)), (8, (2, 2, 1))])
+                                   (7, (1, 2, 1)), (8, (2, 2, 1)),
+                                   # several x tiles (TXE = 2 x 30 nodes for N = 2, 3, 5; 56 for N = 4; 48
+                                   # for N = 8) with a ragged last tile, or the TXE + 1 last tile
+                                   (3, (45, 3, 2)), (2, (60, 2, 2)), (5, (25, 2, 1)), (4, (31, 2, 2)),
+                                   (8, (13, 1, 1))])
 def test_degrees_and_ragged_tiles(N, nel):
-    """Every compiled degree; NX not a multiple of 32, NY not of 8, single-element directions."""
+    """Every compiled degree; NX not a multiple of 32, NY not of 8, single-element directions, several x
+    tiles with ragged or one-node-wider last tiles."""
     rec = cavity_config(nel=nel, degree=N, extent=(1.1e-4 * nel[0], 0.9e-4 * nel[1], 1.3e-4 * nel[2]))
     rec["boxes"][0]["bc"] = [1, 0, 0, 1, 0, 1]           # mixed absorbing / rigid faces
     st = random_state(rec, seed=N)
