@@ -1215,7 +1215,10 @@ static void launch_iface_lg(const IfaceParams& p, cudaStream_t s) {
 //       tau = gamma J - A, sigma = -1/2 c+^2 J (written for the fine nodes the tile owns) and the weighted
 //       coarse-side terms g1 = -W tau, g2 = W (c-^2/c+^2) sigma (W = m_x m_y) in shared memory;
 //   (3) transposed interpolation along y, then (4) along x, divided by the coarse face masses.
-constexpr int kIfTC = 4;   // coarse elements per tile edge
+#ifndef SEM_IF_TC
+#define SEM_IF_TC 4
+#endif
+constexpr int kIfTC = SEM_IF_TC;   // coarse elements per tile edge
 template <int NF, int NC, int R>
 struct IfFused {
     static constexpr int NFR = NF * R;                 // fine nodes per coarse element edge
