@@ -1579,8 +1579,11 @@ constexpr int pml_epb() { return (N + 1) * (N + 1) * (N + 1) >= 256 ? 1 : 256 / 
 // resident blocks per SM the element kernel is compiled for (register budget): more blocks hide the
 // latency of its short, barrier-separated phases (N = 3: 339 vs 458 us per cfg-3 PML step); the larger
 // elements would spill
+#ifndef SEM_PML_MINB3
+#define SEM_PML_MINB3 4
+#endif
 template <int N>
-constexpr int pml_minb() { return N <= 3 ? 4 : (N <= 5 ? 3 : (N == 6 ? 2 : 1)); }
+constexpr int pml_minb() { return N <= 3 ? SEM_PML_MINB3 : (N <= 5 ? 3 : (N == 6 ? 2 : 1)); }
 
 template <int N>
 __global__ void __launch_bounds__(pml_epb<N>() * (N + 1) * (N + 1) * (N + 1), pml_minb<N>()) pml_element_kernel(const __grid_constant__ PmlParams p) {
@@ -1718,13 +1721,15 @@ __global__ void __launch_bounds__(256) pml_fixup_rows_kernel(const __grid_consta
         const long long g0 = p.seg_start[sg];
         const int len = p.seg_len[sg];
         SEM_CHECK(g0 >= 0 && len > 0 && len <= p.NX && g0 + len <= p.PX * p.NY * p.NZ);
+        // da and p^{n+2} are loaded together (one memory round trip per pass, not two dependent ones)
         for (int i = lane; i < len; i += 32) {
             const long long g = g0 + i;
             const double v = p.da[g];
+            const double pn = p.Pn[g];
             if (v != 0.0) {
                 const double dw = p.dt * v;
                 if (!SEM_TWO_LEVEL) p.Wn[g] += dw;
-                p.Pn[g] = fma(p.dt, dw, p.Pn[g]);
+                p.Pn[g] = fma(p.dt, dw, pn);
                 p.da[g] = 0.0;
             }
         }
