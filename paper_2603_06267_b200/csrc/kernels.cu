@@ -20,9 +20,7 @@
 #include "sem_internal.h"
 
 // Volume-kernel tiling (tuned on B200, see profiles/): consumer rows per CTA and minimum CTAs per SM.
-#ifndef SEM_KTY
-#define SEM_KTY 11
-#endif
+
 #ifndef SEM_MINB
 #define SEM_MINB 1
 #endif
@@ -32,7 +30,24 @@
 #ifndef SEM_BW_TEST
 #define SEM_BW_TEST mbar_test_wait
 #endif
-#define SEM_VOL_BOUNDS(TY) __launch_bounds__(32 * (TY + 1), SEM_MINB)
+// SEM_WG 1: warp-specialised warpgroups -- TY (a multiple of 4) consumer warps in TY/4 warpgroups that
+// grow their register budget with setmaxnreg, and one producer warpgroup (one active warp) that shrinks
+// its own, so that 12 row warps get ~160 registers (the register file is split per SM sub-partition: 13
+// warps of one kernel-wide budget would allow only 128)
+#ifndef SEM_WG
+#define SEM_WG 1
+#endif
+#ifndef SEM_KTY
+#define SEM_KTY (SEM_WG ? 12 : 11)   // consumer rows per CTA: 12 in three warpgroups, or 11 + a producer warp
+#endif
+#ifndef SEM_WG_CONS_REGS
+#define SEM_WG_CONS_REGS 160
+#endif
+#ifndef SEM_WG_PROD_REGS
+#define SEM_WG_PROD_REGS 32
+#endif
+#define SEM_VOL_WARPS(TY) ((TY) + (SEM_WG ? 4 : 1))
+#define SEM_VOL_BOUNDS(TY) __launch_bounds__(32 * SEM_VOL_WARPS(TY), SEM_MINB)
 
 namespace sem {
 
@@ -529,6 +544,15 @@ __global__ void SEM_VOL_BOUNDS(TY) vol_kernel(const __grid_constant__ VolLaunch 
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
+#if SEM_WG
+    static_assert(TY % 4 == 0, "warpgroup mode needs whole consumer warpgroups");
+    if (ly >= TY) {   // producer warpgroup: give registers back; its first warp streams the planes
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(SEM_WG_PROD_REGS));
+        if (ly > TY) return;
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SEM_WG_CONS_REGS));
+    }
+#endif
     if (ly == TY) {   // producer warp
         if (lane == 0) {
             unsigned g = 0;
@@ -621,7 +645,7 @@ struct VolInst {
         static int occ = -1;
         if (occ < 0) {
             cudaFuncSetAttribute(vol_kernel<N0, N1, kTY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem());
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vol_kernel<N0, N1, kTY>, 32 * (kTY + 1),
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vol_kernel<N0, N1, kTY>, 32 * SEM_VOL_WARPS(kTY),
                                                               smem()) != cudaSuccess || occ < 1)
                 occ = 1;
         }
@@ -639,7 +663,7 @@ struct VolInst {
         const int nsm_use = nsm - L.reserve_sms > 1 ? nsm - L.reserve_sms : 1;
         unsigned grid = (unsigned)(nsm_use * ctas_per_sm());
         if (grid > ntot) grid = ntot;
-        vol_kernel<N0, N1, kTY><<<grid, dim3(32, kTY + 1), smem(), s>>>(L);
+        vol_kernel<N0, N1, kTY><<<grid, dim3(32, SEM_VOL_WARPS(kTY)), smem(), s>>>(L);
     }
 };
 
