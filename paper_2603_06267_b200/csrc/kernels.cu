@@ -295,7 +295,7 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
 // together (independent dependency chains interleave: twice the ILP per consumer warp) before their
 // stores and slot releases.
 #ifndef SEM_PAIR
-#define SEM_PAIR 1
+#define SEM_PAIR (SEM_WG ? 0 : 1)   // with 12 row warps (warpgroups) the single-plane order is faster
 #endif
 template <int N, int TY, class RG, int F, int C>
 __device__ __forceinline__ void vol_layer_step(const VolParams& p, const VolThread<N>& t, unsigned char* ring,
