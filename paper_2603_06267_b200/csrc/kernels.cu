@@ -24,6 +24,12 @@
 #ifndef SEM_MINB
 #define SEM_MINB 1
 #endif
+#ifndef SEM_XSPLIT
+#define SEM_XSPLIT 0
+#endif
+#ifndef SEM_PSLEEP
+#define SEM_PSLEEP 64   // producer back-off (ns) while the slot it refills is still in use
+#endif
 #ifndef SEM_BATCH_WAIT
 #define SEM_BATCH_WAIT 1   // window slide: the N full-barrier tests issued back to back
 #endif
@@ -32,20 +38,22 @@
 #endif
 // SEM_WG 1: warp-specialised warpgroups -- TY (a multiple of 4) consumer warps in TY/4 warpgroups that
 // grow their register budget with setmaxnreg, and one producer warpgroup (one active warp) that shrinks
-// its own, so that 12 row warps get ~160 registers (the register file is split per SM sub-partition: 13
-// warps of one kernel-wide budget would allow only 128)
+// its own to 24, so that 16 row warps get 112 registers (the register file is split per SM sub-partition:
+// 17 warps of one kernel-wide budget would allow only 96)
 #ifndef SEM_WG
 #define SEM_WG 1
 #endif
 #ifndef SEM_KTY
-#define SEM_KTY (SEM_WG ? 12 : 11)   // consumer rows per CTA: 12 in three warpgroups, or 11 + a producer warp
+#define SEM_KTY (SEM_WG ? 16 : 11)   // consumer rows per CTA: 16 in four warpgroups, or 11 + a producer warp
 #endif
-#ifndef SEM_WG_CONS_REGS
-#define SEM_WG_CONS_REGS 160
+#ifndef SEM_KTY_SLAB
+#define SEM_KTY_SLAB (SEM_WG ? 12 : 11)   // rows per CTA in y-slab contexts (fewer tiles per slab: smaller tail)
 #endif
-#ifndef SEM_WG_PROD_REGS
-#define SEM_WG_PROD_REGS 32
-#endif
+// setmaxnreg budgets per thread: 16 row warps (65536 - 128 * 24) / 512 -> 112 and 24; 12 row warps 160 and 32
+template <int TY>
+constexpr int wg_cons_regs() { return TY >= 16 ? 112 : 160; }
+template <int TY>
+constexpr int wg_prod_regs() { return TY >= 16 ? 24 : 32; }
 #define SEM_VOL_WARPS(TY) ((TY) + (SEM_WG ? 4 : 1))
 #define SEM_VOL_BOUNDS(TY) __launch_bounds__(32 * SEM_VOL_WARPS(TY), SEM_MINB)
 
@@ -197,11 +205,29 @@ __device__ __forceinline__ void vol_plane(const VolParams& p, const VolThread<N>
 #pragma unroll
     for (int b = 0; b <= N; ++b) v[b] = sP[t.xb + b];
     double xr = 0.0, xl = 0.0;
+#if SEM_XSPLIT   // two accumulation chains per x row (shorter fma dependency chains)
+    {
+        double xr1 = 0.0, xl1 = 0.0;
+#pragma unroll
+        for (int b = 0; b <= N; b += 2) {
+            xr = fma(t.cR[b], v[b], xr);
+            xl = fma(RT.L[b], v[b], xl);
+        }
+#pragma unroll
+        for (int b = 1; b <= N; b += 2) {
+            xr1 = fma(t.cR[b], v[b], xr1);
+            xl1 = fma(RT.L[b], v[b], xl1);
+        }
+        xr += xr1;
+        xl += xl1;
+    }
+#else
 #pragma unroll
     for (int b = 0; b <= N; ++b) {
         xr = fma(t.cR[b], v[b], xr);
         xl = fma(RT.L[b], v[b], xl);
     }
+#endif
     const double xlr = __shfl_sync(0xffffffffu, xl, (threadIdx.x + 31) & 31);
     // ---- y: per-warp row (registers, scaled); left row of a shared node: row L
     double y0 = 0.0, y1 = 0.0;
@@ -513,7 +539,7 @@ template <int N0, int N1, int TY>
 struct PairRing {
     static constexpr int SLOT = cmax(vol_slot_bytes(N0, TY), N1 ? vol_slot_bytes(N1, TY) : 0);
     static constexpr int D = cmax(vol_depth_for_slot(N0, SLOT), N1 ? vol_depth_for_slot(N1, SLOT) : 0);
-    static_assert(D >= 2 * cmax(N0, N1) + 2, "ring too shallow for the z window");
+    static_assert(D >= cmax(N0, N1) + 2, "ring too shallow for the z window (it holds N + 1 planes)");
     using RG = Ring<D, SLOT>;
 };
 
@@ -547,10 +573,10 @@ __global__ void SEM_VOL_BOUNDS(TY) vol_kernel(const __grid_constant__ VolLaunch 
 #if SEM_WG
     static_assert(TY % 4 == 0, "warpgroup mode needs whole consumer warpgroups");
     if (ly >= TY) {   // producer warpgroup: give registers back; its first warp streams the planes
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(SEM_WG_PROD_REGS));
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(wg_prod_regs<TY>()));
         if (ly > TY) return;
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SEM_WG_CONS_REGS));
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(wg_cons_regs<TY>()));
     }
 #endif
     if (ly == TY) {   // producer warp
@@ -562,7 +588,7 @@ __global__ void SEM_VOL_BOUNDS(TY) vol_kernel(const __grid_constant__ VolLaunch 
                 if (box < 0) {   // end marker: a header of -1 on the next slot, completed without data
                     const int slot = (int)(g % D);
                     if (g >= (unsigned)D)
-                        while (!mbar_try_wait(bars + 8u * (D + slot), ((g / D) - 1u) & 1u)) __nanosleep(64);
+                        while (!mbar_try_wait(bars + 8u * (D + slot), ((g / D) - 1u) & 1u)) __nanosleep(SEM_PSLEEP);
                     tileq[slot] = -1;
                     mbar_arrive(bars + 8u * slot);
                     break;
@@ -577,7 +603,7 @@ __global__ void SEM_VOL_BOUNDS(TY) vol_kernel(const __grid_constant__ VolLaunch 
                 for (int z = 0; z < NZ; ++z, ++g) {   // plane g reuses the slot of plane g - D
                     const int slot = (int)(g % D);
                     if (g >= (unsigned)D)
-                        while (!mbar_try_wait(bars + 8u * (D + slot), ((g / D) - 1u) & 1u)) __nanosleep(64);
+                        while (!mbar_try_wait(bars + 8u * (D + slot), ((g / D) - 1u) & 1u)) __nanosleep(SEM_PSLEEP);
                     if (z == 0) tileq[slot] = (int)tile;
                     if constexpr (N1 > 0) {
                         if (box) vol_issue<N1, TY, RG>(L.box[1], ring, bars, slot, z, tx0, ty0);
@@ -633,19 +659,20 @@ __global__ void SEM_VOL_BOUNDS(TY) vol_kernel(const __grid_constant__ VolLaunch 
     }
 }
 
-constexpr int kTY = SEM_KTY;   // consumer rows per CTA (+1 producer warp)
+constexpr int kTY = SEM_KTY;        // consumer rows per CTA, one GPU
+constexpr int kTYs = SEM_KTY_SLAB;  // consumer rows per CTA, y-slab contexts
 
-template <int N0, int N1>
+template <int N0, int N1, int TY>
 struct VolInst {
     static int smem() {
-        using R = PairRing<N0, N1, kTY>;
+        using R = PairRing<N0, N1, TY>;
         return R::D * R::SLOT + 2 * R::D * 8 + R::D * 4 + 128;
     }
     static int ctas_per_sm() {   // resident CTAs per SM (occupancy), cached
         static int occ = -1;
         if (occ < 0) {
-            cudaFuncSetAttribute(vol_kernel<N0, N1, kTY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem());
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vol_kernel<N0, N1, kTY>, 32 * SEM_VOL_WARPS(kTY),
+            cudaFuncSetAttribute(vol_kernel<N0, N1, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem());
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vol_kernel<N0, N1, TY>, 32 * SEM_VOL_WARPS(TY),
                                                               smem()) != cudaSuccess || occ < 1)
                 occ = 1;
         }
@@ -663,28 +690,36 @@ struct VolInst {
         const int nsm_use = nsm - L.reserve_sms > 1 ? nsm - L.reserve_sms : 1;
         unsigned grid = (unsigned)(nsm_use * ctas_per_sm());
         if (grid > ntot) grid = ntot;
-        vol_kernel<N0, N1, kTY><<<grid, dim3(32, SEM_VOL_WARPS(kTY)), smem(), s>>>(L);
+        vol_kernel<N0, N1, TY><<<grid, dim3(32, SEM_VOL_WARPS(TY)), smem(), s>>>(L);
     }
 };
 
-void volume_prepare(int N) {
+template <int TY>
+static void volume_prepare_t(int N) {
     switch (N) {
-        case 1: VolInst<1, 0>::ctas_per_sm(); break;
-        case 2: VolInst<2, 0>::ctas_per_sm(); break;
-        case 3: VolInst<3, 0>::ctas_per_sm(); break;
-        case 4: VolInst<4, 0>::ctas_per_sm(); break;
-        case 5: VolInst<5, 0>::ctas_per_sm(); break;
-        case 6: VolInst<6, 0>::ctas_per_sm(); break;
-        case 7: VolInst<7, 0>::ctas_per_sm(); break;
-        case 8: VolInst<8, 0>::ctas_per_sm(); break;
+        case 1: VolInst<1, 0, TY>::ctas_per_sm(); break;
+        case 2: VolInst<2, 0, TY>::ctas_per_sm(); break;
+        case 3: VolInst<3, 0, TY>::ctas_per_sm(); break;
+        case 4: VolInst<4, 0, TY>::ctas_per_sm(); break;
+        case 5: VolInst<5, 0, TY>::ctas_per_sm(); break;
+        case 6: VolInst<6, 0, TY>::ctas_per_sm(); break;
+        case 7: VolInst<7, 0, TY>::ctas_per_sm(); break;
+        case 8: VolInst<8, 0, TY>::ctas_per_sm(); break;
         default: break;
     }
+}
+void volume_prepare(int N, int ty) {
+    if (ty == kTYs) volume_prepare_t<kTYs>(N);
+    else volume_prepare_t<kTY>(N);
 }
 
 bool volume_pair_supported(int N0, int N1) { return N0 == 5 && N1 == 3; }
 
-void volume_pair_prepare(int N0, int N1) {
-    if (N0 == 5 && N1 == 3) VolInst<5, 3>::ctas_per_sm();
+void volume_pair_prepare(int N0, int N1, int ty) {
+    if (N0 == 5 && N1 == 3) {
+        if (ty == kTYs) VolInst<5, 3, kTYs>::ctas_per_sm();
+        else VolInst<5, 3, kTY>::ctas_per_sm();
+    }
 }
 
 void fill_tiles(VolLaunch& L) {
@@ -692,44 +727,52 @@ void fill_tiles(VolLaunch& L) {
         const VolParams& p = L.box[b];
         const int txe = vol_txe(p.N);
         L.ntx[b] = (unsigned)((p.NX - 1 + txe - 1) / txe);   // the last tile may take TXE + 1 nodes
-        L.nty[b] = (unsigned)((p.NY + kTY - 1) / kTY);
+        L.nty[b] = (unsigned)((p.NY + L.ty - 1) / L.ty);
         L.ntiles[b] = L.ntx[b] * L.nty[b];
     }
 }
 
-void launch_volume(VolLaunch L, cudaStream_t s) {
-    fill_tiles(L);
+template <int TY>
+static void launch_volume_t(const VolLaunch& L, cudaStream_t s) {
     if (L.nbox == 2) {
-        if (L.box[0].N == 5 && L.box[1].N == 3) VolInst<5, 3>::launch(L, s);
+        if (L.box[0].N == 5 && L.box[1].N == 3) VolInst<5, 3, TY>::launch(L, s);
         return;
     }
     switch (L.box[0].N) {
-        case 1: VolInst<1, 0>::launch(L, s); break;
-        case 2: VolInst<2, 0>::launch(L, s); break;
-        case 3: VolInst<3, 0>::launch(L, s); break;
-        case 4: VolInst<4, 0>::launch(L, s); break;
-        case 5: VolInst<5, 0>::launch(L, s); break;
-        case 6: VolInst<6, 0>::launch(L, s); break;
-        case 7: VolInst<7, 0>::launch(L, s); break;
-        case 8: VolInst<8, 0>::launch(L, s); break;
+        case 1: VolInst<1, 0, TY>::launch(L, s); break;
+        case 2: VolInst<2, 0, TY>::launch(L, s); break;
+        case 3: VolInst<3, 0, TY>::launch(L, s); break;
+        case 4: VolInst<4, 0, TY>::launch(L, s); break;
+        case 5: VolInst<5, 0, TY>::launch(L, s); break;
+        case 6: VolInst<6, 0, TY>::launch(L, s); break;
+        case 7: VolInst<7, 0, TY>::launch(L, s); break;
+        case 8: VolInst<8, 0, TY>::launch(L, s); break;
         default: break;
     }
 }
 
+void launch_volume(VolLaunch L, cudaStream_t s) {
+    if (L.ty != kTYs) L.ty = kTY;
+    fill_tiles(L);
+    if (L.ty == kTYs) launch_volume_t<kTYs>(L, s);
+    else launch_volume_t<kTY>(L, s);
+}
+
 int volume_smem_bytes(int N) {
     switch (N) {
-        case 1: return VolInst<1, 0>::smem();
-        case 2: return VolInst<2, 0>::smem();
-        case 3: return VolInst<3, 0>::smem();
-        case 4: return VolInst<4, 0>::smem();
-        case 5: return VolInst<5, 0>::smem();
-        case 6: return VolInst<6, 0>::smem();
-        case 7: return VolInst<7, 0>::smem();
-        case 8: return VolInst<8, 0>::smem();
+        case 1: return VolInst<1, 0, kTY>::smem();
+        case 2: return VolInst<2, 0, kTY>::smem();
+        case 3: return VolInst<3, 0, kTY>::smem();
+        case 4: return VolInst<4, 0, kTY>::smem();
+        case 5: return VolInst<5, 0, kTY>::smem();
+        case 6: return VolInst<6, 0, kTY>::smem();
+        case 7: return VolInst<7, 0, kTY>::smem();
+        case 8: return VolInst<8, 0, kTY>::smem();
         default: return 0;
     }
 }
-int volume_tile_y() { return kTY; }
+// consumer rows per volume tile: one GPU, or y-slab contexts (more, smaller launches: a smaller tail)
+int volume_tile_y(bool slabs) { return slabs ? kTYs : kTY; }
 
 // ------------------------------------------------------------------------------------------------
 // Modal kernel: one warp per PMUT

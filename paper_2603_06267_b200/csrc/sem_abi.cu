@@ -829,6 +829,7 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
             // NCCL's send/recv kernel cannot co-reside with a volume CTA (smem, registers): keep a few SMs
             // free so the cut-plane exchange overlaps the volume launch instead of waiting for its end
             ls[i].reserve_sms = nccl_mode(ctx) ? 4 : 0;
+            ls[i].ty = ctx->vol_ty;
             sem::launch_volume(ls[i], s);
             ++nl;
         }
@@ -966,9 +967,10 @@ sem_status setup_part_buffers(sem_ctx* ctx, sem::Part& pt) {
         if (upload(ctx, &b.xc, b.xh) || upload(ctx, &b.yc, b.yh) || upload(ctx, &b.mx, b.mxh) ||
             upload(ctx, &b.my, b.myh))
             return SEM_E_CUDA;
-        sem::volume_prepare(b.N);
-        if (pt.boxes.size() == 2) sem::volume_pair_prepare(pt.boxes[0].N, pt.boxes[1].N);
-        const int TY = sem::volume_tile_y();
+        const int TY = sem::volume_tile_y(ctx->world > 1 || ctx->parts.size() > 1);
+        ctx->vol_ty = TY;
+        sem::volume_prepare(b.N, TY);
+        if (pt.boxes.size() == 2) sem::volume_pair_prepare(pt.boxes[0].N, pt.boxes[1].N, TY);
         if (!make_map(&b.tmP[0], b.P[0], b, sem::vol_pbox_w(b.N), TY + 2 * b.N) ||
             !make_map(&b.tmP[1], b.P[1], b, sem::vol_pbox_w(b.N), TY + 2 * b.N) ||
             !make_map(&b.tmW, b.W, b, sem::vol_wbox_w(b.N), TY) ||

@@ -143,6 +143,7 @@ struct VolLaunch {
     long long* step;                // device step counter, bumped by the last CTA if bump_step
     int bump_step;                  // 1 for the last volume launch of a step
     int reserve_sms;                // SMs kept free (NCCL exchange running beside the launch)
+    int ty;                         // consumer rows per tile (volume_tile_y of the context)
 };
 
 struct ModalParams {
@@ -449,6 +450,7 @@ struct sem_ctx {
     long long step = 0;          // host mirror of the device counter
     long long* d_step = nullptr;
     unsigned int* d_sched = nullptr;  // tile scheduler pairs, one per volume launch of a step
+    int vol_ty = 0;                   // consumer rows per volume tile (sem::volume_tile_y)
     static constexpr int kSchedPairs = 64;
     unsigned long long* d_flag = nullptr;
     cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [parity][1 or 2 steps]
@@ -472,7 +474,7 @@ namespace sem {
 // kernels.cu
 void launch_volume(VolLaunch L, cudaStream_t s);
 bool volume_pair_supported(int N0, int N1);
-void volume_pair_prepare(int N0, int N1);
+void volume_pair_prepare(int N0, int N1, int ty);
 void launch_modal(const ModalParams& p, cudaStream_t s);
 int launch_iface(const IfaceParams& p, cudaStream_t s);   // returns the number of kernel launches
 bool iface_uses_dzf(int Nf, int Nc, int R, int lg);       // the interface path that reads IfaceParams::dzf
@@ -497,6 +499,6 @@ void launch_gather(const double* src, const long long* idx, long long n, double*
 void launch_nonfinite(const double* p, long long NX, long long PX, long long rows, unsigned long long* flag,
                       cudaStream_t s);
 int volume_smem_bytes(int N);
-int volume_tile_y();
-void volume_prepare(int N);
+int volume_tile_y(bool slabs);
+void volume_prepare(int N, int ty);
 }  // namespace sem
