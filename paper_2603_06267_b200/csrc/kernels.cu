@@ -1855,6 +1855,9 @@ constexpr int curved_smem() { return 8 * (curved_epb<N>() * (4 * (N + 1) * (N + 
 #ifndef SEM_CV_MINB
 #define SEM_CV_MINB 2
 #endif
+#ifndef SEM_CV_LINES
+#define SEM_CV_LINES 1   // y / z derivatives and their transposes by line passes (0: every x-line reads
+#endif                   // its y- and z-neighbour lines from shared memory, the round-1 form)
 
 
 template <int N>
@@ -1906,8 +1909,49 @@ __global__ void __launch_bounds__(curved_threads<N>(), SEM_CV_MINB) curved_resid
         cp_async_commit();
         const double* sp = spb + (k * EPB + el) * nl;
         const double* Xv = Xvb + (k * EPB + el) * 24;
+        double* const f1 = sf1 + el * nl;
+        double* const f2 = sf2 + el * nl;
         // ---- reference gradient on the line
         double cur[n1], gx[n1], gy[n1], gz[n1];
+#if SEM_CV_LINES
+        // y and z derivatives by line passes: thread ln also acts as the y-line (a, c) and the z-line
+        // (a, b) with (a, c|b) = (ln % n1, ln / n1); the output index is a compile-time loop index, so the
+        // D entries are immediates and each line is read once (6 + 6 loads instead of 36 + 36)
+        {
+            const int la = ln % n1, lo = ln / n1;
+            double vy[n1], vz[n1];
+#pragma unroll
+            for (int j = 0; j <= N; ++j) {
+                vy[j] = sp[la + n1 * (j + n1 * lo)];
+                vz[j] = sp[la + n1 * (lo + n1 * j)];
+            }
+#pragma unroll
+            for (int i = 0; i <= N; ++i) {
+                double sy = 0.0, sz = 0.0;
+#pragma unroll
+                for (int j = 0; j <= N; ++j) {
+                    sy = fma(RT.D[i][j], vy[j], sy);
+                    sz = fma(RT.D[i][j], vz[j], sz);
+                }
+                f1[la + n1 * (i + n1 * lo)] = sy;
+                f2[la + n1 * (lo + n1 * i)] = sz;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a <= N; ++a) {
+            cur[a] = sp[a + n1 * ln];
+            gy[a] = f1[a + n1 * ln];
+            gz[a] = f2[a + n1 * ln];
+        }
+#pragma unroll
+        for (int a = 0; a <= N; ++a) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j <= N; ++j) s = fma(RT.D[a][j], cur[j], s);
+            gx[a] = s;
+        }
+#else
 #pragma unroll
         for (int a = 0; a <= N; ++a) cur[a] = sp[a + n1 * ln];
 #pragma unroll
@@ -1928,6 +1972,7 @@ __global__ void __launch_bounds__(curved_threads<N>(), SEM_CV_MINB) curved_resid
                 gz[a] = fma(dzj, sp[a + n1 * (b + n1 * j)], gz[a]);
             }
         }
+#endif
         // ---- Jacobian pieces of the line: J[:,0] constant, J[:,1] = P1 + xi Q1, J[:,2] = P2 + xi Q2
         double J0[3], P1[3], Q1[3], P2[3], Q2[3];
 #pragma unroll
@@ -1943,9 +1988,7 @@ __global__ void __launch_bounds__(curved_threads<N>(), SEM_CV_MINB) curved_resid
             P2[i] = 0.5 * fma(ly1, s3 - s1, ly0 * (s2 - s0));
             Q2[i] = 0.5 * fma(ly1, h3 - h1, ly0 * (h2 - h0));
         }
-        double f0[n1];
-        double* const f1 = sf1 + el * nl;
-        double* const f2 = sf2 + el * nl;
+        double f0[n1];   // f1 / f2 overwrite this line's own gy / gz entries (already in registers)
 #pragma unroll
         for (int a = 0; a <= N; ++a) {
             const double xa = RT.x[a];
@@ -1986,6 +2029,33 @@ __global__ void __launch_bounds__(curved_threads<N>(), SEM_CV_MINB) curved_resid
             for (int j = 0; j <= N; ++j) s = fma(RT.D[j][a], f0[j], s);
             r[a] = s;
         }
+#if SEM_CV_LINES
+        // D^T along y and z by the same line passes, in place (a line's entries are read by its own
+        // thread only), then the x-line adds its two entries
+        {
+            const int la = ln % n1, lo = ln / n1;
+            double vy[n1], vz[n1];
+#pragma unroll
+            for (int j = 0; j <= N; ++j) {
+                vy[j] = f1[la + n1 * (j + n1 * lo)];
+                vz[j] = f2[la + n1 * (lo + n1 * j)];
+            }
+#pragma unroll
+            for (int i = 0; i <= N; ++i) {
+                double sy = 0.0, sz = 0.0;
+#pragma unroll
+                for (int j = 0; j <= N; ++j) {
+                    sy = fma(RT.D[j][i], vy[j], sy);
+                    sz = fma(RT.D[j][i], vz[j], sz);
+                }
+                f1[la + n1 * (i + n1 * lo)] = sy;
+                f2[la + n1 * (lo + n1 * i)] = sz;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a <= N; ++a) r[a] += f1[a + n1 * ln] + f2[a + n1 * ln];
+#else
 #pragma unroll
         for (int j = 0; j <= N; ++j) {
             const double dyj = Ds[j * n1 + b], dzj = Ds[j * n1 + c];
@@ -1995,6 +2065,7 @@ __global__ void __launch_bounds__(curved_threads<N>(), SEM_CV_MINB) curved_resid
                 r[a] = fma(dzj, f2[a + n1 * (b + n1 * j)], r[a]);
             }
         }
+#endif
         if (g0 >= 0) {
 #pragma unroll
             for (int a = 0; a <= N; ++a) atomicAdd(p.res + g0 + a, r[a]);
