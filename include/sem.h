@@ -149,13 +149,13 @@ typedef struct {
 sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pm);
 
 /* Host-only (no device touched): the y-slab plan of `world` slabs for these global boxes and (optional)
- * PMUT array.  slab_x0[world+1] receives the box-0 element y index where each slab starts: equal slabs
+ * PMUT array.  slab_y0[world+1] receives the box-0 element y index where each slab starts: equal slabs
  * when they are admissible, else the admissible cuts nearest to the equal ones (uneven slabs): every cut
  * on an element boundary of every box (so a 2:1 interface's face pairs stay slab-local) and in a gap
  * between membranes (the paper's membrane-preserving partition).  SEM_E_PARTITION if
  * no admissible plan exists. */
 sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, const sem_pmut_desc* pm,
-                         long long* slab_x0);
+                         long long* slab_y0);
 
 /* Non-conforming SIPG interface between the +z face of `fine_box` and the -z face of
  * `coarse_box` (Eq. 7's three Gamma_I sums), gamma_F = penalty_alpha cbar^2

@@ -1246,13 +1246,13 @@ sem_status sem_nccl_unique_id(void* out) {
 }
 
 sem_status sem_slab_plan(const sem_box_desc* boxes, int n_boxes, int world, const sem_pmut_desc* pm,
-                         long long* slab_x0) {
+                         long long* slab_y0) {
     if (!boxes || n_boxes < 1 || n_boxes > 2 || world < 1) return SEM_E_ARG;
     if (pm && (pm->box < 0 || pm->box >= n_boxes || !pm->center)) return SEM_E_ARG;
     std::vector<long long> cuts;
     if (!auto_plan(boxes, n_boxes, world, pm, cuts)) return SEM_E_PARTITION;
-    if (slab_x0)
-        for (int r = 0; r <= world; ++r) slab_x0[r] = cuts[r];
+    if (slab_y0)
+        for (int r = 0; r <= world; ++r) slab_y0[r] = cuts[r];
     return SEM_OK;
 }
 
