@@ -113,13 +113,18 @@ def penalty_gamma(c_plus, c_minus, r_in, r_out, h_in, h_out, alpha):
 
 
 def mode_shape(pm, k, m, x, y):
-    """S_{k,m}(x, y) = sin(m pi x'/a) sin(n pi y'/a) on the square membrane, 0 outside (reading R19)."""
+    """S_{k,m}(x, y) = sin(m pi x'/a) sin(n pi y'/a) on the square membrane, 0 outside (reading R19).
+    With pm["shape_fn"] (an input: the paper's U_{k,m} are FEM eigenmodes; reading R33)
+    S_{k,m}(x, y) = shape_fn(k, m, x - cx, y - cy) inside the membrane's bounding square, 0 outside."""
     a = pm["side"]
     cx, cy = pm["centers"][k]
     mm, nn = pm["mode_mn"][m]
     xl = x - (cx - a / 2)
     yl = y - (cy - a / 2)
     inside = (xl >= 0) & (xl <= a) & (yl >= 0) & (yl <= a)
+    if pm.get("shape_fn") is not None:
+        s = np.array([pm["shape_fn"](k, m, float(xv - cx), float(yv - cy)) for xv, yv in zip(x, y)], dtype=np.float64)
+        return np.where(inside, s, 0.0)
     return np.where(inside, np.sin(mm * math.pi * xl / a) * np.sin(nn * math.pi * yl / a), 0.0)
 
 

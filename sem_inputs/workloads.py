@@ -496,3 +496,51 @@ def curved_pmut_config(nel=(6, 6, 4), degree=4, h=25e-6, amp=0.12, floor_jitter=
     cx, cy = extent[0] / 2, extent[1] / 2
     rec["pmut"] = _pmut([[cx, cy]], MODES_3, FREQS_3, None, [0.0], rx=rx)
     return rec
+
+
+def clamped_disc_shape(radius, modes=((0, 1), (1, 1), (0, 2))):
+    """Mode shapes of a clamped circular plate of radius `radius` -- an INPUT of the method (the paper
+    takes U_{k,m} from a 3D FEM eigen-analysis of the membrane; this textbook family
+    stands in for it on the circular membranes of P:L1097, reading R33): for (n, s)
+      S(r, theta) = cos(n theta) [J_n(l r/R) - J_n(l)/I_n(l) I_n(l r/R)] / max,  r <= R, else 0,
+    l = the s-th positive root of J_n(l) I_{n+1}(l) + I_n(l) J_{n+1}(l) (S = dS/dr = 0 at r = R).
+    Returns shape_fn(k, m, x_rel, y_rel) -> float for oracle and C ABI alike."""
+    from scipy.optimize import brentq
+    from scipy.special import iv, jv
+
+    lam, scale = [], []
+    for n, s in modes:
+        f = lambda l, n=n: jv(n, l) * iv(n + 1, l) + iv(n, l) * jv(n + 1, l)
+        grid = np.linspace(0.5, 40.0, 4000)
+        v = f(grid)
+        roots = [brentq(f, grid[i], grid[i + 1], xtol=1e-15) for i in range(len(grid) - 1) if v[i] * v[i + 1] < 0]
+        l = roots[s - 1]
+        rr = np.linspace(0.0, 1.0, 2001)
+        prof = jv(n, l * rr) - jv(n, l) / iv(n, l) * iv(n, l * rr)
+        lam.append(l)
+        scale.append(1.0 / np.abs(prof).max())
+
+    def shape_fn(k, m, xr, yr):
+        r = math.hypot(xr, yr) / radius
+        if r > 1.0:
+            return 0.0
+        n, l = modes[m][0], lam[m]
+        ang = math.cos(n * math.atan2(yr, xr)) if n else 1.0
+        return float(scale[m] * ang * (jv(n, l * r) - jv(n, l) / iv(n, l) * iv(n, l * r)))
+
+    shape_fn.lam = tuple(lam)
+    shape_fn.scale = tuple(scale)
+    return shape_fn
+
+
+def circular_pmut_config(radius=65 * UM, nel=(6, 6, 4), degree=4, h=25e-6, rx=False, n_steps=300, **kw):
+    """curved_pmut_config's box (bulged, jittered vertex lattice, in-plane jitter on the membrane face)
+    carrying one CIRCULAR membrane of radius r_p = 65 um with clamped_disc_shape's modes
+    (reading R33) instead of the square sines; `side` is the bounding square 2 r_p."""
+    rec = curved_pmut_config(nel=nel, degree=degree, h=h, rx=rx, n_steps=n_steps, **kw)
+    rec["name"] = "circular_pmut"
+    modes = ((0, 1), (1, 1), (0, 2))
+    rec["pmut"]["side"] = 2.0 * radius
+    rec["pmut"]["mode_mn"] = np.asarray(modes, np.int32)
+    rec["pmut"]["shape_fn"] = clamped_disc_shape(radius, modes)
+    return rec

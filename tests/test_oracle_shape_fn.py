@@ -1,0 +1,64 @@
+"""Pins for caller-defined mode shapes in the oracle's coupling table (reading R33; Eqs. 11-12 with
+U_{k,m} an input): B_{k,m,j} = sum_F w_q |J_s| S_{k,m}(x_j) must reproduce closed-form
+integrals of the shape -- exactly for a polynomial on a membrane aligned with element boundaries (GLL
+exactness), including its first moments (which fix the sign and the x / y order of the arguments the
+shape is called with), and up to the quadrature error for the clamped circular plate of P:L1097."""
+import math
+
+import numpy as np
+from scipy.special import iv, jv
+
+from oracle.operators import System
+from sem_inputs import circular_pmut_config, clamped_disc_shape, curved_pmut_config
+
+
+def test_polynomial_shape_integrates_exactly():
+    # 6 x 6 face elements of 25 um, N = 4; membrane = the 4 x 4 central elements (side 100 um)
+    rec = curved_pmut_config(amp=0.0, floor_jitter=0.0)
+    a = 100e-6
+    cfs = (0.0, 0.8, -1.7)
+
+    def shape(k, m, xr, yr):      # vanishes on the square's edge; degree 3 in x, 4 in y
+        u, v = 2 * xr / a, 2 * yr / a
+        return (1 - u * u) * (1 - v * v) * (1 + cfs[m] * u + 0.5 * cfs[m] * v * v)
+
+    rec["pmut"]["side"] = a
+    rec["pmut"]["shape_fn"] = shape
+    s = System(rec)
+    xyz = s.node_coords()
+    cx, cy = rec["pmut"]["centers"][0]
+    one = np.ones(s.ndof)
+    G0 = s.pmut_project(one)[0]
+    Gx = s.pmut_project(xyz[:, 0] - cx)[0]
+    Gy = s.pmut_project(xyz[:, 1] - cy)[0]
+    for m, c in enumerate(cfs):
+        # int (1-u^2)(1 + c u) (a/2) du = 2a/3;  int (1-v^2)(1 + c/2 v^2) (a/2) dv = (a/2)(4/3 + (c/2)(4/15))
+        i0 = (2 * a / 3) * (a / 2) * (4 / 3) + (2 * a / 3) * (a / 2) * (0.5 * c) * (4 / 15)
+        # x moment: only the c u term survives: (a/2)^2 c int (1-u^2) u^2 du = (a^2/4) c (4/15), times (a/2)(4/3)
+        ix = (a * a / 4) * c * (4 / 15) * (a / 2) * (4 / 3)
+        assert abs(G0[m] - i0) < 1e-13 * a * a, (m, G0[m], i0)
+        assert abs(Gx[m] - ix) < 1e-13 * a ** 3, (m, Gx[m], ix)
+        assert abs(Gy[m]) < 1e-13 * a ** 3
+
+
+def test_clamped_disc_modes_and_their_integrals():
+    R = 65e-6
+    modes = ((0, 1), (1, 1), (0, 2))
+    f = clamped_disc_shape(R, modes)
+    # textbook eigenvalues of the clamped circular plate (lambda_01, lambda_11, lambda_02)
+    assert np.allclose(f.lam, (3.19622, 4.61090, 6.30644), atol=1e-5)
+    # clamped: S = dS/dr = 0 at r = R; unit peak
+    for m in range(3):
+        assert abs(f(0, m, R, 0.0)) < 1e-14
+        assert abs(f(0, m, R * (1 - 1e-6), 0.0)) < 1e-10
+        assert f(0, m, 0.0, 1.0001 * R) == 0.0
+    assert abs(f(0, 0, 0.0, 0.0) - 1.0) < 1e-12 and abs(f(0, 1, 0.3 * R, 0.0) + f(0, 1, -0.3 * R, 0.0)) < 1e-15
+    assert abs(f(0, 1, 0.0, 0.4 * R)) < 1e-15      # cos(theta) nodal line on the y axis
+    rec = circular_pmut_config(amp=0.0, floor_jitter=0.0, degree=5)
+    s = System(rec)
+    G = s.pmut_project(np.ones(s.ndof))[0]
+    for m, (n, _) in enumerate(modes):
+        l = f.lam[m]
+        exact = 0.0 if n else 2 * math.pi * R * R * f.scale[m] * (jv(1, l) - jv(0, l) / iv(0, l) * iv(1, l)) / l
+        assert abs(G[m] - exact) < 2e-3 * math.pi * R * R, (m, G[m], exact)
+    assert abs(G[0]) > 0.25 * math.pi * R * R
