@@ -127,8 +127,16 @@ sem_status sem_nccl_unique_id(void* out128);
  * curved box (sem_box_set_vertices, called first): there the coupling is tabulated per membrane node,
  * B_{k,m,j} = sum_F w_a w_b |J_s| S_{k,m}(x_j) with the trilinear face's |J_s| and physical node
  * positions (not separable), and the force enters the box's assembled residual.
+ * Caller-defined mode shapes (the paper's U_{k,m} are the eigenmodes of a 3D FEM model of the
+ * membrane, so any shape must be admissible -- e.g. the circular membranes of P:L1097, reading
+ * R33): with shape_fn != NULL the table uses S_{k,m}(x_j) = shape_fn(k, m, x_j - center_x, y_j -
+ * center_y, shape_user) instead of the square sines; it is called on the host during this call only,
+ * for the face nodes inside the membrane's bounding square of side `side` (S = 0 outside it; a disc's
+ * shape returns 0 beyond its radius); mode_mn is then only a label.  Needs the tabulated coupling, i.e.
+ * a curved box (sem_box_set_vertices, possibly with the affine lattice): SEM_E_ARG on any other box.
  * Errors: SEM_E_ARG (membranes overlapping or off the face, zero-node membrane, membrane on a solid
- * element's face, rx with C <= 0), SEM_E_STATE (already attached). */
+ * element's face, rx with C <= 0, a non-finite shape value), SEM_E_STATE (already attached). */
+typedef double (*sem_shape_fn)(int k, int m, double x_rel, double y_rel, void* user);
 typedef struct {
     int box, face;
     int n_pmut, n_modes;
@@ -145,6 +153,8 @@ typedef struct {
     double amp_v, f0_hz;          /* TX burst amplitude [V] and carrier [Hz]             */
     int n_cycles;
     const double* delay_s;
+    sem_shape_fn shape_fn;        /* NULL: the square sines of mode_mn (reading R19)     */
+    void* shape_user;
 } sem_pmut_desc;
 sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pm);
 

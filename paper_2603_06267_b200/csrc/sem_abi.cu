@@ -1214,7 +1214,10 @@ sem_status pmut_tables(sem_ctx* ctx, sem::Part& pt, Box& b, const sem_pmut_desc&
                 std::vector<double> row(M);
                 bool nz = false;
                 for (int m = 0; m < M; ++m) {
-                    const double S = std::sin(pd.mode_mn[2 * m] * M_PI * xl / a) * std::sin(pd.mode_mn[2 * m + 1] * M_PI * yl / a);
+                    const double S = pd.shape_fn
+                                         ? pd.shape_fn(k, m, fx[j] - pd.center[2 * k], fy[j] - pd.center[2 * k + 1], pd.shape_user)
+                                         : std::sin(pd.mode_mn[2 * m] * M_PI * xl / a) * std::sin(pd.mode_mn[2 * m + 1] * M_PI * yl / a);
+                    if (!std::isfinite(S)) return fail(ctx, SEM_E_ARG, "shape_fn returned a non-finite value");
                     row[m] = fw[j] * S;
                     nz = nz || S != 0.0;
                 }
@@ -1431,6 +1434,8 @@ sem_status sem_pmut_attach(sem_ctx* ctx, const sem_pmut_desc* pd) {
                                     return fail(ctx, SEM_E_ARG, "membrane on the face of an obstacle element");
             }
         }
+        if (pd->shape_fn && !b.verts_set)
+            return fail(ctx, SEM_E_ARG, "caller-defined mode shapes need the tabulated coupling of a curved box (sem_box_set_vertices first)");
         if (b.verts_set) {   // curved box: tabulated coupling
             st = pmut_tables(ctx, pt, b, *pd, ks);
             if (st) return st;

@@ -65,6 +65,9 @@ class FaceSet(C.Structure):
     _fields_ = [("n", C.c_int), ("verts", C.POINTER(C.c_double)), ("face", C.POINTER(C.c_int))]
 
 
+SHAPE_FN = C.CFUNCTYPE(C.c_double, C.c_int, C.c_int, C.c_double, C.c_double, C.c_void_p)
+
+
 class PmutDesc(C.Structure):
     _fields_ = [("box", C.c_int), ("face", C.c_int), ("n_pmut", C.c_int), ("n_modes", C.c_int),
                 ("center", C.POINTER(C.c_double)), ("side", C.c_double), ("mode_mn", C.POINTER(C.c_int)),
@@ -72,7 +75,7 @@ class PmutDesc(C.Structure):
                 ("damping_ratio", C.POINTER(C.c_double)), ("eta", C.POINTER(C.c_double)),
                 ("rx", C.c_int), ("t_switch", C.c_double), ("capacitance", C.c_double),
                 ("amp_v", C.c_double), ("f0_hz", C.c_double), ("n_cycles", C.c_int),
-                ("delay_s", C.POINTER(C.c_double))]
+                ("delay_s", C.POINTER(C.c_double)), ("shape_fn", SHAPE_FN), ("shape_user", C.c_void_p)]
 
 
 def _load():
@@ -204,6 +207,10 @@ def _pmut_desc(pm):
                  float(pm["t_switch"]) if math.isfinite(pm["t_switch"]) else 1e300,
                  float(pm["capacitance"]), float(pm["amp_v"]), float(pm["f0_hz"]), int(pm["n_cycles"]),
                  _dptr(keep["delay"]))
+    if pm.get("shape_fn") is not None:     # caller-defined mode shapes (sem.h, reading R33): passed through
+        fn = pm["shape_fn"]
+        keep["shape_fn"] = SHAPE_FN(lambda k, m, xr, yr, _user: float(fn(k, m, xr, yr)))
+        d.shape_fn = keep["shape_fn"]
     return d, keep
 
 

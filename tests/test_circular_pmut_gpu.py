@@ -1,0 +1,52 @@
+"""GPU parity of a circular membrane (r_p = 65 um) with caller-defined mode shapes
+(sem_pmut_desc.shape_fn, reading R33: clamped circular plate modes standing in for the paper's FEM
+eigenmodes) on a curved box: TX run, RX from a random state, and the error paths."""
+import numpy as np
+import pytest
+
+from sem_inputs import circular_pmut_config, config, random_state
+
+from parity import TOL, compare, gpu_run, oracle_run
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def test_circular_pmut_tx():
+    rec = circular_pmut_config()
+    nm = oracle_run(rec, rec["n_steps"])
+    sim = gpu_run(rec, rec["n_steps"], chunks=[100, 99, 101])
+    r = compare(sim, nm)
+    assert np.abs(nm.p).max() > 1.0 and np.abs(nm.q).max() > 1e-13
+    assert np.abs(nm.q[0, 2]) > 0.0       # the second axisymmetric mode is driven too
+    for k, v in r.items():
+        assert v < TOL, (k, v, r)
+
+
+def test_circular_pmut_rx_random_state():
+    rec = circular_pmut_config(rx=True, n_steps=60)
+    st = random_state(rec, seed=23)
+    for n in (1, 5, 60):
+        nm = oracle_run(rec, n, state=st)
+        sim = gpu_run(rec, n, state=st)
+        r = compare(sim, nm)
+        assert n == 1 or np.abs(nm.q).max() > 0.0
+        if n == 60:
+            assert np.abs(nm.q[0, 1]) > 0.0   # the cos(theta) mode sees the rough field
+        for k, v in r.items():
+            assert v < TOL, (n, k, v, r)
+        sim.close()
+
+
+def test_shape_fn_needs_a_curved_box():
+    from paper_2603_06267_b200.sem import SemError, Simulation
+    rec = config(0)
+    rec["pmut"]["shape_fn"] = lambda k, m, xr, yr: 1.0
+    with pytest.raises(SemError):
+        Simulation(rec)
