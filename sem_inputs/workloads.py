@@ -544,3 +544,33 @@ def circular_pmut_config(radius=65 * UM, nel=(6, 6, 4), degree=4, h=25e-6, rx=Fa
     rec["pmut"]["mode_mn"] = np.asarray(modes, np.int32)
     rec["pmut"]["shape_fn"] = clamped_disc_shape(radius, modes)
     return rec
+
+
+def cylinder_pmut_config(domain_radius=90 * UM, radius=65 * UM, nel=(6, 6, 4), degree=4, height=100 * UM, rx=False,
+                         n_steps=300, cfl=0.25):
+    """A cylindrical water column (the cylinder domains of P:L1225) as ONE logically structured box: the
+    square vertex lattice [-1, 1]^2 is mapped onto the disc by (x, y) -> (x sqrt(1 - y^2/2),
+    y sqrt(1 - x^2/2)) R in every z layer (an extruded cylinder whose rigid wall is the polygon through
+    the mapped boundary vertices; the four corner elements have one 180 deg - 90 deg/nel angle, so the
+    lattice stays coarse; dt = cfl min(0.75 h, h_z) / (c N^2) is half the stability limit, pinned in the tests), absorbing top, one circular membrane r_p = 65 um
+     with clamped_disc_shape's modes centred on the floor."""
+    h = 2.0 * domain_radius / nel[0]
+    rec = curved_pmut_config(nel=nel, degree=degree, h=h, amp=0.0, floor_jitter=0.0, rx=rx, n_steps=n_steps, cfl=cfl)
+    rec["name"] = "cylinder_pmut"
+    b = rec["boxes"][0]
+    ext = (2.0 * domain_radius, 2.0 * domain_radius * nel[1] / nel[0], height)
+    gx, gy, gz = [np.linspace(0.0, e, n + 1) for e, n in zip(ext, nel)]
+    Z, Y, X = np.meshgrid(gz, gy, gx, indexing="ij")
+    u = X / domain_radius - 1.0
+    v = Y / (0.5 * ext[1]) - 1.0
+    b["extent"] = ext
+    b["vertices"] = np.stack([(1.0 + u * np.sqrt(1.0 - 0.5 * v * v)) * domain_radius,
+                              (1.0 + v * np.sqrt(1.0 - 0.5 * u * u)) * 0.5 * ext[1], Z], axis=-1).reshape(-1, 3)
+    hz = height / nel[2]
+    rec["dt"] = cfl * min(0.75 * h, hz) / (b["c"] * degree ** 2)
+    modes = ((0, 1), (1, 1), (0, 2))
+    rec["pmut"]["centers"] = np.array([[domain_radius, 0.5 * ext[1]]])
+    rec["pmut"]["side"] = 2.0 * radius
+    rec["pmut"]["mode_mn"] = np.asarray(modes, np.int32)
+    rec["pmut"]["shape_fn"] = clamped_disc_shape(radius, modes)
+    return rec

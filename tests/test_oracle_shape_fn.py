@@ -62,3 +62,32 @@ def test_clamped_disc_modes_and_their_integrals():
         exact = 0.0 if n else 2 * math.pi * R * R * f.scale[m] * (jv(1, l) - jv(0, l) / iv(0, l) * iv(1, l)) / l
         assert abs(G[m] - exact) < 2e-3 * math.pi * R * R, (m, G[m], exact)
     assert abs(G[0]) > 0.25 * math.pi * R * R
+
+
+def test_cylinder_domain_geometry_and_stability():
+    """The cylinder column of P:L1225 as one mapped box: the lumped mass sums to the volume of the
+    extruded polygon through the mapped boundary vertices (shoelace area x height, exact for the
+    trilinear map), the absorbing top's ABC diagonal to c x that area, K 1 = 0, and the record's time step
+    is inside the leapfrog stability limit of this mesh."""
+    from sem_inputs import cylinder_pmut_config
+    rec = cylinder_pmut_config(n_steps=120)
+    b = rec["boxes"][0]
+    nx, ny, nz = b["nel"]
+    V = b["vertices"].reshape(nz + 1, ny + 1, nx + 1, 3)[0, :, :, :2]
+    ring = np.concatenate([V[0, :-1], V[:-1, -1], V[-1, :0:-1], V[:0:-1, 0]])       # counter-clockwise boundary
+    area = 0.5 * abs(np.sum(ring[:, 0] * np.roll(ring[:, 1], -1) - np.roll(ring[:, 0], -1) * ring[:, 1]))
+    R = 0.5 * b["extent"][0]
+    assert np.allclose(np.hypot(ring[:, 0] - R, ring[:, 1] - R), R, rtol=1e-12)      # wall vertices on the circle
+    assert 0.93 * math.pi * R * R < area < math.pi * R * R
+    s = System(rec)
+    H = b["extent"][2]
+    assert abs(s.M.sum() - area * H) < 1e-12 * area * H
+    assert abs(s.C.sum() - b["c"] * area) < 1e-12 * b["c"] * area
+    assert np.abs(s.apply_K(np.ones(s.ndof))).max() < 1e-10 * b["c"] ** 2 * area * H / (H / nz) ** 2
+    # stability of the record's time step: dt < 2 / sqrt(lambda_max(M^-1 K)) (power iteration), margin >= 1.5
+    v = np.random.default_rng(0).standard_normal(s.ndof)
+    for _ in range(150):
+        w = s.apply_K(v) / s.M
+        lam = np.linalg.norm(w) / np.linalg.norm(v)
+        v = w / np.linalg.norm(w)
+    assert rec["dt"] * math.sqrt(lam) / 2 < 0.67, rec["dt"] * math.sqrt(lam) / 2
