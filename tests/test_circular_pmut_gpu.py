@@ -50,3 +50,18 @@ def test_shape_fn_needs_a_curved_box():
     rec["pmut"]["shape_fn"] = lambda k, m, xr, yr: 1.0
     with pytest.raises(SemError):
         Simulation(rec)
+
+
+def test_cylinder_domain_circular_pmut():
+    """The cylinder column of P:L1225 (one box mapped onto the disc, rigid wall, absorbing top) with the
+    circular membrane transmitting, then receiving its own field (TX -> RX switch)."""
+    from sem_inputs import cylinder_pmut_config
+    rec = cylinder_pmut_config(n_steps=400)
+    rec["pmut"]["rx"] = True
+    rec["pmut"]["t_switch"] = 250 * rec["dt"]
+    nm = oracle_run(rec, rec["n_steps"])
+    sim = gpu_run(rec, rec["n_steps"], chunks=[150, 101, 149])
+    r = compare(sim, nm)
+    assert np.abs(nm.p).max() > 1.0 and np.abs(nm.q).max() > 1e-13
+    for k, v in r.items():
+        assert v < TOL, (k, v, r)
