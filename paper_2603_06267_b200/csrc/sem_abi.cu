@@ -1193,25 +1193,43 @@ sem_status pmut_tables(sem_ctx* ctx, sem::Part& pt, Box& b, const sem_pmut_desc&
     std::vector<double> B;
     std::vector<int> used((size_t)b.NX * b.NY, -1);
     const double a = pd.side;
-    // candidate nodes of a membrane: its square on the affine lattice widened by two elements (a vertex
-    // lattice moves the nodes by less than an element)
-    const double hx = g.extent[0] / g.nel[0], hy = g.extent[1] / g.nel[1];
-    auto lat_range = [](double lo, double hi, double org, double h, int N, long long n, long long& i0, long long& i1) {
-        i0 = std::max<long long>(0, (long long)std::floor((lo - org) / h - 2.0) * N);
-        i1 = std::min<long long>(n - 1, (long long)std::ceil((hi - org) / h + 2.0) * N);
-    };
+    // candidate nodes of a membrane: the face nodes whose PHYSICAL position lies in its square, whatever
+    // the vertex lattice does to the node positions (a mapped lattice, e.g. square -> disc, moves nodes by
+    // several elements).  Membranes are binned on a uniform grid of cell size a (a square meets <= 4
+    // cells per axis pair), every node looks its cell up; nodes are visited in lattice order (y, then x),
+    // so each membrane's rows keep that order.
+    double bx0 = 1e300, by0 = 1e300, bx1 = -1e300, by1 = -1e300;
+    for (int l = 0; l < KL; ++l) {
+        const int k = ks[l];
+        bx0 = std::min(bx0, pd.center[2 * k] - 0.5 * a);
+        by0 = std::min(by0, pd.center[2 * k + 1] - 0.5 * a);
+        bx1 = std::max(bx1, pd.center[2 * k] + 0.5 * a);
+        by1 = std::max(by1, pd.center[2 * k + 1] + 0.5 * a);
+    }
+    const long long gnx = std::max<long long>(1, (long long)std::ceil((bx1 - bx0) / a)) + 1,
+                    gny = std::max<long long>(1, (long long)std::ceil((by1 - by0) / a)) + 1;
+    std::vector<std::vector<int>> cell((size_t)(gnx * gny));
     for (int l = 0; l < KL; ++l) {
         const int k = ks[l];
         const double x0 = pd.center[2 * k] - 0.5 * a, y0 = pd.center[2 * k + 1] - 0.5 * a;
-        long long ix0, ix1, iy0, iy1;
-        lat_range(x0, x0 + a, g.origin[0], hx, N, b.NX, ix0, ix1);
-        lat_range(y0, y0 + a, g.origin[1], hy, N, b.NY, iy0, iy1);
-        for (long long jy = iy0; jy <= iy1; ++jy)
-            for (long long jx = ix0; jx <= ix1; ++jx) {
-                const size_t j = (size_t)jy * b.NX + (size_t)jx;
-                const double xl = fx[j] - x0, yl = fy[j] - y0;
+        const long long cx0 = std::max<long long>(0, (long long)std::floor((x0 - bx0) / a) - 1),
+                        cy0 = std::max<long long>(0, (long long)std::floor((y0 - by0) / a) - 1);
+        for (long long cy = cy0; cy <= std::min(gny - 1, cy0 + 3); ++cy)
+            for (long long cx = cx0; cx <= std::min(gnx - 1, cx0 + 3); ++cx) cell[(size_t)(cy * gnx + cx)].push_back(l);
+    }
+    std::vector<std::vector<long long>> midx(KL);
+    std::vector<std::vector<double>> mB(KL);
+    std::vector<double> row(M);
+    for (long long jy = 0; jy < b.NY; ++jy)
+        for (long long jx = 0; jx < b.NX; ++jx) {
+            const size_t j = (size_t)jy * b.NX + (size_t)jx;
+            if (!(fx[j] >= bx0 && fx[j] <= bx1 && fy[j] >= by0 && fy[j] <= by1)) continue;
+            const long long cx = std::min(gnx - 1, (long long)std::floor((fx[j] - bx0) / a)),
+                            cy = std::min(gny - 1, (long long)std::floor((fy[j] - by0) / a));
+            for (int l : cell[(size_t)(cy * gnx + cx)]) {
+                const int k = ks[l];
+                const double xl = fx[j] - (pd.center[2 * k] - 0.5 * a), yl = fy[j] - (pd.center[2 * k + 1] - 0.5 * a);
                 if (!(xl >= 0 && xl <= a && yl >= 0 && yl <= a)) continue;
-                std::vector<double> row(M);
                 bool nz = false;
                 for (int m = 0; m < M; ++m) {
                     const double S = pd.shape_fn
@@ -1224,9 +1242,13 @@ sem_status pmut_tables(sem_ctx* ctx, sem::Part& pt, Box& b, const sem_pmut_desc&
                 if (!nz) continue;
                 if (used[j] >= 0) return fail(ctx, SEM_E_ARG, "membranes overlap");
                 used[j] = l;
-                idx.push_back((long long)(j / b.NX) * b.PX + (long long)(j % b.NX));   // pitched, plane z = 0
-                B.insert(B.end(), row.begin(), row.end());
+                midx[l].push_back((long long)(j / b.NX) * b.PX + (long long)(j % b.NX));   // pitched, plane z = 0
+                mB[l].insert(mB[l].end(), row.begin(), row.end());
             }
+        }
+    for (int l = 0; l < KL; ++l) {
+        idx.insert(idx.end(), midx[l].begin(), midx[l].end());
+        B.insert(B.end(), mB[l].begin(), mB[l].end());
         off[l + 1] = (int)idx.size();
         if (off[l + 1] == off[l]) return fail(ctx, SEM_E_ARG, "membrane with no face node");
     }

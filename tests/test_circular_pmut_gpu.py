@@ -65,3 +65,22 @@ def test_cylinder_domain_circular_pmut():
     assert np.abs(nm.p).max() > 1.0 and np.abs(nm.q).max() > 1e-13
     for k, v in r.items():
         assert v < TOL, (k, v, r)
+
+
+def test_cylinder_fine_lattice_offcentre_membrane():
+    """A 16 x 16 mapped lattice moves the face nodes near the corners by more than two elements: the
+    coupling table must pick a membrane's nodes by their physical positions (a small off-centre disc
+    towards the mapped corner), not from the affine lattice."""
+    from sem_inputs import clamped_disc_shape, cylinder_pmut_config
+    rec = cylinder_pmut_config(nel=(16, 16, 2), degree=3, height=40e-6, n_steps=80, cfl=0.1)
+    R, r = 90e-6, 15e-6
+    modes = ((0, 1), (1, 1), (0, 2))
+    rec["pmut"]["centers"] = np.array([[R + 0.55 * R, R + 0.55 * R]])
+    rec["pmut"]["side"] = 2 * r
+    rec["pmut"]["shape_fn"] = clamped_disc_shape(r, modes)
+    nm = oracle_run(rec, rec["n_steps"])
+    sim = gpu_run(rec, rec["n_steps"])
+    r_ = compare(sim, nm)
+    assert np.abs(nm.q).max() > 0.0 and np.abs(nm.p).max() > 0.0
+    for k, v in r_.items():
+        assert v < TOL, (k, v, r_)
