@@ -574,3 +574,50 @@ def cylinder_pmut_config(domain_radius=90 * UM, radius=65 * UM, nel=(6, 6, 4), d
     rec["pmut"]["mode_mn"] = np.asarray(modes, np.int32)
     rec["pmut"]["shape_fn"] = clamped_disc_shape(radius, modes)
     return rec
+
+
+def cylinder_two_box_config(domain_radius=90 * UM, radius=65 * UM, nc=(4, 4, 2), ratio=2, nfz=3, degree_f=4,
+                            degree_c=3, coarse_height=90 * UM, n_steps=500, cfl=0.35, alpha=PENALTY_ALPHA):
+    """The paper's array geometry in a cylinder: a fine inner box carrying a
+    circular membrane (r_p = 65 um, clamped_disc_shape, reading R33) under a coarse outer box, both
+    mapped onto the same polygonal cylinder, joined by the general non-conforming interface.  The coarse
+    lateral vertex lattice is cylinder_pmut_config's square -> disc map; the fine one (ratio x finer) is
+    its bilinear subdivision, so every fine face lies in one coarse face (curved faces that nest) and
+    both boxes have the same polygonal wall.  Rigid wall and floor, absorbing top."""
+    ncx, ncy, ncz = nc
+    nf = (ratio * ncx, ratio * ncy, nfz)
+    hc = 2.0 * domain_radius / ncx
+    hf = hc / ratio
+    z0 = nfz * hf
+    g = np.linspace(-1.0, 1.0, ncx + 1)
+    gy = np.linspace(-1.0, 1.0, ncy + 1)
+    V, U = np.meshgrid(gy, g, indexing="ij")
+    cl = np.stack([(1.0 + U * np.sqrt(1.0 - 0.5 * V * V)) * domain_radius,
+                   (1.0 + V * np.sqrt(1.0 - 0.5 * U * U)) * domain_radius], axis=-1)       # [ncy+1][ncx+1][2]
+    fl = np.empty((nf[1] + 1, nf[0] + 1, 2))
+    for j in range(nf[1] + 1):
+        for i in range(nf[0] + 1):
+            I, Jc = min(i // ratio, ncx - 1), min(j // ratio, ncy - 1)
+            u, v = i / ratio - I, j / ratio - Jc
+            fl[j, i] = ((1 - u) * (1 - v) * cl[Jc, I] + u * (1 - v) * cl[Jc, I + 1] + (1 - u) * v * cl[Jc + 1, I] +
+                        u * v * cl[Jc + 1, I + 1])
+
+    def extrude(lat, zs):
+        out = np.empty((len(zs),) + lat.shape[:2] + (3,))
+        out[..., :2] = lat[None]
+        out[..., 2] = np.asarray(zs)[:, None, None]
+        return out.reshape(-1, 3)
+
+    L = 2.0 * domain_radius
+    fine = _box((0, 0, 0), (L, L, z0), nf, degree_f, [BC_RIGID] * 5 + [BC_INTERFACE])
+    coarse = _box((0, 0, z0), (L, L, coarse_height), nc, degree_c, [BC_RIGID] * 4 + [BC_INTERFACE, BC_ABSORBING])
+    fine["vertices"] = extrude(fl, np.arange(nfz + 1) * hf)
+    coarse["vertices"] = extrude(cl, z0 + np.arange(ncz + 1) * (coarse_height / ncz))
+    rec = {"name": "cylinder_two_box", "boxes": [fine, coarse], "n_steps": n_steps, "seed": 0,
+           "interface": {"fine_box": 0, "coarse_box": 1, "alpha": alpha}}
+    modes = ((0, 1), (1, 1), (0, 2))
+    rec["pmut"] = _pmut([[domain_radius, domain_radius]], modes, FREQS_3, None, [0.0])
+    rec["pmut"]["side"] = 2.0 * radius
+    rec["pmut"]["shape_fn"] = clamped_disc_shape(radius, modes)
+    rec["dt"] = cfl * min(0.6 * hf / degree_f ** 2, 0.6 * hc / degree_c ** 2, coarse_height / ncz / degree_c ** 2) / C_WATER
+    return _finish(rec)
