@@ -84,3 +84,16 @@ def test_cylinder_fine_lattice_offcentre_membrane():
     assert np.abs(nm.q).max() > 0.0 and np.abs(nm.p).max() > 0.0
     for k, v in r_.items():
         assert v < TOL, (k, v, r_)
+
+
+def test_cylinder_two_boxes_circular_pmut_through_the_interface():
+    """Fine inner box with the circular membrane under a coarse outer box, both on the same polygonal
+    cylinder, joined by the general non-conforming interface (Algorithm 3 on curved nested faces): the
+    burst crosses the interface within the run."""
+    from sem_inputs import cylinder_two_box_config
+    rec = cylinder_two_box_config()
+    nm = oracle_run(rec, rec["n_steps"])
+    sim = gpu_run(rec, rec["n_steps"], chunks=[200, 99, 201])
+    assert np.abs(nm.q).max() > 1e-13 and np.abs(nm.sys.split(nm.p)[1]).max() > 1e-2
+    for k, v in compare(sim, nm).items():
+        assert v < TOL, (k, v)
