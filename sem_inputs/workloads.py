@@ -621,3 +621,12 @@ def cylinder_two_box_config(domain_radius=90 * UM, radius=65 * UM, nc=(4, 4, 2),
     rec["pmut"]["shape_fn"] = clamped_disc_shape(radius, modes)
     rec["dt"] = cfl * min(0.6 * hf / degree_f ** 2, 0.6 * hc / degree_c ** 2, coarse_height / ncz / degree_c ** 2) / C_WATER
     return _finish(rec)
+
+
+def plane_wave_source(box, *, amp=1e3, f0=3.0e6, deg=20.0, azimuth_deg=0.0):
+    """Reading R13's incident wave record for any box (config 4's source; tests attach it to curved
+    boxes): direction (sin th cos az, sin th sin az, -cos th) entering through +z."""
+    pw = _plane_wave(box, amp=amp, f0=f0, deg=deg)
+    th, az = math.radians(deg), math.radians(azimuth_deg)
+    pw["direction"] = (math.sin(th) * math.cos(az), math.sin(th) * math.sin(az), -math.cos(th))
+    return pw
