@@ -196,7 +196,7 @@ sem_status sem_dg_interface_build(sem_ctx* ctx, int fine_box, int coarse_box, do
  * metric terms w_q c^2 |J| J^-1 J^-T recomputed from the 8 vertices at every GLL point (nothing
  * stored per quadrature point), FP64 atomics into an assembled residual, and a nodal kick-drift with
  * the assembled lumped mass and ABC diagonal (computed here on the host).  Call right after
- * sem_mesh_create: curved boxes carry no PML / plane wave (SEM_E_STATE); PMUTs (tabulated coupling) and
+ * sem_mesh_create: curved boxes carry no PML (SEM_E_STATE); PMUTs (tabulated coupling), a plane wave and
  * an interface between two curved boxes (the general one of sem_dg_interface_build) are attached
  * afterwards; world 1 only (SEM_E_PARTITION).  Caller owns `verts` (copied).  Errors: SEM_E_ARG (size, non-positive
  * Jacobian at a GLL point), SEM_E_STATE, SEM_E_OOM. */
@@ -257,7 +257,12 @@ sem_status sem_face_match(int device, const sem_face_set* fine, const sem_face_s
 /* Incident plane wave entering through absorbing face `face` (only 5 = +z) of `box`
  * (reading R13): p_inc = amp s(t - k.(x - x_ref)/c), s(u) = exp(-(u-t0)^2/(2 sigma^2))
  * sin(2 pi f0 (u-t0)), imposed as total-field first-order ABC data
- * b_j = int c amp s'(tau) (1 - n.k) psi_j.  dir is the unit propagation direction k. */
+ * b_j = int c amp s'(tau) (1 - n.k) psi_j.  dir is the unit propagation direction k.
+ * On a curved box (sem_box_set_vertices first; every box of the context on the element-scatter path,
+ * SEM_E_STATE otherwise) the load is tabulated per face node with the trilinear faces' weights
+ * w_a w_b |J_s| and physical node positions; the +z face must be planar (SEM_E_ARG), x_ref is the
+ * first-hit corner of its bounding rectangle.
+ * Errors: SEM_E_ARG (face, non-absorbing face, parameters), SEM_E_STATE. */
 sem_status sem_plane_wave_source(sem_ctx* ctx, int box, int face, double amp_pa, double f0_hz,
                                  double sigma_s, double t0_s, const double dir[3]);
 

@@ -2113,6 +2113,14 @@ int curved_grid(int N, int nel) {
     return (int)(g < groups ? g : (groups > 0 ? groups : 1));
 }
 
+// b_j(t) = pwf_j s'(tau_j - t0), s(u) = exp(-u^2 / (2 sigma^2)) sin(om u), tau_j = t - pwd_j (reading R13)
+__device__ __forceinline__ double curved_pw_load(const CurvedParams& p, double t1, long long j) {
+    const double u = t1 - __ldg(p.pwd + j) - p.pw_t0;
+    double sn, cs;
+    sincos(p.pw_om * u, &sn, &cs);
+    return __ldg(p.pwf + j) * (exp(-0.5 * u * u * p.pw_is2) * (-u * p.pw_is2 * sn + p.pw_om * cs));
+}
+
 // Nodal kick-drift of a curved box as one flat stream over the padded lattice (16-byte accesses,
 // grid-stride over 8 resident blocks per SM -- the register cap keeps all of them resident, a second
 // wave of blocks would double the time): pad entries carry minv = cdamp = res = 0 and w = p = 0.
@@ -2139,6 +2147,12 @@ __global__ void __launch_bounds__(256, 8) curved_update_kernel(const __grid_cons
             const long long d = 2 * i, ix = d % p.PX, iy = d / p.PX;   // PX even: both nodes on one row
             if (ix < p.NX) r.x -= __ldg(p.F + iy * p.NX + ix) * __ldg(p.fmx + ix) * __ldg(p.fmy + iy);
             if (ix + 1 < p.NX) r.y -= __ldg(p.F + iy * p.NX + ix + 1) * __ldg(p.fmx + ix + 1) * __ldg(p.fmy + iy);
+        }
+        if (p.pwd && 2 * i >= p.PX * p.NY * (p.NZ - 1)) {   // top plane: incident plane wave load (R13)
+            const long long d = 2 * i - p.PX * p.NY * (p.NZ - 1), ix = d % p.PX, iy = d / p.PX;
+            const double t1 = (double)(__ldcg(p.step) + 1) * p.dt;
+            if (ix < p.NX) r.x -= curved_pw_load(p, t1, iy * p.NX + ix);
+            if (ix + 1 < p.NX) r.y -= curved_pw_load(p, t1, iy * p.NX + ix + 1);
         }
         double2 wn, pn;
         wn.x = fma(p.dt, -mi.x * r.x - cd.x * wv.x, wv.x);

@@ -633,6 +633,14 @@ sem::CurvedParams curved_params(sem_ctx* ctx, sem::Part& pt, int bi, int cur) {
     p.c2 = b.d.c * b.d.c;
     p.dt = ctx->dt;
     p.inv_dt = 1.0 / ctx->dt;
+    if (ctx->pw.on && ctx->pw.box == bi && b.pwd) {
+        p.pwd = b.pwd;
+        p.pwf = b.pwf;
+        p.step = ctx->d_step;
+        p.pw_t0 = ctx->pw.t0;
+        p.pw_is2 = 1.0 / (ctx->pw.sigma * ctx->pw.sigma);
+        p.pw_om = 2.0 * M_PI * ctx->pw.f0;
+    }
     if (pt.pm.on && pt.pm.box == bi && !pt.pm.toff) {   // affine obstacle box: separable coupling
         p.F = pt.pm.F;
         p.fmx = b.mx;
@@ -1253,6 +1261,80 @@ sem_status pmut_tables(sem_ctx* ctx, sem::Part& pt, Box& b, const sem_pmut_desc&
         if (off[l + 1] == off[l]) return fail(ctx, SEM_E_ARG, "membrane with no face node");
     }
     if (upload(ctx, &pt.pm.toff, off) || upload(ctx, &pt.pm.tidx, idx) || upload(ctx, &pt.pm.tB, B)) return SEM_E_CUDA;
+    return SEM_OK;
+}
+
+// Incident plane wave on the +z face of a curved box (reading R13 on a vertex lattice): per top-face
+// node the assembled face weight W_j = sum_F w_a w_b |J_s| and the physical position from the trilinear
+// maps of the top element layer; x_ref = the corner of the face's bounding rectangle the wavefront
+// reaches first; tables pwd_j = k.(x_j - x_ref)/c and pwf_j = c A (1 - n.k) W_j.  The face must be planar
+// (n = +z), as the boxes' faces are in every supported configuration.
+sem_status curved_plane_wave(sem_ctx* ctx, Box& b, double amp, const double kk[3]) {
+    const sem_box_desc& g = b.d;
+    const int N = b.N;
+    std::vector<double> x, w;
+    gll_rule(N, x, w);
+    const long long nx = g.nel[0] + 1, ny = g.nel[1] + 1;
+    const size_t nn = (size_t)b.NX * b.NY;
+    std::vector<double> fw(nn, 0.0), fx(nn), fy(nn), fz(nn);
+    const int ez = g.nel[2] - 1;
+    for (int ey = 0; ey < g.nel[1]; ++ey)
+        for (int ex = 0; ex < g.nel[0]; ++ex) {
+            double V[24];
+            for (int v = 0; v < 8; ++v) {
+                const long long vx = ex + (v & 1), vy = ey + ((v >> 1) & 1), vz = ez + (v >> 2);
+                for (int i = 0; i < 3; ++i) V[3 * v + i] = b.vlat_h[3 * (vx + nx * (vy + ny * vz)) + i];
+            }
+            for (int bb = 0; bb <= N; ++bb)
+                for (int a = 0; a <= N; ++a) {
+                    const double xi[3] = {x[a], x[bb], 1.0};
+                    double J[3][3];
+                    trilinear_jacobian(V, xi, J);
+                    const double cx = J[1][0] * J[2][1] - J[2][0] * J[1][1], cy = J[2][0] * J[0][1] - J[0][0] * J[2][1],
+                                 cz = J[0][0] * J[1][1] - J[1][0] * J[0][1];
+                    double X[3] = {0, 0, 0};
+                    for (int v = 0; v < 8; ++v) {
+                        const double sh = 0.125 * (1.0 + ((v & 1) ? 1 : -1) * xi[0]) * (1.0 + ((v & 2) ? 1 : -1) * xi[1]) *
+                                          (1.0 + ((v & 4) ? 1 : -1) * xi[2]);
+                        for (int i = 0; i < 3; ++i) X[i] += sh * V[3 * v + i];
+                    }
+                    const size_t j = (size_t)(N * ey + bb) * b.NX + (N * ex + a);
+                    fw[j] += w[a] * w[bb] * std::sqrt(cx * cx + cy * cy + cz * cz);
+                    fx[j] = X[0];
+                    fy[j] = X[1];
+                    fz[j] = X[2];
+                }
+        }
+    double lo[2] = {1e300, 1e300}, hi[2] = {-1e300, -1e300}, zmin = 1e300, zmax = -1e300;
+    for (size_t j = 0; j < nn; ++j) {
+        lo[0] = std::min(lo[0], fx[j]);
+        hi[0] = std::max(hi[0], fx[j]);
+        lo[1] = std::min(lo[1], fy[j]);
+        hi[1] = std::max(hi[1], fy[j]);
+        zmin = std::min(zmin, fz[j]);
+        zmax = std::max(zmax, fz[j]);
+    }
+    if (zmax - zmin > 1e-9 * std::max(hi[0] - lo[0], hi[1] - lo[1]))
+        return fail(ctx, SEM_E_ARG, "plane wave on a curved box: the +z face must be planar");
+    double best = std::numeric_limits<double>::infinity();
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) {
+            const double cxr = i ? hi[0] : lo[0], cyr = j ? hi[1] : lo[1];
+            const double kx = kk[0] * cxr + kk[1] * cyr + kk[2] * fz[0];
+            if (kx < best) {
+                best = kx;
+                ctx->pw_xref_curved[0] = cxr;
+                ctx->pw_xref_curved[1] = cyr;
+                ctx->pw_xref_curved[2] = fz[0];
+            }
+        }
+    std::vector<double> dl(nn), fc(nn);
+    for (size_t j = 0; j < nn; ++j) {
+        dl[j] = (kk[0] * (fx[j] - ctx->pw_xref_curved[0]) + kk[1] * (fy[j] - ctx->pw_xref_curved[1]) +
+                 kk[2] * (fz[j] - ctx->pw_xref_curved[2])) / g.c;
+        fc[j] = g.c * amp * (1.0 - kk[2]) * fw[j];
+    }
+    if (upload(ctx, &b.pwd, dl) || upload(ctx, &b.pwf, fc)) return SEM_E_CUDA;
     return SEM_OK;
 }
 
@@ -1986,10 +2068,17 @@ sem_status sem_plane_wave_source(sem_ctx* ctx, int box, int face, double amp, do
         return fail(ctx, SEM_E_ARG, "plane wave: +z face of an existing box only");
     const sem_box_desc& g = ctx->gdesc[box];
     if (g.bc[5] != SEM_BC_ABSORBING) return fail(ctx, SEM_E_ARG, "plane wave needs an absorbing face");
-    for (auto& pt : ctx->parts)
-        if (pt.boxes[box].curved) return fail(ctx, SEM_E_STATE, "a plane wave on a curved box is not supported");
     const double nk = std::sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
     if (!(nk > 0) || !(sigma > 0)) return fail(ctx, SEM_E_ARG, "bad plane-wave parameters");
+    if (ctx->parts[0].boxes[box].curved) {
+        // element-scatter box: the load is tabulated per top-face node from the vertex lattice
+        for (auto& b : ctx->parts[0].boxes)
+            if (!b.curved) return fail(ctx, SEM_E_STATE, "a plane wave on a curved box needs every box on the element-scatter path");
+        double kk[3];
+        for (int k = 0; k < 3; ++k) kk[k] = dir[k] / nk;
+        st = curved_plane_wave(ctx, ctx->parts[0].boxes[box], amp, kk);
+        if (st) return st;
+    }
     sem::PlaneWave& pw = ctx->pw;
     pw.box = box;
     pw.amp = amp;
@@ -2012,6 +2101,8 @@ sem_status sem_plane_wave_source(sem_ctx* ctx, int box, int face, double amp, do
                 pw.xref[2] = zt;
             }
         }
+    if (ctx->parts[0].boxes[box].curved)
+        for (int k = 0; k < 3; ++k) pw.xref[k] = ctx->pw_xref_curved[k];
     pw.on = true;
     drop_graphs(ctx);
     return SEM_OK;

@@ -275,6 +275,13 @@ struct CurvedParams {
     const double* __restrict__ F;    // [NY][NX] or nullptr
     const double* __restrict__ fmx;  // [NX] face mass factors
     const double* __restrict__ fmy;  // [NY]
+    // incident plane wave on the planar +z face (reading R13): the update subtracts b_j(t^{n+1}) =
+    // pwf_j s'(t^{n+1} - pwd_j - t0) from the residual of the top-plane nodes; pwf_j = c A (1 - n.k) W_j
+    // (W_j the assembled face weight w_a w_b |J_s|), pwd_j = k.(x_j - x_ref)/c (host tables)
+    const double* __restrict__ pwd;  // [NY][NX] or nullptr
+    const double* __restrict__ pwf;  // [NY][NX]
+    const long long* __restrict__ step;
+    double pw_t0, pw_is2, pw_om;
 };
 
 // General non-conforming SIPG interface between two element-scatter boxes (curved vertex lattices):
@@ -355,6 +362,8 @@ struct Box {
     double* cdamp = nullptr;  // pitched: C_ii / M_ii on absorbing faces, 0 elsewhere
     double* res = nullptr;    // pitched: assembled K p residual (atomics), cleared by the update
     unsigned char* solid = nullptr;            // [nel] obstacle elements (nullptr: none)
+    double* pwd = nullptr;    // plane wave on a curved box: per top-face node delay and factor
+    double* pwf = nullptr;
     std::vector<double> vlat_h;                // host copy of the vertex lattice
     bool verts_set = false;                    // sem_box_set_vertices called (else affine lattice)
     std::vector<unsigned char> solid_h;        // host copy of the obstacle mask (empty: none)
@@ -446,6 +455,7 @@ struct sem_ctx {
     std::vector<std::vector<int>> pm_lists;        // global PMUT indices per slab
     bool itf_on = false;
     sem::PlaneWave pw;
+    double pw_xref_curved[3] = {0, 0, 0};   // x_ref of a plane wave on a curved box (set by curved_plane_wave)
     int cur = 0;                 // P[cur] = p^{step+1}, P[1-cur] = p^{step}
     long long step = 0;          // host mirror of the device counter
     long long* d_step = nullptr;
