@@ -1,7 +1,8 @@
 """Every kernel family on small cases, for the bounds-checked build (SEM_LIB=.../libsem_debug.so):
 PMUT (cfg 0), 2:1 interface (fused and generic, both quadrature rules), RX + plane wave (cfg 4s), PML
 (also under 2 slabs), curved box, obstacle, emulated slab decompositions (even and uneven), face
-matching, the general interface, PMUTs on curved and obstacle boxes.  Prints "debug run ok"."""
+matching, the general interface, PMUTs on curved and obstacle boxes, the two-box cylinder (caller-defined
+shapes, plane wave on a curved box).  Prints "debug run ok"."""
 import os
 import sys
 
@@ -9,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_06267_b200 import LIB_PATH, SEM_F_EMULATE_SLABS, Simulation, sem_face_match  # noqa: E402
 from sem_inputs import (conforming_cut_config, config, curved_config, curved_interface_config,  # noqa: E402
                         curved_pmut_config, interface_faces, obstacle_config, obstacle_pmut_config, pml_config,
-                        random_state, small_config)
+                        random_state, small_config, cylinder_two_box_config, plane_wave_source)
 
 print("library:", LIB_PATH)
 cases = [(config(0), {}), (small_config("cfg2s"), {}), (small_config("cfg4s"), {}),
@@ -21,6 +22,9 @@ cases = [(config(0), {}), (small_config("cfg2s"), {}), (small_config("cfg4s"), {
          (curved_interface_config(jitter=0.15, seed=3), {}), (curved_pmut_config(), {}),
          (obstacle_pmut_config(), {}), (config(1), {"world": 4, "flags": SEM_F_EMULATE_SLABS}),
          (pml_config(nel=(3, 6, 3), degree=3, layers=(1, 1, 1, 1, 0, 1), layer_el=1), {"world": 2, "flags": SEM_F_EMULATE_SLABS})]
+cyl = cylinder_two_box_config()          # circular membrane (shape_fn), general interface, plane wave on a curved box
+cyl["plane_wave"] = plane_wave_source(1, deg=20.0, azimuth_deg=30.0)
+cases.append((cyl, {}))
 for rec, kw in cases:
     sim = Simulation(rec, **kw)
     st = random_state(rec, seed=1)
