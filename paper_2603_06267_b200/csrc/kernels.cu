@@ -2121,6 +2121,17 @@ __device__ __forceinline__ double curved_pw_load(const CurvedParams& p, double t
     return __ldg(p.pwf + j) * (exp(-0.5 * u * u * p.pw_is2) * (-u * p.pw_is2 * sn + p.pw_om * cs));
 }
 
+// Incident plane wave on a curved box's top plane: res_j -= b_j(t^{n+1}) before the nodal update (a kernel
+// of its own: inside curved_update_kernel the sincos / exp path doubled that kernel's spills under its
+// 32-register cap and cost 4% of the curved step)
+__global__ void __launch_bounds__(256) curved_pw_kernel(const __grid_constant__ CurvedParams p) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= p.NX * p.NY) return;
+    const double t1 = (double)(__ldcg(p.step) + 1) * p.dt;
+    const long long ix = j % p.NX, iy = j / p.NX;
+    p.res[(p.NY * (p.NZ - 1) + iy) * p.PX + ix] -= curved_pw_load(p, t1, j);
+}
+
 // Nodal kick-drift of a curved box as one flat stream over the padded lattice (16-byte accesses,
 // grid-stride over 8 resident blocks per SM -- the register cap keeps all of them resident, a second
 // wave of blocks would double the time): pad entries carry minv = cdamp = res = 0 and w = p = 0.
@@ -2148,12 +2159,6 @@ __global__ void __launch_bounds__(256, 8) curved_update_kernel(const __grid_cons
             if (ix < p.NX) r.x -= __ldg(p.F + iy * p.NX + ix) * __ldg(p.fmx + ix) * __ldg(p.fmy + iy);
             if (ix + 1 < p.NX) r.y -= __ldg(p.F + iy * p.NX + ix + 1) * __ldg(p.fmx + ix + 1) * __ldg(p.fmy + iy);
         }
-        if (p.pwd && 2 * i >= p.PX * p.NY * (p.NZ - 1)) {   // top plane: incident plane wave load (R13)
-            const long long d = 2 * i - p.PX * p.NY * (p.NZ - 1), ix = d % p.PX, iy = d / p.PX;
-            const double t1 = (double)(__ldcg(p.step) + 1) * p.dt;
-            if (ix < p.NX) r.x -= curved_pw_load(p, t1, iy * p.NX + ix);
-            if (ix + 1 < p.NX) r.y -= curved_pw_load(p, t1, iy * p.NX + ix + 1);
-        }
         double2 wn, pn;
         wn.x = fma(p.dt, -mi.x * r.x - cd.x * wv.x, wv.x);
         wn.y = fma(p.dt, -mi.y * r.y - cd.y * wv.y, wv.y);
@@ -2177,6 +2182,7 @@ void launch_curved(const CurvedParams& p, cudaStream_t s) {
 #undef SEM_CV_CASE
         default: break;
     }
+    if (p.pwd) curved_pw_kernel<<<(unsigned)((p.NX * p.NY + 255) / 256), 256, 0, s>>>(p);
     const long long n2 = p.PX * p.NY * p.NZ / 2;
     const long long want = (n2 + 255) / 256, cap = 8LL * device_sms();
     curved_update_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(p);

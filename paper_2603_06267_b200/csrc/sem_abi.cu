@@ -845,8 +845,9 @@ int enqueue_step(sem_ctx* ctx, int cur, bool prof) {
         for (auto& pt : ctx->parts)
             for (int bi = 0; bi < (int)pt.boxes.size(); ++bi)
                 if (pt.boxes[bi].curved) {
-                    sem::launch_curved(curved_params(ctx, pt, bi, cur), s);
-                    nl += 2;
+                    const sem::CurvedParams cp = curved_params(ctx, pt, bi, cur);
+                    sem::launch_curved(cp, s);
+                    nl += cp.pwd ? 3 : 2;
                 }
         if (ls.empty()) {
             sem::launch_step_bump(ctx->d_step, s);
