@@ -12,5 +12,5 @@ from .workloads import (  # noqa: F401
     config, config_names, small_config, small_config_names,
     random_state, n_nodes, box_dof, total_dof, cavity_config, conforming_cut_config, pml_config,
     interface_faces, curved_config, obstacle_config, solid_block, obstacle_pmut_config,
-    curved_interface_config, curved_pmut_config, clamped_disc_shape, circular_pmut_config, cylinder_pmut_config, cylinder_two_box_config, plane_wave_source,
+    curved_interface_config, curved_pmut_config, clamped_disc_shape, circular_pmut_config, cylinder_pmut_config, cylinder_two_box_config, cylinder_obstacle_config, plane_wave_source,
 )

@@ -118,3 +118,25 @@ def test_cylinder_two_box_geometry_and_stability():
         lam = np.linalg.norm(w) / np.linalg.norm(v)
         v = w / np.linalg.norm(w)
     assert rec["dt"] * math.sqrt(lam) / 2 < 0.67, rec["dt"] * math.sqrt(lam) / 2
+
+
+def test_cylinder_obstacle_fluid_volume():
+    """Section 6.2's cylinder with its rounded rigid slab: the lumped mass (fluid only) sums to the column's
+    volume minus the slab's -- both extruded polygons (shoelace areas of the mapped boundary rings)."""
+    from sem_inputs import cylinder_obstacle_config
+
+    def shoelace(ring):
+        return 0.5 * abs(np.sum(ring[:, 0] * np.roll(ring[:, 1], -1) - np.roll(ring[:, 0], -1) * ring[:, 1]))
+
+    rec = cylinder_obstacle_config(n_steps=1)
+    b = rec["boxes"][0]
+    nx, ny, nz = b["nel"]
+    V = b["vertices"].reshape(nz + 1, ny + 1, nx + 1, 3)[0, :, :, :2]
+    outer = np.concatenate([V[0, :-1], V[:-1, -1], V[-1, :0:-1], V[:0:-1, 0]])
+    B = V[1:ny, 1:nx]                                     # vertices of the 6 x 6 central element block
+    inner = np.concatenate([B[0, :-1], B[:-1, -1], B[-1, :0:-1], B[:0:-1, 0]])
+    hz = b["extent"][2] / nz
+    vol = shoelace(outer) * b["extent"][2] - shoelace(inner) * hz
+    s = System(rec)
+    assert abs(s.M.sum() - vol) < 1e-12 * vol
+    assert 0.55 < shoelace(inner) / shoelace(outer) < 0.8   # (6/8)^2-ish of the section: ~5/6 of the diameter
